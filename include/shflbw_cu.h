@@ -1,0 +1,199 @@
+/*
+ * shflbw_cu.h -- C ABI of the B200-native Shfl-BW hot path.
+ *
+ * Plain pointers and sizes only; every entry point is stream-ordered on the
+ * cudaStream_t passed as `stream` (NULL = legacy default stream).  Device
+ * pointers are marked [dev], host pointers [host].  All calls return a
+ * status code; shflbw_cu_last_error() gives the thread-local message of the
+ * last failure.  There is no CPU fallback: without a usable sm_100 device
+ * every compute entry point returns SHFLBW_CUDA_ERROR.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj, see INTEGRATION.md for the binding a maintainer
+ * adds on the reference side).
+ *
+ * Status codes map 1:1 onto the reference's exception classes
+ * (include/shflbw/errors.hpp:9-40).
+ */
+#ifndef SHFLBW_CU_H
+#define SHFLBW_CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* shflbw_stream_t; /* == cudaStream_t */
+
+enum shflbw_status {
+    SHFLBW_OK = 0,
+    SHFLBW_SHAPE_MISMATCH = 1,     /* shflbw::ShapeMismatch     */
+    SHFLBW_NONCONFORMANT_MASK = 2, /* shflbw::NonConformantMask */
+    SHFLBW_BAD_PARAMS = 3,         /* shflbw::BadParams         */
+    SHFLBW_BAD_GEOMETRY = 4,       /* shflbw::BadGeometry       */
+    SHFLBW_CUDA_ERROR = 5,         /* shflbw::Error (runtime)   */
+    SHFLBW_UNSUPPORTED = 6         /* shflbw::Error (no kernel for this case) */
+};
+
+enum shflbw_dtype { SHFLBW_F32 = 0, SHFLBW_BF16 = 1, SHFLBW_F16 = 2 };
+
+/* kPadColumn (include/shflbw/formats.hpp:109, 0xffffffff) as int32. */
+#define SHFLBW_PAD_COLUMN (-1)
+/* Every group's column list is padded to a multiple of this (the SpMM
+ * kernel's K block); padding follows stitch_to_blockwise
+ * (src/formats.cpp:221-250): index SHFLBW_PAD_COLUMN, value 0. */
+#define SHFLBW_K_TILE 64
+
+/*
+ * Device-resident Shfl-BW matrix: the reference's ShflBWMatrix
+ * (include/shflbw/formats.hpp:14-42) with each group's column-major V x n_g
+ * value block stored contiguously (values[(group_ptr[g] + j) * v + r] is row r
+ * of group g at column col_idx[group_ptr[g] + j]) and 16-bit values.
+ */
+typedef struct shflbw_cu_matrix {
+    int32_t rows;        /* M (K_f for conv weights)                      */
+    int32_t cols;        /* K (C*R*S for conv weights)                    */
+    int32_t v;           /* V, rows per group                             */
+    int32_t groups;      /* G = M / V                                     */
+    int32_t dtype;       /* SHFLBW_BF16 / SHFLBW_F16; SHFLBW_F32 = storage
+                            only (exact host round trips), not computable */
+    int32_t k_tile;      /* SHFLBW_K_TILE                                 */
+    int64_t total_cols;  /* group_ptr[groups]                             */
+    int32_t* row_indices; /* [dev] M: compressed row r -> original row    */
+    int32_t* group_ptr;   /* [dev] G+1: padded column offsets              */
+    int32_t* group_ncols; /* [dev] G: n_g (unpadded)                       */
+    int32_t* col_idx;     /* [dev] total_cols, SHFLBW_PAD_COLUMN padding   */
+    void* values;         /* [dev] total_cols * v 16-bit values            */
+    int32_t device;       /* CUDA device ordinal                           */
+    int32_t owns;         /* 1: free with shflbw_cu_matrix_free            */
+} shflbw_cu_matrix;
+
+/* ---- library ---------------------------------------------------------- */
+const char* shflbw_cu_last_error(void);
+int shflbw_cu_version(void);
+/* Tuning / testing knobs.  Keys: "force_simt" (1: use the CUDA-core kernel
+ * for every V), "split" (cluster split of V for the tcgen05 kernel, 0 =
+ * auto), "stages" (pipeline depth, 0 = auto).  Unknown key: BAD_PARAMS. */
+int shflbw_cu_set_option(const char* key, int64_t value);
+/* Number of kernels this library launched on the calling thread so far. */
+int64_t shflbw_cu_launch_count(void);
+
+/* ---- converter (replaces validate_pattern(ShflBW), src/formats.cpp:113-138,
+ *      and compress_shflbw, include/shflbw/formats.hpp:98-99 /
+ *      src/formats.cpp:140-181) ------------------------------------------- */
+
+/* mask [dev] M*K bytes, each 0 or 1.  *pass = 1/0; *fail_row = smallest row of
+ * the lexicographically first support class whose size is not a multiple of
+ * V.  BAD_PARAMS if V == 0, V does not divide M, or a mask byte > 1.
+ * Synchronises `stream`. */
+int shflbw_cu_validate(const uint8_t* mask, int32_t M, int32_t K, int32_t V,
+                       int32_t* pass, uint32_t* fail_row, shflbw_stream_t stream);
+
+/* dense [dev] M*K of dense_dtype, mask [dev] M*K bytes.  Builds *out (device
+ * buffers owned by the library) with values rounded to value_dtype (RNE;
+ * F32 keeps them exact).
+ * NONCONFORMANT_MASK sets *fail_row.  Synchronises `stream` once (sizes). */
+int shflbw_cu_compress(const void* dense, int32_t dense_dtype, const uint8_t* mask,
+                       int32_t M, int32_t K, int32_t V, int32_t value_dtype,
+                       shflbw_cu_matrix* out, uint32_t* fail_row,
+                       shflbw_stream_t stream);
+
+void shflbw_cu_matrix_free(shflbw_cu_matrix* m);
+
+/* Host ShflBWMatrix (flattened: row_indices[M], group_ncols[G], cols[sum n_g],
+ * values[V*sum n_g] f32) -> device layout.  ShapeMismatch on a row index >= M
+ * or a column >= K (the reference checks the former in spmm_execute,
+ * src/spmm.cpp:82-86, and the latter in stitch_tile, src/spmm.cpp:50-52). */
+int shflbw_cu_matrix_upload(int32_t M, int32_t K, int32_t V,
+                            const uint32_t* row_indices, const uint32_t* group_ncols,
+                            const uint32_t* cols, const float* values,
+                            int32_t value_dtype, shflbw_cu_matrix* out,
+                            shflbw_stream_t stream);
+
+/* Device layout -> host flattened ShflBWMatrix (values widened to f32).
+ * cols / values capacity: sum n_g and V*sum n_g.  Synchronises `stream`. */
+int shflbw_cu_matrix_download(const shflbw_cu_matrix* m, uint32_t* row_indices,
+                              uint32_t* group_ncols, uint32_t* cols, float* values,
+                              shflbw_stream_t stream);
+
+/* The raw device layout -> host: group_ptr[G+1], col_idx[total_cols],
+ * values[total_cols * V] as raw 2-byte (BF16/F16) or 4-byte (F32) words (for
+ * layout checks and serialisers).
+ * Synchronises `stream`. */
+int shflbw_cu_matrix_export_raw(const shflbw_cu_matrix* m, int32_t* group_ptr, int32_t* col_idx,
+                                uint16_t* values, shflbw_stream_t stream);
+
+/* decompress(ShflBWMatrix), src/formats.cpp:195-206: dense [dev] M*K f32. */
+int shflbw_cu_decompress(const shflbw_cu_matrix* m, float* dense, shflbw_stream_t stream);
+
+/* ---- SpMM (replaces spmm_execute, include/shflbw/spmm.hpp:28-29 /
+ *      src/spmm.cpp:76-146) ---------------------------------------------- */
+
+/* C[row_indices[g*V+r]][n] = sum_j values[g][j][r] * B[col_idx[g][j]][n].
+ * B [dev] K_b x N, row stride ldb elements, dtype == a->dtype.
+ * C [dev] M x N, row stride ldc, c_dtype F32 or BF16/F16.
+ * ShapeMismatch if K_b != a->cols.  Asynchronous. */
+int shflbw_cu_spmm(const shflbw_cu_matrix* a, const void* B, int32_t K_b, int32_t N,
+                   int64_t ldb, void* C, int32_t c_dtype, int64_t ldc,
+                   shflbw_stream_t stream);
+
+/* One shard's share: groups [g_begin, g_end) (the reference's per-worker
+ * run_groups range, src/spmm.cpp:93-144).  compact = 0 writes through
+ * row_indices into the full C; compact = 1 writes group-ordered rows
+ * C[(g - g_begin)*V + r] (input of an all-gather + shflbw_cu_unpermute_rows). */
+int shflbw_cu_spmm_groups(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_end,
+                          const void* B, int32_t K_b, int32_t N, int64_t ldb, void* C,
+                          int32_t c_dtype, int64_t ldc, int32_t compact,
+                          shflbw_stream_t stream);
+
+/* C[row_indices[r]][:] = C_perm[r][:] for r < M (2- or 4-byte elements). */
+int shflbw_cu_unpermute_rows(const int32_t* row_indices, int32_t M, int32_t N,
+                             const void* C_perm, int64_t ld_perm, void* C, int64_t ldc,
+                             int32_t dtype, shflbw_stream_t stream);
+
+/* ---- sparse convolution (replaces conv2d, include/shflbw/spmm.hpp:87-89 /
+ *      src/spmm.cpp:193-291, and conv_output_size, src/spmm.cpp:177-191) ---- */
+
+int shflbw_cu_conv_output_size(int32_t H, int32_t W, int32_t R, int32_t S,
+                               int32_t stride, int32_t pad, int32_t* P, int32_t* Q);
+
+/* input [dev] [C][H][W][Nb] (dtype == w->dtype); out [dev] [K_f][P][Q][Nb] of
+ * out_dtype.  Weights are K_f x C*R*S; column c decodes to
+ * (c / (R*S), (c % (R*S)) / S, c % S).  BadGeometry as the reference. */
+int shflbw_cu_conv2d(const shflbw_cu_matrix* w, const void* input, int32_t C, int32_t H,
+                     int32_t W, int32_t Nb, int32_t R, int32_t S, int32_t stride,
+                     int32_t pad, void* out, int32_t out_dtype, shflbw_stream_t stream);
+
+/* ---- the reference's public helpers, on the device ------------------------ */
+
+/* spmm_dense_oracle (src/spmm.cpp:148-161): C = A*B, fp32, each product
+ * rounded then added, k ascending (bit-identical to the reference loop).
+ * A [dev] MxK, B [dev] KxN, C [dev] MxN. */
+int shflbw_cu_dense_matmul_f32(const float* A, int32_t M, int32_t K, const float* B, int32_t N,
+                               float* C, shflbw_stream_t stream);
+
+/* stitch_tile (src/spmm.cpp:37-58): staging [dev] t_k x t_n row-major gets
+ * the rows of B [dev] named by group_cols[chunk_begin..+t_k) [dev], zero past
+ * the list or B's edge; ShapeMismatch if a named row >= B_rows (synchronises). */
+int shflbw_cu_stitch_tile(const uint32_t* group_cols, int64_t ncols, int64_t chunk_begin,
+                          int64_t t_k, const float* B, int32_t B_rows, int32_t B_cols,
+                          int64_t slice_begin, int64_t t_n, float* staging,
+                          shflbw_stream_t stream);
+
+/* tile_mma (src/spmm.cpp:60-74): acc [dev] v_rows x t_n += a_tile (column-major
+ * v_rows x k_len) * b_tile (k_len x t_n), products added one k at a time. */
+int shflbw_cu_tile_mma(float* acc, const float* a_tile, const float* b_tile, int64_t v_rows,
+                       int64_t k_len, int64_t t_n, shflbw_stream_t stream);
+
+/* ---- utilities ---------------------------------------------------------- */
+
+/* dst[i] = (dst_dtype) src[i], RNE; src_dtype/dst_dtype any of F32/BF16/F16. */
+int shflbw_cu_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype,
+                      int64_t n, shflbw_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHFLBW_CU_H */

@@ -1,0 +1,17 @@
+"""B200-native Shfl-BW (arXiv 2203.05016) sparse linear / conv hot path.
+
+The product is ``lib/libshflbw_b200.so``: hand-written sm_100a kernels
+(tcgen05 + TMEM + TMA gather4) behind the C ABI of ``include/shflbw_cu.h``
+and the reference-compatible C++ API of ``include/shflbw/``.  This Python
+package is a thin host mirror of the reference interface over that ABI
+(``shflbw``) plus the multi-GPU row-group sharding (``sharded``).
+"""
+from .shflbw import (BadGeometry, BadParams, ConvGeometry, Error, NonConformantMask, ShapeMismatch,
+                     ShflBWMatrix, TileConfig, compress_shflbw, conv2d, conv_output_size, decompress,
+                     launch_count, set_option, spmm_execute, spmm_groups, unpermute_rows, upload,
+                     validate_pattern)
+
+__all__ = ["BadGeometry", "BadParams", "ConvGeometry", "Error", "NonConformantMask", "ShapeMismatch",
+           "ShflBWMatrix", "TileConfig", "compress_shflbw", "conv2d", "conv_output_size", "decompress",
+           "launch_count", "set_option", "spmm_execute", "spmm_groups", "unpermute_rows", "upload",
+           "validate_pattern"]

@@ -1,0 +1,857 @@
+// convert.cu -- K1: Shfl-BW format converter on the GPU.
+//
+// Replaces validate_pattern(ShflBW) + compress_shflbw
+// (/root/reference/proj/src/formats.cpp:85-93, 113-125, 140-181).
+//
+// The reference groups rows by exact mask-row equality with a std::map keyed
+// by the whole row (src/formats.cpp:40-46), cuts each class into V-row chunks
+// of ascending rows and orders the chunks by first row.  Here:
+//
+//   1. k_pack_rows   one warp per row: the mask row becomes 64-bit words with
+//                    column 0 as the MSB of word 0 (so unsigned word order is
+//                    the reference's lexicographic byte order), plus popcount
+//                    and a 64-bit hash; bytes > 1 are flagged (SparsityMask's
+//                    constructor rejects them, src/matrix.cpp:24-31).
+//   2. radix sort    stable LSD sort of (hash, row) pairs: equal rows become
+//                    runs, rows ascending inside a run.
+//   3. k_runs        run bounds by binary search; adjacent rows of a run are
+//                    compared word by word -- a hash collision is detected
+//                    exactly and the host retries with another seed, so the
+//                    grouping is exact, not probabilistic.
+//   4. groups        leaders = run positions whose rank is a multiple of V; an
+//                    exclusive scan over rows numbers them by first row, which
+//                    is the reference's group order.
+//   5. packing       per group: column list = set bits of the leader row,
+//                    padded with kPadColumn to a multiple of SHFLBW_K_TILE;
+//                    values gathered, rounded to bf16/fp16 (RNE) and written
+//                    column-major (V contiguous) through a shared-memory tile.
+//
+// A failing class is reported like the reference: the lexicographically
+// smallest failing support class (word-wise argmin over run heads) gives its
+// smallest row as fail_row.
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace sbw {
+
+namespace {
+
+constexpr int kRadixTile = 2048;  // items per block (256 threads x 8)
+constexpr int kScanTile = 2048;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t word_hash(uint64_t word, int w, uint64_t seed) {
+    return mix64(word + mix64(seed ^ (0x9E3779B97F4A7C15ULL * static_cast<uint64_t>(w + 1))));
+}
+
+// flags[0]: mask byte > 1, flags[1]: hash collision, flags[2]: failing class,
+// flags[3]: upload range error
+__global__ void k_pack_rows(const uint8_t* __restrict__ mask, int M, int K, int W,
+                            uint64_t seed, uint64_t* __restrict__ words,
+                            int* __restrict__ popc, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals, uint32_t* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (r >= M) return;
+    const uint8_t* row = mask + static_cast<int64_t>(r) * K;
+    uint64_t h = 0;
+    int pc = 0;
+    bool bad = false;
+    for (int w = 0; w < W; ++w) {
+        const int c0 = w * 64;
+        const uint8_t b0 = (c0 + lane < K) ? row[c0 + lane] : 0;
+        const uint8_t b1 = (c0 + 32 + lane < K) ? row[c0 + 32 + lane] : 0;
+        bad |= (b0 > 1) | (b1 > 1);
+        const uint32_t hi = __brev(__ballot_sync(0xffffffffu, b0 != 0));
+        const uint32_t lo = __brev(__ballot_sync(0xffffffffu, b1 != 0));
+        const uint64_t word = (static_cast<uint64_t>(hi) << 32) | lo;
+        if (lane == (w & 31)) words[static_cast<int64_t>(r) * W + w] = word;
+        pc += __popc(hi) + __popc(lo);
+        h += word_hash(word, w, seed);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags[0], 1u);
+    if (lane == 0) {
+        popc[r] = pc;
+        keys[r] = h;
+        vals[r] = static_cast<uint32_t>(r);
+    }
+}
+
+// Re-hash with another seed (collision retry): one warp per row.
+__global__ void k_hash_rows(const uint64_t* __restrict__ words, int M, int W, uint64_t seed,
+                            uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (r >= M) return;
+    uint64_t h = 0;
+    for (int w = lane; w < W; w += 32) h += word_hash(words[static_cast<int64_t>(r) * W + w], w, seed);
+    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0) {
+        keys[r] = h;
+        vals[r] = static_cast<uint32_t>(r);
+    }
+}
+
+// ---- stable LSD radix sort of (u64 key, u32 value), 8-bit digits ---------
+
+__global__ void k_radix_hist(const uint64_t* __restrict__ keys, int n, int shift,
+                             int* __restrict__ hist, int nblocks) {
+    __shared__ int cnt[256];
+    cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int base = blockIdx.x * kRadixTile;
+    for (int i = threadIdx.x; i < kRadixTile; i += 256) {
+        const int idx = base + i;
+        if (idx < n) atomicAdd(&cnt[(keys[idx] >> shift) & 0xFF], 1);
+    }
+    __syncthreads();
+    hist[threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void k_radix_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                uint64_t* __restrict__ kout, uint32_t* __restrict__ vout, int n,
+                                int shift, const int* __restrict__ offs, int nblocks) {
+    __shared__ int warp_cnt[8][256];
+    __shared__ int base_cnt[256];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int w = 0; w < 8; ++w) warp_cnt[w][tid] = 0;
+    base_cnt[tid] = offs[tid * nblocks + blockIdx.x];
+    __syncthreads();
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (int round = 0; round < kRadixTile / 256; ++round) {
+        const int idx = blockIdx.x * kRadixTile + round * 256 + tid;
+        const bool valid = idx < n;
+        uint64_t k = 0;
+        uint32_t v = 0;
+        int d = 256;  // sentinel digit for padding lanes
+        if (valid) {
+            k = kin[idx];
+            v = vin[idx];
+            d = static_cast<int>((k >> shift) & 0xFF);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int rank = __popc(peers & lt_mask);
+        if (valid && rank == 0) warp_cnt[warp][d] = __popc(peers);
+        __syncthreads();
+        {   // digit `tid`: exclusive prefix over warps plus running base
+            int run = base_cnt[tid];
+            for (int w = 0; w < 8; ++w) {
+                const int c = warp_cnt[w][tid];
+                warp_cnt[w][tid] = run;
+                run += c;
+            }
+            base_cnt[tid] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            const int pos = warp_cnt[warp][d] + rank;
+            kout[pos] = k;
+            vout[pos] = v;
+        }
+        __syncthreads();
+        for (int w = 0; w < 8; ++w) warp_cnt[w][tid] = 0;
+        __syncthreads();
+    }
+}
+
+// ---- exclusive scan (int32 sum) ------------------------------------------
+
+__global__ void k_scan_block(const int* __restrict__ in, int* __restrict__ out, int n,
+                             int* __restrict__ block_sums) {
+    __shared__ int s[256];
+    const int tid = threadIdx.x;
+    const int base = blockIdx.x * kScanTile + tid * 8;
+    int v[8];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        sum += v[i];
+    }
+    s[tid] = sum;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+        const int t = tid >= o ? s[tid - o] : 0;
+        __syncthreads();
+        s[tid] += t;
+        __syncthreads();
+    }
+    int run = s[tid] - sum;  // exclusive prefix of this thread
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+    if (tid == 255 && block_sums) block_sums[blockIdx.x] = s[255];
+}
+
+__global__ void k_scan_add(int* __restrict__ out, int n, const int* __restrict__ block_offs) {
+    const int idx = blockIdx.x * kScanTile + threadIdx.x;
+    const int add = block_offs[blockIdx.x];
+    for (int i = 0; i < kScanTile; i += 256)
+        if (idx + i < n) out[idx + i] += add;
+}
+
+__global__ void k_total(const int* __restrict__ in, const int* __restrict__ ex, int n,
+                        int* __restrict__ total) {
+    *total = n ? ex[n - 1] + in[n - 1] : 0;
+}
+
+// ---- runs / groups ---------------------------------------------------------
+
+__device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int upper_bound_u64(const uint64_t* a, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_runs(const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ srows,
+                       const uint64_t* __restrict__ words, int M, int W, int V,
+                       int* __restrict__ rank_out, int* __restrict__ lead_by_row,
+                       int* __restrict__ fail_head, uint32_t* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const uint64_t k = skeys[i];
+    const int rs = lower_bound_u64(skeys, M, k);
+    const int re = upper_bound_u64(skeys, M, k);
+    const int rank = i - rs;
+    if (rank > 0) {  // exact check against the previous row of the run
+        const uint64_t* a = words + static_cast<int64_t>(srows[i]) * W;
+        const uint64_t* b = words + static_cast<int64_t>(srows[i - 1]) * W;
+        for (int w = 0; w < W; ++w)
+            if (a[w] != b[w]) {
+                atomicOr(&flags[1], 1u);
+                break;
+            }
+    }
+    rank_out[i] = rank;
+    lead_by_row[srows[i]] = (rank % V == 0) ? 1 : 0;
+    const bool failing = ((re - rs) % V) != 0;
+    fail_head[i] = (failing && rank == 0) ? 1 : 0;
+    if (failing && rank == 0) atomicOr(&flags[2], 1u);
+}
+
+// lexicographically smallest failing class -> its smallest row
+__global__ void k_fail_argmin(const int* __restrict__ fail_head, const uint32_t* __restrict__ srows,
+                              const uint64_t* __restrict__ words, int M, int W,
+                              uint32_t* __restrict__ fail_row) {
+    __shared__ int best[1024];
+    const int tid = threadIdx.x;
+    auto less = [&](int a, int b) {  // rows a, b; -1 = none
+        if (b < 0) return a >= 0;
+        if (a < 0) return false;
+        const uint64_t* x = words + static_cast<int64_t>(a) * W;
+        const uint64_t* y = words + static_cast<int64_t>(b) * W;
+        for (int w = 0; w < W; ++w)
+            if (x[w] != y[w]) return x[w] < y[w];
+        return a < b;
+    };
+    int mine = -1;
+    for (int i = tid; i < M; i += blockDim.x)
+        if (fail_head[i] && less(static_cast<int>(srows[i]), mine)) mine = static_cast<int>(srows[i]);
+    best[tid] = mine;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (tid < o && less(best[tid + o], best[tid])) best[tid] = best[tid + o];
+        __syncthreads();
+    }
+    if (tid == 0) *fail_row = static_cast<uint32_t>(best[0] < 0 ? 0 : best[0]);
+}
+
+__global__ void k_assign(const uint32_t* __restrict__ srows, const int* __restrict__ rank,
+                         const int* __restrict__ gid_by_row, const int* __restrict__ popc, int M,
+                         int V, int ktile, int32_t* __restrict__ row_indices,
+                         int32_t* __restrict__ group_leader, int32_t* __restrict__ group_ncols,
+                         int* __restrict__ padded) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int slot = rank[i] % V;
+    const int lead_row = static_cast<int>(srows[i - slot]);
+    const int g = gid_by_row[lead_row];
+    row_indices[static_cast<int64_t>(g) * V + slot] = static_cast<int32_t>(srows[i]);
+    if (slot == 0) {
+        const int n = popc[lead_row];
+        group_leader[g] = lead_row;
+        group_ncols[g] = n;
+        padded[g] = (n + ktile - 1) / ktile * ktile;
+    }
+}
+
+// column list of group g: ascending set bits of the leader row, padded.
+__global__ void k_pack_cols(const uint64_t* __restrict__ words, int W,
+                            const int32_t* __restrict__ group_leader,
+                            const int32_t* __restrict__ group_ptr,
+                            const int32_t* __restrict__ group_ncols, int32_t* __restrict__ col_idx) {
+    __shared__ int s[128];
+    const int g = blockIdx.x, tid = threadIdx.x;
+    const uint64_t* lw = words + static_cast<int64_t>(group_leader[g]) * W;
+    const int wpt = (W + 127) / 128;
+    const int w0 = tid * wpt, w1 = min(W, w0 + wpt);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popcll(lw[w]);
+    s[tid] = cnt;
+    __syncthreads();
+    for (int o = 1; o < 128; o <<= 1) {
+        const int t = tid >= o ? s[tid - o] : 0;
+        __syncthreads();
+        s[tid] += t;
+        __syncthreads();
+    }
+    int out = group_ptr[g] + s[tid] - cnt;
+    for (int w = w0; w < w1; ++w) {
+        uint64_t x = lw[w];
+        while (x) {
+            const int b = __clzll(x);  // MSB first = ascending column
+            col_idx[out++] = w * 64 + b;
+            x &= ~(0x8000000000000000ULL >> b);
+        }
+    }
+    const int ng = group_ncols[g], pend = group_ptr[g + 1] - group_ptr[g];
+    for (int j = ng + tid; j < pend; j += 128) col_idx[group_ptr[g] + j] = SHFLBW_PAD_COLUMN;
+}
+
+// values[(gp + j) * V + v] = round16(dense[row_v][col_j]); pad columns -> 0.
+template <int DT>
+__global__ void k_pack_values(const void* __restrict__ dense, int dense_dtype, int K, int V,
+                              int jc, const int32_t* __restrict__ row_indices,
+                              const int32_t* __restrict__ group_ptr,
+                              const int32_t* __restrict__ group_ncols,
+                              const int32_t* __restrict__ col_idx, void* __restrict__ values) {
+    using T = typename Elem<DT>::T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* tile = reinterpret_cast<T*>(smem_raw);  // [jc][V]
+    const int g = blockIdx.y;
+    const int j0 = blockIdx.x * jc;
+    const int gp = group_ptr[g];
+    const int padded = group_ptr[g + 1] - gp;
+    if (j0 >= padded) return;
+    const int ng = group_ncols[g];
+    const int total = jc * V;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int v = idx / jc, jj = idx % jc;  // jj fastest: same row, ascending columns
+        const int j = j0 + jj;
+        float x = 0.0f;
+        if (j < ng) {
+            const int64_t row = row_indices[static_cast<int64_t>(g) * V + v];
+            x = load_as_f32(dense, dense_dtype, row * K + col_idx[gp + j]);
+        }
+        tile[jj * V + v] = Elem<DT>::from_f(x);
+    }
+    __syncthreads();
+    T* dst = static_cast<T*>(values) + static_cast<int64_t>(gp + j0) * V;
+    const int lim = min(jc, padded - j0) * V;
+    for (int idx = threadIdx.x; idx < lim; idx += blockDim.x) dst[idx] = tile[idx];
+}
+
+// ---- upload / download / decompress --------------------------------------
+
+__global__ void k_upload_groups(const int32_t* __restrict__ gn, int G, int V, int K, int ktile,
+                                int* __restrict__ padded, uint32_t* __restrict__ flags) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    const int n = gn[g];
+    if (n < 0 || n > K) atomicOr(&flags[3], 1u);
+    padded[g] = (n + ktile - 1) / ktile * ktile;
+}
+
+__global__ void k_check_rows(const int32_t* __restrict__ ri, int M, uint32_t* __restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < M && (ri[i] < 0 || ri[i] >= M)) atomicOr(&flags[0], 1u);
+}
+
+template <int DT>
+__global__ void k_upload_values(const uint32_t* __restrict__ cols_in, const float* __restrict__ vals_in,
+                                const int* __restrict__ src_off, const int32_t* __restrict__ group_ptr,
+                                const int32_t* __restrict__ group_ncols, int V, int K,
+                                int32_t* __restrict__ col_idx, void* __restrict__ values,
+                                uint32_t* __restrict__ flags) {
+    using T = typename Elem<DT>::T;
+    const int g = blockIdx.y;
+    const int gp = group_ptr[g], padded = group_ptr[g + 1] - gp, ng = group_ncols[g];
+    const int64_t so = src_off[g];
+    T* dst = static_cast<T*>(values);
+    const int64_t total = static_cast<int64_t>(padded) * V;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(idx / V), v = static_cast<int>(idx % V);
+        const float x = j < ng ? vals_in[(so + j) * V + v] : 0.0f;
+        dst[(static_cast<int64_t>(gp) + j) * V + v] = Elem<DT>::from_f(x);
+        if (v == 0) {
+            int32_t c = SHFLBW_PAD_COLUMN;
+            if (j < ng) {
+                const uint32_t cu = cols_in[so + j];
+                if (cu >= static_cast<uint32_t>(K) ||
+                    (j > 0 && cols_in[so + j - 1] >= cu)) atomicOr(&flags[1], 1u);
+                c = static_cast<int32_t>(cu);
+            }
+            col_idx[gp + j] = c;
+        }
+    }
+}
+
+template <int DT>
+__global__ void k_download_values(const int32_t* __restrict__ col_idx, const void* __restrict__ values,
+                                  const int* __restrict__ dst_off, const int32_t* __restrict__ group_ptr,
+                                  const int32_t* __restrict__ group_ncols, int V,
+                                  uint32_t* __restrict__ cols_out, float* __restrict__ vals_out) {
+    const int g = blockIdx.y;
+    const int gp = group_ptr[g], ng = group_ncols[g];
+    const int64_t dof = dst_off[g];
+    const int64_t total = static_cast<int64_t>(ng) * V;
+    const auto* src = static_cast<const typename Elem<DT>::T*>(values);
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(idx / V), v = static_cast<int>(idx % V);
+        vals_out[(dof + j) * V + v] = Elem<DT>::to_f(src[(static_cast<int64_t>(gp) + j) * V + v]);
+        if (v == 0) cols_out[dof + j] = static_cast<uint32_t>(col_idx[gp + j]);
+    }
+}
+
+template <int DT>
+__global__ void k_decompress(const int32_t* __restrict__ row_indices, const int32_t* __restrict__ group_ptr,
+                             const int32_t* __restrict__ group_ncols, const int32_t* __restrict__ col_idx,
+                             const void* __restrict__ values, int V, int K, float* __restrict__ dense) {
+    const int g = blockIdx.y;
+    const int gp = group_ptr[g], ng = group_ncols[g];
+    const auto* src = static_cast<const typename Elem<DT>::T*>(values);
+    const int64_t total = static_cast<int64_t>(ng) * V;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(idx / V), v = static_cast<int>(idx % V);
+        const int64_t row = row_indices[static_cast<int64_t>(g) * V + v];
+        dense[row * K + col_idx[gp + j]] = Elem<DT>::to_f(src[(static_cast<int64_t>(gp) + j) * V + v]);
+    }
+}
+
+__global__ void k_convert(const void* __restrict__ src, int sdt, void* __restrict__ dst, int ddt,
+                          int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        store_from_f32(dst, ddt, i, load_as_f32(src, sdt, i));
+}
+
+// ---- host helpers ------------------------------------------------------------
+
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    cudaError_t alloc(size_t bytes, cudaStream_t st) {
+        s = st;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, st);
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+int grid_for(int64_t n, int per_block) {
+    const int64_t b = (n + per_block - 1) / per_block;
+    return static_cast<int>(b < 1 ? 1 : (b > 1048576 ? 1048576 : b));
+}
+
+}  // namespace
+
+// exclusive scan, out may alias nothing; *total_dev (optional) = sum
+int scan_exclusive(const int* in, int* out, int n, int* total_dev, cudaStream_t s) {
+    if (n <= 0) {
+        if (total_dev) SBW_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(int), s));
+        return SHFLBW_OK;
+    }
+    const int nb = (n + kScanTile - 1) / kScanTile;
+    if (nb == 1) {
+        k_scan_block<<<1, 256, 0, s>>>(in, out, n, nullptr);
+        SBW_LAUNCHED("k_scan_block");
+    } else {
+        DevBuf sums, offs;
+        SBW_CUDA(sums.alloc(sizeof(int) * nb, s));
+        SBW_CUDA(offs.alloc(sizeof(int) * nb, s));
+        k_scan_block<<<nb, 256, 0, s>>>(in, out, n, sums.as<int>());
+        SBW_LAUNCHED("k_scan_block");
+        const int st = scan_exclusive(sums.as<int>(), offs.as<int>(), nb, nullptr, s);
+        if (st) return st;
+        k_scan_add<<<nb, 256, 0, s>>>(out, n, offs.as<int>());
+        SBW_LAUNCHED("k_scan_add");
+    }
+    if (total_dev) {
+        k_total<<<1, 1, 0, s>>>(in, out, n, total_dev);
+        SBW_LAUNCHED("k_total");
+    }
+    return SHFLBW_OK;
+}
+
+namespace {
+
+int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int n,
+                     cudaStream_t s) {
+    const int nb = (n + kRadixTile - 1) / kRadixTile;
+    DevBuf hist, offs;
+    SBW_CUDA(hist.alloc(sizeof(int) * 256 * nb, s));
+    SBW_CUDA(offs.alloc(sizeof(int) * 256 * nb, s));
+    uint64_t *ki = keys, *ko = keys_tmp;
+    uint32_t *vi = vals, *vo = vals_tmp;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = pass * 8;
+        k_radix_hist<<<nb, 256, 0, s>>>(ki, n, shift, hist.as<int>(), nb);
+        SBW_LAUNCHED("k_radix_hist");
+        int st = scan_exclusive(hist.as<int>(), offs.as<int>(), 256 * nb, nullptr, s);
+        if (st) return st;
+        k_radix_scatter<<<nb, 256, 0, s>>>(ki, vi, ko, vo, n, shift, offs.as<int>(), nb);
+        SBW_LAUNCHED("k_radix_scatter");
+        std::swap(ki, ko);
+        std::swap(vi, vo);
+    }
+    // 8 passes: result is back in keys / vals
+    return SHFLBW_OK;
+}
+
+// Steps 1-4 shared by validate and compress.
+struct ClassPlan {
+    DevBuf words, popc, keys, vals, keys2, vals2, rank, lead, fail_head, flags;
+    int W = 1;
+};
+
+int plan_classes(const uint8_t* mask, int M, int K, int V, ClassPlan& p, uint32_t host_flags[4],
+                 cudaStream_t s) {
+    p.W = K > 0 ? (K + 63) / 64 : 1;
+    const int64_t MW = static_cast<int64_t>(M) * p.W;
+    SBW_CUDA(p.words.alloc(sizeof(uint64_t) * MW, s));
+    SBW_CUDA(p.popc.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.keys.alloc(sizeof(uint64_t) * M, s));
+    SBW_CUDA(p.vals.alloc(sizeof(uint32_t) * M, s));
+    SBW_CUDA(p.keys2.alloc(sizeof(uint64_t) * M, s));
+    SBW_CUDA(p.vals2.alloc(sizeof(uint32_t) * M, s));
+    SBW_CUDA(p.rank.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.lead.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.fail_head.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.flags.alloc(sizeof(uint32_t) * 4, s));
+    if (K == 0) SBW_CUDA(cudaMemsetAsync(p.words.p, 0, sizeof(uint64_t) * MW, s));
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        const uint64_t seed = 0x5ca1ab1e00000000ULL + attempt;
+        SBW_CUDA(cudaMemsetAsync(p.flags.p, 0, sizeof(uint32_t) * 4, s));
+        if (attempt == 0) {
+            k_pack_rows<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, p.W, seed, p.words.as<uint64_t>(),
+                                                       p.popc.as<int>(), p.keys.as<uint64_t>(),
+                                                       p.vals.as<uint32_t>(), p.flags.as<uint32_t>());
+            SBW_LAUNCHED("k_pack_rows");
+            if (K == 0) {  // no columns: every row is the empty support
+                SBW_CUDA(cudaMemsetAsync(p.popc.p, 0, sizeof(int) * M, s));
+                k_hash_rows<<<grid_for(M, 8), 256, 0, s>>>(p.words.as<uint64_t>(), M, p.W, seed,
+                                                           p.keys.as<uint64_t>(), p.vals.as<uint32_t>());
+                SBW_LAUNCHED("k_hash_rows");
+            }
+        } else {
+            k_hash_rows<<<grid_for(M, 8), 256, 0, s>>>(p.words.as<uint64_t>(), M, p.W, seed,
+                                                       p.keys.as<uint64_t>(), p.vals.as<uint32_t>());
+            SBW_LAUNCHED("k_hash_rows");
+        }
+        int st = radix_sort_pairs(p.keys.as<uint64_t>(), p.vals.as<uint32_t>(), p.keys2.as<uint64_t>(),
+                                  p.vals2.as<uint32_t>(), M, s);
+        if (st) return st;
+        k_runs<<<grid_for(M, 256), 256, 0, s>>>(p.keys.as<uint64_t>(), p.vals.as<uint32_t>(),
+                                                p.words.as<uint64_t>(), M, p.W, V, p.rank.as<int>(),
+                                                p.lead.as<int>(), p.fail_head.as<int>(),
+                                                p.flags.as<uint32_t>());
+        SBW_LAUNCHED("k_runs");
+        SBW_CUDA(cudaMemcpyAsync(host_flags, p.flags.p, sizeof(uint32_t) * 4, cudaMemcpyDeviceToHost, s));
+        SBW_CUDA(cudaStreamSynchronize(s));
+        if (host_flags[0]) return fail(SHFLBW_BAD_PARAMS, "SparsityMask: entries must be 0 or 1");
+        if (!host_flags[1]) return SHFLBW_OK;
+    }
+    return fail(SHFLBW_CUDA_ERROR, "compress: unresolvable row-hash collisions");
+}
+
+int first_failing_row(ClassPlan& p, int M, uint32_t* fail_row, cudaStream_t s) {
+    DevBuf fr;
+    SBW_CUDA(fr.alloc(sizeof(uint32_t), s));
+    k_fail_argmin<<<1, 1024, 0, s>>>(p.fail_head.as<int>(), p.vals.as<uint32_t>(),
+                                     p.words.as<uint64_t>(), M, p.W, fr.as<uint32_t>());
+    SBW_LAUNCHED("k_fail_argmin");
+    SBW_CUDA(cudaMemcpyAsync(fail_row, fr.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaStreamSynchronize(s));
+    return SHFLBW_OK;
+}
+
+int check_dtype16(int dt) {
+    if (dt != SHFLBW_BF16 && dt != SHFLBW_F16 && dt != SHFLBW_F32)
+        return fail(SHFLBW_BAD_PARAMS, "value dtype must be SHFLBW_BF16, SHFLBW_F16 or SHFLBW_F32");
+    return SHFLBW_OK;
+}
+
+// run `f.template operator()<DT>()` for the matrix value dtype
+template <class F>
+void by_dtype(int dt, F&& f) {
+    if (dt == SHFLBW_BF16) f.template operator()<SHFLBW_BF16>();
+    else if (dt == SHFLBW_F16) f.template operator()<SHFLBW_F16>();
+    else f.template operator()<SHFLBW_F32>();
+}
+
+// allocate meta (row_indices, group_ptr, group_ncols) in one block
+int alloc_meta(shflbw_cu_matrix* out, int M, int K, int V, int dtype) {
+    const int G = M / V;
+    const size_t a = (static_cast<size_t>(M) * 4 + 255) / 256 * 256;
+    const size_t b = (static_cast<size_t>(G + 1) * 4 + 255) / 256 * 256;
+    const size_t c = (static_cast<size_t>(G) * 4 + 255) / 256 * 256;
+    char* base = nullptr;
+    SBW_CUDA(cudaMalloc(&base, a + b + c + 256));
+    *out = shflbw_cu_matrix{};
+    out->rows = M;
+    out->cols = K;
+    out->v = V;
+    out->groups = G;
+    out->dtype = dtype;
+    out->k_tile = SHFLBW_K_TILE;
+    out->row_indices = reinterpret_cast<int32_t*>(base);
+    out->group_ptr = reinterpret_cast<int32_t*>(base + a);
+    out->group_ncols = reinterpret_cast<int32_t*>(base + a + b);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    out->device = dev;
+    out->owns = 1;
+    return SHFLBW_OK;
+}
+
+int alloc_data(shflbw_cu_matrix* out, int64_t total) {
+    const size_t a = (static_cast<size_t>(total) * 4 + 255) / 256 * 256;
+    const size_t b = static_cast<size_t>(total) * out->v * dtype_bytes(out->dtype);
+    char* base = nullptr;
+    SBW_CUDA(cudaMalloc(&base, a + b + 256));
+    out->col_idx = reinterpret_cast<int32_t*>(base);
+    out->values = base + a;
+    out->total_cols = total;
+    return SHFLBW_OK;
+}
+
+}  // namespace
+
+void free_matrix(shflbw_cu_matrix* m) {
+    if (!m || !m->owns) return;
+    if (m->row_indices) cudaFree(m->row_indices);
+    if (m->col_idx) cudaFree(m->col_idx);
+    m->row_indices = m->group_ptr = m->group_ncols = m->col_idx = nullptr;
+    m->values = nullptr;
+    m->owns = 0;
+}
+
+int validate_impl(const uint8_t* mask, int M, int K, int V, int32_t* pass, uint32_t* fail_row,
+                  cudaStream_t s) {
+    if (V <= 0 || M < 0 || K < 0 || M % V != 0) return fail(SHFLBW_BAD_PARAMS, "V must divide M");
+    *pass = 1;
+    *fail_row = 0;
+    if (M == 0) return SHFLBW_OK;
+    ClassPlan p;
+    uint32_t hf[4];
+    int st = plan_classes(mask, M, K, V, p, hf, s);
+    if (st) return st;
+    if (hf[2]) {
+        *pass = 0;
+        return first_failing_row(p, M, fail_row, s);
+    }
+    return SHFLBW_OK;
+}
+
+int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M, int K, int V,
+                  int value_dtype, shflbw_cu_matrix* out, uint32_t* fail_row, cudaStream_t s) {
+    if (int st = check_dtype16(value_dtype)) return st;
+    if (dense_dtype < SHFLBW_F32 || dense_dtype > SHFLBW_F16) return fail(SHFLBW_BAD_PARAMS, "dense dtype");
+    if (V <= 0 || M < 0 || K < 0 || M % V != 0) return fail(SHFLBW_BAD_PARAMS, "V must divide M");
+    if (fail_row) *fail_row = 0;
+    const int G = M / V;
+    if (int st = alloc_meta(out, M, K, V, value_dtype)) return st;
+    auto cleanup = [&](int st) {
+        if (st) free_matrix(out);
+        return st;
+    };
+    if (M == 0) {
+        SBW_CUDA(cudaMemsetAsync(out->group_ptr, 0, sizeof(int32_t), s));
+        return cleanup(alloc_data(out, 0));
+    }
+    ClassPlan p;
+    uint32_t hf[4];
+    int st = plan_classes(mask, M, K, V, p, hf, s);
+    if (st) return cleanup(st);
+    if (hf[2]) {
+        uint32_t fr = 0;
+        st = first_failing_row(p, M, &fr, s);
+        if (st) return cleanup(st);
+        if (fail_row) *fail_row = fr;
+        return cleanup(fail(SHFLBW_NONCONFORMANT_MASK,
+                            "compress_shflbw: support class size is not a multiple of V (row " +
+                                std::to_string(fr) + ")"));
+    }
+    DevBuf gid, leader, padded, total;
+    SBW_CUDA(gid.alloc(sizeof(int) * M, s));
+    SBW_CUDA(leader.alloc(sizeof(int) * G, s));
+    SBW_CUDA(padded.alloc(sizeof(int) * G, s));
+    SBW_CUDA(total.alloc(sizeof(int), s));
+    if ((st = scan_exclusive(p.lead.as<int>(), gid.as<int>(), M, nullptr, s))) return cleanup(st);
+    k_assign<<<grid_for(M, 256), 256, 0, s>>>(p.vals.as<uint32_t>(), p.rank.as<int>(), gid.as<int>(),
+                                              p.popc.as<int>(), M, V, SHFLBW_K_TILE, out->row_indices,
+                                              leader.as<int32_t>(), out->group_ncols, padded.as<int>());
+    SBW_LAUNCHED("k_assign");
+    if ((st = scan_exclusive(padded.as<int>(), out->group_ptr, G, out->group_ptr + G, s))) return cleanup(st);
+    int total_cols = 0;
+    SBW_CUDA(cudaMemcpyAsync(&total_cols, out->group_ptr + G, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaStreamSynchronize(s));
+    if ((st = alloc_data(out, total_cols))) return cleanup(st);
+    if (G > 0) {
+        k_pack_cols<<<G, 128, 0, s>>>(p.words.as<uint64_t>(), p.W, leader.as<int32_t>(), out->group_ptr,
+                                      out->group_ncols, out->col_idx);
+        SBW_LAUNCHED("k_pack_cols");
+        const int jc = V <= 1024 ? 64 : 8;
+        const size_t smem = static_cast<size_t>(jc) * V * dtype_bytes(value_dtype);
+        int max_padded = K <= 0 ? 0 : (K + SHFLBW_K_TILE - 1) / SHFLBW_K_TILE * SHFLBW_K_TILE;
+        dim3 grid((max_padded + jc - 1) / jc, G);
+        if (grid.x > 0) {
+            cudaError_t ce = cudaSuccess;
+            by_dtype(value_dtype, [&]<int DT>() {
+                if (smem > 48 * 1024)
+                    ce = cudaFuncSetAttribute(k_pack_values<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem));
+                k_pack_values<DT><<<grid, 256, smem, s>>>(dense, dense_dtype, K, V, jc, out->row_indices,
+                                                          out->group_ptr, out->group_ncols, out->col_idx,
+                                                          out->values);
+            });
+            if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaFuncSetAttribute"));
+            SBW_LAUNCHED("k_pack_values");
+        }
+    }
+    return SHFLBW_OK;
+}
+
+int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t* group_ncols,
+                const uint32_t* cols, const float* values, int value_dtype, shflbw_cu_matrix* out,
+                cudaStream_t s) {
+    if (int st = check_dtype16(value_dtype)) return st;
+    if (V <= 0 || M < 0 || K < 0 || M % V != 0) return fail(SHFLBW_BAD_PARAMS, "V must divide M");
+    const int G = M / V;
+    int64_t nnzc = 0;
+    for (int g = 0; g < G; ++g) nnzc += group_ncols[g];
+    if (int st = alloc_meta(out, M, K, V, value_dtype)) return st;
+    auto cleanup = [&](int st) {
+        if (st) free_matrix(out);
+        return st;
+    };
+    DevBuf d_cols, d_vals, d_off, d_pad, flags;
+    SBW_CUDA(d_cols.alloc(sizeof(uint32_t) * nnzc, s));
+    SBW_CUDA(d_vals.alloc(sizeof(float) * nnzc * V, s));
+    SBW_CUDA(d_off.alloc(sizeof(int) * (G + 1), s));
+    SBW_CUDA(d_pad.alloc(sizeof(int) * (G + 1), s));
+    SBW_CUDA(flags.alloc(sizeof(uint32_t) * 4, s));
+    SBW_CUDA(cudaMemsetAsync(flags.p, 0, 16, s));
+    SBW_CUDA(cudaMemcpyAsync(out->row_indices, row_indices, sizeof(int32_t) * M, cudaMemcpyHostToDevice, s));
+    SBW_CUDA(cudaMemcpyAsync(out->group_ncols, group_ncols, sizeof(int32_t) * G, cudaMemcpyHostToDevice, s));
+    if (nnzc) {
+        SBW_CUDA(cudaMemcpyAsync(d_cols.p, cols, sizeof(uint32_t) * nnzc, cudaMemcpyHostToDevice, s));
+        SBW_CUDA(cudaMemcpyAsync(d_vals.p, values, sizeof(float) * nnzc * V, cudaMemcpyHostToDevice, s));
+    }
+    int st;
+    if (G > 0) {
+        k_upload_groups<<<grid_for(G, 256), 256, 0, s>>>(out->group_ncols, G, V, K, SHFLBW_K_TILE,
+                                                         d_pad.as<int>(), flags.as<uint32_t>());
+        SBW_LAUNCHED("k_upload_groups");
+    }
+    if (M > 0) {
+        k_check_rows<<<grid_for(M, 256), 256, 0, s>>>(out->row_indices, M, flags.as<uint32_t>());
+        SBW_LAUNCHED("k_check_rows");
+    }
+    if ((st = scan_exclusive(out->group_ncols, d_off.as<int>(), G, nullptr, s))) return cleanup(st);
+    if ((st = scan_exclusive(d_pad.as<int>(), out->group_ptr, G, out->group_ptr + G, s))) return cleanup(st);
+    int total_cols = 0;
+    uint32_t hf[4];
+    SBW_CUDA(cudaMemcpyAsync(&total_cols, out->group_ptr + G, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaMemcpyAsync(hf, flags.p, 16, cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaStreamSynchronize(s));
+    if (hf[0]) return cleanup(fail(SHFLBW_SHAPE_MISMATCH, "spmm: row index out of range"));
+    if (hf[3]) return cleanup(fail(SHFLBW_BAD_PARAMS, "group column count exceeds K"));
+    if ((st = alloc_data(out, total_cols))) return cleanup(st);
+    if (G > 0 && total_cols > 0) {
+        dim3 grid(grid_for(static_cast<int64_t>(K + SHFLBW_K_TILE) * V, 256 * 4), G);
+        by_dtype(value_dtype, [&]<int DT>() {
+            k_upload_values<DT><<<grid, 256, 0, s>>>(d_cols.as<uint32_t>(), d_vals.as<float>(), d_off.as<int>(),
+                                                     out->group_ptr, out->group_ncols, V, K, out->col_idx,
+                                                     out->values, flags.as<uint32_t>());
+        });
+        SBW_LAUNCHED("k_upload_values");
+        SBW_CUDA(cudaMemcpyAsync(hf, flags.p, 16, cudaMemcpyDeviceToHost, s));
+        SBW_CUDA(cudaStreamSynchronize(s));
+        if (hf[1]) return cleanup(fail(SHFLBW_SHAPE_MISMATCH, "column index exceeds B rows or is not increasing"));
+    }
+    return SHFLBW_OK;
+}
+
+int download_impl(const shflbw_cu_matrix* m, uint32_t* row_indices, uint32_t* group_ncols,
+                  uint32_t* cols, float* values, cudaStream_t s) {
+    const int G = m->groups, V = m->v, M = m->rows;
+    SBW_CUDA(cudaMemcpyAsync(row_indices, m->row_indices, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaMemcpyAsync(group_ncols, m->group_ncols, sizeof(int32_t) * G, cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaStreamSynchronize(s));
+    int64_t nnzc = 0;
+    for (int g = 0; g < G; ++g) nnzc += group_ncols[g];
+    if (nnzc == 0) return SHFLBW_OK;
+    DevBuf d_off, d_cols, d_vals;
+    SBW_CUDA(d_off.alloc(sizeof(int) * (G + 1), s));
+    SBW_CUDA(d_cols.alloc(sizeof(uint32_t) * nnzc, s));
+    SBW_CUDA(d_vals.alloc(sizeof(float) * nnzc * V, s));
+    int st = scan_exclusive(m->group_ncols, d_off.as<int>(), G, nullptr, s);
+    if (st) return st;
+    dim3 grid(grid_for(static_cast<int64_t>(m->cols + 1) * V, 1024), G);
+    by_dtype(m->dtype, [&]<int DT>() {
+        k_download_values<DT><<<grid, 256, 0, s>>>(m->col_idx, m->values, d_off.as<int>(), m->group_ptr,
+                                                   m->group_ncols, V, d_cols.as<uint32_t>(), d_vals.as<float>());
+    });
+    SBW_LAUNCHED("k_download_values");
+    SBW_CUDA(cudaMemcpyAsync(cols, d_cols.p, sizeof(uint32_t) * nnzc, cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaMemcpyAsync(values, d_vals.p, sizeof(float) * nnzc * V, cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaStreamSynchronize(s));
+    return SHFLBW_OK;
+}
+
+int decompress_impl(const shflbw_cu_matrix* m, float* dense, cudaStream_t s) {
+    SBW_CUDA(cudaMemsetAsync(dense, 0, sizeof(float) * static_cast<size_t>(m->rows) * m->cols, s));
+    if (m->groups == 0) return SHFLBW_OK;
+    dim3 grid(grid_for(static_cast<int64_t>(m->cols + 1) * m->v, 1024), m->groups);
+    by_dtype(m->dtype, [&]<int DT>() {
+        k_decompress<DT><<<grid, 256, 0, s>>>(m->row_indices, m->group_ptr, m->group_ncols, m->col_idx, m->values,
+                                              m->v, m->cols, dense);
+    });
+    SBW_LAUNCHED("k_decompress");
+    return SHFLBW_OK;
+}
+
+int convert_impl(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s) {
+    if (n <= 0) return SHFLBW_OK;
+    k_convert<<<grid_for(n, 256 * 8), 256, 0, s>>>(src, sdt, dst, ddt, n);
+    SBW_LAUNCHED("k_convert");
+    return SHFLBW_OK;
+}
+
+}  // namespace sbw

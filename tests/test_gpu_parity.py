@@ -1,0 +1,384 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle.
+
+Inputs follow SURVEY.md §8(d): synthetic W, B from the reference's own
+generators, rounded to bf16 (RNE) before BOTH sides see them, so operands
+are identical and every product is exact in fp32.  Bars:
+  * converter: bit-exact row permutation, group column lists, padded device
+    layout and bf16 values;
+  * CUDA-core path (any V): bit-exact vs the reference's pinned order;
+  * tcgen05 path: rel. Frobenius error <= 1e-5 vs the fp32 oracle (the
+    reference's own --check bar, tools/shflbw.cpp:33) in fp32-output mode,
+    and in bf16-output mode exactly that fp32 result rounded once (RNE).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def sb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2203_05016_b200 as sb
+    sb.set_option("force_simt", 0)
+    sb.set_option("split", 0)
+    sb.set_option("stages", 0)
+    return sb
+
+
+def dev(x, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(dtype) if dtype is not None else t
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def synthetic(oracle, M, K, N, V, alpha, seed=1234):
+    """SURVEY §8(d) synthetic inputs: mask random_shflbw_mask(..., mt19937_64(1234)),
+    W = random_dense(M,K,1), B = random_dense(K,N,2), bf16-rounded."""
+    cpg = int(np.floor(alpha * K + 0.5))
+    mask = oracle.random_shflbw_mask(M, K, V, cpg, oracle.rng(seed))
+    W = oracle.round16(oracle.random_dense(M, K, 1))
+    B = oracle.round16(oracle.random_dense(K, N, 2))
+    return mask, W, B
+
+
+def compress_both(sb, oracle, W, mask, V):
+    a = sb.compress_shflbw(dev(W), dev(mask), V)
+    return a, oracle.compress(W, mask, V)
+
+
+def assert_same_packing(a, p, oracle):
+    ri, gn, cols, vals = a.to_host()
+    assert np.array_equal(ri, p.row_indices)
+    assert np.array_equal(gn, p.group_ncols)
+    assert np.array_equal(cols, p.cols)
+    assert np.array_equal(vals.view(np.uint32), oracle.round16(p.values).view(np.uint32))
+    gp, ci, vv = a.raw()
+    egp, eci, evv = oracle.pack_device(p, 64, "bf16")
+    assert np.array_equal(gp, egp)
+    assert np.array_equal(ci, eci)
+    assert np.array_equal(vv, evv)
+
+
+# ---------------------------------------------------------------- converter
+
+@pytest.mark.parametrize("case", load_golden("formats_kat.json")["compress"], ids=lambda c: c["name"])
+def test_compress_known_answers(sb, oracle, case):
+    if case["name"] == "shape_mismatch":
+        with pytest.raises(sb.ShapeMismatch):
+            sb.compress_shflbw(torch.zeros(2, 2, device="cuda"), torch.zeros(2, 3, dtype=torch.uint8,
+                                                                            device="cuda"), 2)
+        return
+    dense = np.array(case["dense_bits"], np.uint32).view(np.float32).reshape(case["dense_shape"])
+    mask = np.array(case["mask"], np.uint8).reshape(case["mask_shape"])
+    V = case["V"]
+    if case["status"] == 3:
+        with pytest.raises(sb.BadParams):
+            sb.compress_shflbw(dev(dense), dev(mask), V)
+        return
+    if case["status"] == 2:
+        with pytest.raises(sb.NonConformantMask, match=rf"\(row {case['fail_row']}\)"):
+            sb.compress_shflbw(dev(dense), dev(mask), V)
+        assert sb.validate_pattern(dev(mask), "shfl_bw", V) == (False, case["fail_row"])
+        return
+    a = sb.compress_shflbw(dev(dense), dev(mask), V)
+    want = case["packed"]
+    ri, gn, cols, vals = a.to_host()
+    assert ri.tolist() == want["row_indices"]
+    assert gn.tolist() == want["group_ncols"]
+    assert cols.tolist() == want["cols"]
+    wv = oracle.round16(np.array(want["values_bits"], np.uint32).view(np.float32))
+    assert np.array_equal(vals, wv)
+    d = sb.decompress(a).cpu().numpy()
+    assert np.array_equal(d, oracle.round16(
+        np.array(case["decompressed_bits"], np.uint32).view(np.float32).reshape(d.shape)))
+
+
+def test_compress_random_sequences(sb, oracle):
+    for case in load_golden("compress_random.json"):
+        m, k, V = case["m"], case["k"], case["V"]
+        mask = np.array(case["mask"], np.uint8).reshape(m, k)
+        if case["suite"] == "roundtrip":
+            W = oracle.round16(oracle.random_dense(m, k, case["dense_seed"]))
+            a = sb.compress_shflbw(dev(W), dev(mask), V)
+            want = case["packed"]
+            ri, gn, cols, vals = a.to_host()
+            assert ri.tolist() == want["row_indices"]
+            assert gn.tolist() == want["group_ncols"]
+            assert cols.tolist() == want["cols"]
+            d = sb.decompress(a).cpu().numpy()
+            assert np.array_equal(d, W * mask)
+        else:
+            assert sb.validate_pattern(dev(mask), "shfl_bw", V) == (case["pass"], case["fail_row"])
+            if case["status"] == 0:
+                sb.compress_shflbw(torch.zeros(m, k, device="cuda"), dev(mask), V)
+            else:
+                with pytest.raises(sb.NonConformantMask):
+                    sb.compress_shflbw(torch.zeros(m, k, device="cuda"), dev(mask), V)
+
+
+@pytest.mark.parametrize("case", load_golden("full_size.json"),
+                         ids=lambda c: f"M{c['M']}K{c['K']}V{c['V']}")
+def test_compress_full_size_bit_exact(sb, oracle, case):
+    M, K, V = case["M"], case["K"], case["V"]
+    mask = oracle.random_shflbw_mask(M, K, V, case["cpg"], oracle.rng(1234))
+    W = oracle.round16(oracle.random_dense(M, K, 1))
+    a, p = compress_both(sb, oracle, W, mask, V)
+    assert digest(p.row_indices) == case["row_indices_digest"]  # oracle pinned to the reference
+    assert_same_packing(a, p, oracle)
+
+
+def test_compress_fp32_dense_rounds_rne(sb, oracle):
+    """Unrounded fp32 weights: the converter's bf16 RNE equals the oracle's."""
+    mask, _, _ = synthetic(oracle, 256, 512, 8, 32, 0.5)
+    W = oracle.random_dense(256, 512, 9)
+    a, p = compress_both(sb, oracle, W, mask, 32)
+    assert_same_packing(a, p, oracle)
+
+
+def test_validate_nonconformant_lexicographic(sb, oracle):
+    rs = np.random.RandomState(3)
+    for t in range(40):
+        V = int(rs.randint(2, 5))
+        M = V * int(rs.randint(1, 20))
+        K = int(rs.randint(1, 150))
+        mask = (rs.rand(M, K) < 0.5).astype(np.uint8)
+        if t % 3 == 0:  # mostly-conformant: duplicate rows, then break one class
+            base = (rs.rand(M // V, K) < 0.3).astype(np.uint8)
+            mask = base[rs.permutation(np.repeat(np.arange(M // V), V))]
+            mask[rs.randint(M), rs.randint(K)] ^= 1
+        assert sb.validate_pattern(dev(mask), "shfl_bw", V) == oracle.validate(mask, V)
+
+
+def test_mask_entries_must_be_binary(sb):
+    mask = torch.ones(4, 4, dtype=torch.uint8, device="cuda")
+    mask[1, 2] = 2
+    with pytest.raises(sb.BadParams):
+        sb.compress_shflbw(torch.zeros(4, 4, device="cuda"), mask, 2)
+
+
+def test_upload_roundtrip(sb, oracle):
+    mask, W, _ = synthetic(oracle, 512, 256, 8, 64, 0.3)
+    p = oracle.compress(W, mask, 64)
+    a = sb.upload(512, 256, 64, p.row_indices, p.group_ncols, p.cols, p.values)
+    assert_same_packing(a, p, oracle)
+
+
+# ---------------------------------------------------------------- SpMM
+
+def test_spmm_unit_instances_bit_exact(sb, oracle):
+    """tests/test_spmm.cpp:115-131 instances (V in {2,4,8}: CUDA-core path),
+    bf16 inputs: bit-identical to the reference order."""
+    for case in [c for c in load_golden("spmm_random.json") if c["suite"] == "unit"]:
+        m, k, n, V = case["m"], case["k"], case["n"], case["V"]
+        mask = np.array(case["mask"], np.uint8).reshape(m, k)
+        W = oracle.round16(oracle.random_dense(m, k, case["dense_seed"]))
+        B = oracle.round16(oracle.random_dense(k, n, case["b_seed"]))
+        a, p = compress_both(sb, oracle, W, mask, V)
+        got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
+        assert np.array_equal(got, oracle.spmm(p, B))
+
+
+def test_spmm_acceptance_instances(sb, oracle):
+    """acceptance criterion 1 sequence (tests/acceptance.cpp:59-92): V 2..16."""
+    rng = oracle.rng(1001)
+    worst = 0.0
+    for _ in range(120):
+        V = 1 << (1 + rng() % 4)
+        m = V * (1 + rng() % (256 // V))
+        k = 1 + rng() % 256
+        n = 1 + rng() % 64
+        alpha = 0.1 * (1 + rng() % 10)
+        cpg = int(np.floor(alpha * k + 0.5)) % (k + 1)
+        mask = oracle.random_shflbw_mask(m, k, V, cpg, rng)
+        W = oracle.round16(oracle.random_dense(m, k, rng()))
+        B = oracle.round16(oracle.random_dense(k, n, rng()))
+        rng(), rng(), rng()
+        a, p = compress_both(sb, oracle, W, mask, V)
+        got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
+        want = oracle.spmm(p, B)
+        if V == 16:
+            worst = max(worst, oracle.rel_frobenius(got, want))
+        else:
+            assert np.array_equal(got, want)
+    assert worst <= TOL
+
+
+@pytest.mark.parametrize("M,N,K,V,alpha", [(2048, 128, 2048, 64, 0.25), (2048, 128, 2048, 32, 0.25),
+                                           (2048, 128, 2048, 128, 0.25), (4096, 128, 1024, 64, 0.25),
+                                           (512, 4096, 2048, 64, 0.25), (2048, 512, 512, 32, 0.5),
+                                           (512, 256, 512, 16, 0.5)])
+def test_spmm_tc_matches_oracle(sb, oracle, M, N, K, V, alpha):
+    mask, W, B = synthetic(oracle, M, K, N, V, alpha)
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    n0 = sb.launch_count()
+    got = sb.spmm_execute(a, Bd).cpu().numpy()
+    assert sb.launch_count() == n0 + 1
+    want = oracle.spmm(p, B)
+    err = oracle.rel_frobenius(got, want)
+    assert err <= TOL, err
+    # bf16 output = the same fp32 accumulator rounded once (RNE), bit for bit
+    got16 = sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(got16, oracle.round16(got))
+
+
+def test_spmm_tc_equals_simt_within_tolerance_and_split_is_bitwise(sb, oracle):
+    mask, W, B = synthetic(oracle, 2048, 1024, 256, 64, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, 64)
+    Bd = dev(B, torch.bfloat16)
+    outs = {}
+    for split in (1, 2, 4):
+        sb.set_option("split", split)
+        outs[split] = sb.spmm_execute(a, Bd).cpu().numpy()
+    sb.set_option("split", 0)
+    sb.set_option("force_simt", 1)
+    simt = sb.spmm_execute(a, Bd).cpu().numpy()
+    sb.set_option("force_simt", 0)
+    assert np.array_equal(simt, oracle.spmm(p, B))  # CUDA-core path is bit-exact
+    assert np.array_equal(outs[1], outs[2]) and np.array_equal(outs[1], outs[4])
+    assert oracle.rel_frobenius(outs[1], simt) <= TOL
+
+
+@pytest.mark.parametrize("N", [8, 136, 200, 1000])
+def test_spmm_ragged_n(sb, oracle, N):
+    mask, W, B = synthetic(oracle, 1024, 512, N, 64, 0.2)
+    a, p = compress_both(sb, oracle, W, mask, 64)
+    got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
+    assert oracle.rel_frobenius(got, oracle.spmm(p, B)) <= TOL
+
+
+def test_spmm_ragged_and_empty_groups(sb, oracle):
+    """groups with different n_g (not multiples of 64) and n_g = 0 (zero rows,
+    src/spmm.cpp:103, 115-123)."""
+    rs = np.random.RandomState(11)
+    M, K, V, N = 64 * 24, 700, 64, 192
+    supports = []
+    for g in range(M // V):
+        n = [0, 1, 63, 64, 65, 130, 700][g % 7]
+        supports.append(np.sort(rs.choice(K, n, replace=False)))
+    perm = rs.permutation(M)
+    mask = np.zeros((M, K), np.uint8)
+    for r in range(M):
+        mask[perm[r], supports[r // V]] = 1
+    W = oracle.round16(oracle.random_dense(M, K, 5))
+    B = oracle.round16(oracle.random_dense(K, N, 6))
+    a, p = compress_both(sb, oracle, W, mask, V)
+    assert_same_packing(a, p, oracle)
+    got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
+    want = oracle.spmm(p, B)
+    assert oracle.rel_frobenius(got, want) <= TOL
+    zero_rows = [int(r) for g in range(M // V) if p.group_ncols[g] == 0
+                 for r in p.row_indices[g * V:(g + 1) * V]]
+    assert zero_rows and np.all(got[zero_rows] == 0)
+
+
+def test_spmm_unaligned_leading_dim_uses_simt(sb, oracle):
+    mask, W, B = synthetic(oracle, 256, 128, 13, 64, 0.5)
+    a, p = compress_both(sb, oracle, W, mask, 64)
+    got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
+    assert np.array_equal(got, oracle.spmm(p, B))  # N=13: ldb%8 != 0 -> exact path
+
+
+def test_spmm_fp16(sb, oracle):
+    cpg = 128
+    mask = oracle.random_shflbw_mask(1024, 512, 64, cpg, oracle.rng(1234))
+    W = oracle.round16(oracle.random_dense(1024, 512, 1), "f16")
+    B = oracle.round16(oracle.random_dense(512, 256, 2), "f16")
+    a = sb.compress_shflbw(dev(W), dev(mask), 64, dtype=torch.float16)
+    p = oracle.compress(W, mask, 64)
+    got = sb.spmm_execute(a, dev(B, torch.float16)).cpu().numpy()
+    assert oracle.rel_frobenius(got, oracle.spmm(p, B)) <= TOL
+
+
+def test_spmm_shape_errors(sb, oracle):
+    mask, W, B = synthetic(oracle, 128, 64, 16, 64, 0.5)
+    a, _ = compress_both(sb, oracle, W, mask, 64)
+    with pytest.raises(sb.ShapeMismatch):
+        sb.spmm_execute(a, torch.zeros(65, 16, dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(sb.BadParams):
+        sb.spmm_execute(a, dev(B, torch.bfloat16), cfg=sb.TileConfig(t_n=0))
+    with pytest.raises(sb.BadParams):
+        sb.spmm_execute(a, dev(B, torch.bfloat16), cfg=sb.TileConfig(pipe_stage=1))
+
+
+def test_sharded_groups_compact_plus_unpermute(sb, oracle):
+    """The multi-GPU data path on one device: per-shard compact rows,
+    concatenated (what all_gather produces), un-permuted == full SpMM."""
+    mask, W, B = synthetic(oracle, 2048, 512, 256, 64, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, 64)
+    Bd = dev(B, torch.bfloat16)
+    full = sb.spmm_execute(a, Bd)
+    G = a.group_count()
+    for world in (2, 4, 8):
+        parts = []
+        for rank in range(world):
+            g0, g1 = G * rank // world, G * (rank + 1) // world
+            out = torch.empty(((g1 - g0) * 64, 256), dtype=torch.float32, device="cuda")
+            parts.append(sb.spmm_groups(a, g0, g1, Bd, out, compact=True))
+        gathered = torch.cat(parts)
+        res = torch.empty_like(full)
+        sb.unpermute_rows(a.row_indices_ptr, gathered, res)
+        assert torch.equal(res, full)
+
+
+# ---------------------------------------------------------------- conv
+
+def test_conv_cases_bit_exact(sb, oracle):
+    for case in load_golden("conv_cases.json"):
+        crs = case["C"] * case["R"] * case["S"]
+        mask = np.array(case["mask"], np.uint8).reshape(case["Kf"], crs)
+        W = oracle.round16(oracle.random_dense(case["Kf"], crs, case["dense_seed"]))
+        x = oracle.round16(oracle.fill_uniform(oracle.rng(case["input_seed"]),
+                                               case["C"] * case["H"] * case["W"] * case["Nb"]).reshape(
+            case["C"], case["H"], case["W"], case["Nb"]))
+        geo = sb.ConvGeometry(case["R"], case["S"], case["stride"], case["pad"])
+        a, p = compress_both(sb, oracle, W, mask, case["V"])
+        got = sb.conv2d(a, dev(x, torch.bfloat16), geo).cpu().numpy()
+        want = oracle.conv2d(p, x, case["R"], case["S"], case["stride"], case["pad"])
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("C,H,Kf,R,pad,V,Nb", [(64, 56, 64, 3, 1, 64, 8), (32, 14, 128, 3, 1, 32, 4),
+                                               (64, 12, 256, 1, 0, 64, 16)])
+def test_conv_resnet_like(sb, oracle, C, H, Kf, R, pad, V, Nb):
+    crs = C * R * R
+    mask = oracle.random_shflbw_mask(Kf, crs, V, crs // 4, oracle.rng(1234))
+    W = oracle.round16(oracle.random_dense(Kf, crs, 1))
+    x = oracle.round16(oracle.fill_uniform(oracle.rng(7), C * H * H * Nb).reshape(C, H, H, Nb))
+    a, p = compress_both(sb, oracle, W, mask, V)
+    got = sb.conv2d(a, dev(x, torch.bfloat16), sb.ConvGeometry(R, R, 1, pad)).cpu().numpy()
+    want = oracle.conv2d(p, x, R, R, 1, pad)
+    assert oracle.rel_frobenius(got, want) <= TOL
+
+
+def test_conv_1x1_equals_spmm_bitwise(sb, oracle):
+    C, H, Wd, Nb, Kf, V = 64, 7, 8, 4, 128, 64
+    mask = oracle.random_shflbw_mask(Kf, C, V, 16, oracle.rng(3))
+    W = oracle.round16(oracle.random_dense(Kf, C, 1))
+    x = oracle.round16(oracle.fill_uniform(oracle.rng(4), C * H * Wd * Nb))
+    a, _ = compress_both(sb, oracle, W, mask, V)
+    xd = dev(x.reshape(C, H, Wd, Nb), torch.bfloat16)
+    out = sb.conv2d(a, xd, sb.ConvGeometry())
+    ref = sb.spmm_execute(a, xd.reshape(C, H * Wd * Nb))
+    assert torch.equal(out.reshape(Kf, -1), ref)
+
+
+def test_conv_geometry_errors(sb, oracle):
+    mask = oracle.random_shflbw_mask(4, 27, 2, 9, oracle.rng(59))
+    a = sb.compress_shflbw(dev(oracle.random_dense(4, 27, 1)), dev(mask), 2)
+    with pytest.raises(sb.BadGeometry):  # weight cols say C=3, input has C=2
+        sb.conv2d(a, torch.zeros(2, 6, 6, 1, device="cuda"), sb.ConvGeometry(3, 3))
+    with pytest.raises(sb.BadGeometry):  # (6-3) % 2 != 0
+        sb.conv2d(a, torch.zeros(3, 6, 6, 1, device="cuda"), sb.ConvGeometry(3, 3, 2))
