@@ -75,7 +75,13 @@ const char* shflbw_cu_last_error(void);
 int shflbw_cu_version(void);
 /* Tuning / testing knobs.  Keys: "force_simt" (1: use the CUDA-core kernel
  * for every V), "split" (cluster split of V for the tcgen05 kernel, 0 =
- * auto), "stages" (pipeline depth, 0 = auto).  Unknown key: BAD_PARAMS. */
+ * auto), "stages" (pipeline depth, 0 = auto), "pdl" (1 = default:
+ * programmatic dependent launch -- the SpMM prologue, which reads only the
+ * sparse matrix, overlaps the previous kernel on the stream; the activation
+ * B and the output C are touched only after the previous grid completes, so
+ * a matrix must not be written by work still in flight when an SpMM using it
+ * is enqueued -- shflbw_cu_compress / _upload return with it complete).
+ * Unknown key: BAD_PARAMS. */
 int shflbw_cu_set_option(const char* key, int64_t value);
 /* Number of kernels this library launched on the calling thread so far. */
 int64_t shflbw_cu_launch_count(void);

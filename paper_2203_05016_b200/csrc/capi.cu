@@ -12,7 +12,7 @@ namespace sbw {
 namespace {
 thread_local std::string g_error;
 thread_local int64_t g_launches = 0;
-std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0};
+std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0}, g_pdl{1};
 }  // namespace
 
 void set_error(const std::string& msg) { g_error = msg; }
@@ -30,6 +30,7 @@ int64_t option(const char* key) {
     if (!std::strcmp(key, "force_simt")) return g_force_simt.load();
     if (!std::strcmp(key, "split")) return g_split.load();
     if (!std::strcmp(key, "stages")) return g_stages.load();
+    if (!std::strcmp(key, "pdl")) return g_pdl.load();
     return 0;
 }
 
@@ -107,6 +108,7 @@ int shflbw_cu_set_option(const char* key, int64_t value) {
     if (!std::strcmp(key, "force_simt")) g_force_simt = value;
     else if (!std::strcmp(key, "split")) g_split = value;
     else if (!std::strcmp(key, "stages")) g_stages = value;
+    else if (!std::strcmp(key, "pdl")) g_pdl = value;
     else return fail(SHFLBW_BAD_PARAMS, std::string("unknown option ") + key);
     return SHFLBW_OK;
 }

@@ -744,6 +744,9 @@ int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M
             SBW_LAUNCHED("k_pack_values");
         }
     }
+    // the matrix is complete on return (SpMM prologues read it before their
+    // programmatic-launch wait, see the "pdl" option)
+    SBW_CUDA(cudaStreamSynchronize(s));
     return SHFLBW_OK;
 }
 
@@ -805,6 +808,7 @@ int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t
         SBW_CUDA(cudaStreamSynchronize(s));
         if (hf[1]) return cleanup(fail(SHFLBW_SHAPE_MISMATCH, "column index exceeds B rows or is not increasing"));
     }
+    SBW_CUDA(cudaStreamSynchronize(s));
     return SHFLBW_OK;
 }
 

@@ -78,6 +78,15 @@ struct WeightLayout {
     static constexpr uint32_t kSBO = 8 * kRowBytes;
 };
 
+constexpr int kMetaBlocks = 16;  // K blocks of column indices staged in smem at a time
+
+__device__ __forceinline__ void grid_dependency_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 template <int DT, int VS, int CS>
 __global__ void __launch_bounds__(kThreads, 1)
     k_spmm_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
@@ -91,11 +100,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int stages = p.stages;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStageBytes);
+    int32_t* meta_s = reinterpret_cast<int32_t*>(smem + stages * kStageBytes);  // kMetaBlocks*64
+    int32_t* rows_s = meta_s + kMetaBlocks * kBlockK;                           // VS
+    uint64_t* full = reinterpret_cast<uint64_t*>(rows_s + (VS < 2 ? 2 : VS));
     uint64_t* empty = full + stages;
     uint64_t* accum = empty + stages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
-    int32_t* rows_s = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
@@ -106,6 +116,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nkb = (p.group_ptr[g + 1] - gp) / kBlockK;
     const int vbase = static_cast<int>(rank) * VS;
 
+    // ---- prologue: everything here reads only the (static) sparse matrix,
+    //      so with PDL it overlaps the tail of the previous kernel ----------
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
@@ -129,20 +141,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_d = *tmem_slot;
+    if (threadIdx.x == 0) grid_launch_dependents();
 
     if (warp == 0) {
         // ---------------- producer ----------------
         const int slab = lane >> 4, rg = lane & 15;
         const bool issue_gather = CS == 1 || (lane % CS) == static_cast<int>(rank);
+        const int pre = nkb < stages ? nkb : stages;
+        // weights of the first `pre` stages and the first index window: no
+        // dependency on the previous grid
+        if (lane == 0) {
+            for (int kb = 0; kb < pre; ++kb) {
+                mbar_arrive_expect_tx(&full[kb], kStageBytes);
+#pragma unroll
+                for (int sl = 0; sl < WL::kSlabs; ++sl)
+                    tma_load_2d(smem + kb * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[kb],
+                                vbase + sl * 64, gp + kb * kBlockK);
+            }
+        }
+        auto stage_meta = [&](int kb) {  // next window of column indices, coalesced
+            const int nb = nkb - kb < kMetaBlocks ? nkb - kb : kMetaBlocks;
+            const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + kb * kBlockK);
+            for (int i = lane; i < nb * (kBlockK / 4); i += 32) reinterpret_cast<int4*>(meta_s)[i] = src[i];
+            __syncwarp();
+        };
+        if (nkb > 0) stage_meta(0);
+        grid_dependency_wait();  // B may be the previous kernel's output
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % stages;
-            mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+            const int win = kb % kMetaBlocks;
+            if (win == 0 && kb > 0) stage_meta(kb);
             unsigned char* a_st = smem + s * kStageBytes;
-            unsigned char* w_st = a_st + kABytes;
-            if (lane == 0) mbar_arrive_expect_tx(&full[s], kStageBytes);
-            __syncwarp();
+            if (kb >= pre) {
+                mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&full[s], kStageBytes);
+#pragma unroll
+                    for (int sl = 0; sl < WL::kSlabs; ++sl)
+                        tma_load_2d(a_st + kABytes + sl * WL::kSlabBytes, &tmW, &full[s], vbase + sl * 64,
+                                    gp + kb * kBlockK);
+                }
+                __syncwarp();
+            }
             if (issue_gather) {
-                const int4 ci = *reinterpret_cast<const int4*>(p.col_idx + gp + kb * kBlockK + 4 * rg);
+                const int4 ci = reinterpret_cast<const int4*>(meta_s)[win * (kBlockK / 4) + rg];
                 void* dst = a_st + slab * (kABytes / 2) + rg * 512;
                 if (CS == 1)
                     tma_gather4(dst, &tmB, &full[s], n0 + slab * 64, ci.x, ci.y, ci.z, ci.w);
@@ -150,12 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_gather4_mc(dst, &tmB, &full[s], static_cast<uint16_t>((1u << CS) - 1u),
                                    n0 + slab * 64, ci.x, ci.y, ci.z, ci.w);
             }
-            if (lane == 0) {
-#pragma unroll
-                for (int sl = 0; sl < WL::kSlabs; ++sl)
-                    tma_load_2d(w_st + sl * WL::kSlabBytes, &tmW, &full[s], vbase + sl * 64,
-                                gp + kb * kBlockK);
-            }
+            __syncwarp();
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
@@ -185,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue: TMEM -> permuted rows of C ----------------
     mbar_wait(accum, 0);
     tc_fence_after();
+    grid_dependency_wait();  // C may still be read by the previous kernel
     const int m = warp * 32 + lane;
     const int n = n0 + m;
     const bool live = n < p.N;
@@ -272,7 +310,8 @@ template <int DT, int VS, int CS>
 int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
               cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
-    const size_t smem = static_cast<size_t>(prm.stages) * kStage + 1024 + 256 + VS * 4;
+    const size_t smem = static_cast<size_t>(prm.stages) * kStage + 1024 + kMetaBlocks * kBlockK * 4 +
+                        (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 2) * 8 + 16;
     auto kern = k_spmm_tc<DT, VS, CS>;
     SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
@@ -280,13 +319,15 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = option("pdl") ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, prm));
     count_launch();
     return SHFLBW_OK;
