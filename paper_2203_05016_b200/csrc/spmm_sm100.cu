@@ -51,7 +51,6 @@ namespace {
 constexpr int kBlockN = 128;  // output columns per CTA (MMA M)
 constexpr int kBlockK = 64;   // sparse columns per pipeline stage
 constexpr int kABytes = kBlockK * kBlockN * 2;  // 16 KB, two 64-column slabs
-constexpr int kThreads = 128;
 
 struct TcParams {
     const int32_t* row_indices;
@@ -65,7 +64,21 @@ struct TcParams {
     int c_dtype;
     int compact;
     int stages;
+    int cps;         // activation slabs filled by cp.async (0..2); the rest by TMA gather4
+    const void* B;   // activations (cp.async path)
+    int64_t ldb;
+    unsigned long long* trace;  // optional per-CTA event timestamps (development)
+    int bulk_out;               // 1: C rows 16-byte aligned -> smem-staged bulk stores
 };
+
+__device__ __forceinline__ void trace_event(unsigned long long* tr, int e) {
+    if (tr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+        tr[cta * 8 + e] = t;
+    }
+}
 
 template <int VS>
 struct WeightLayout {
@@ -87,20 +100,32 @@ __device__ __forceinline__ void grid_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+// warp roles (192 threads):
+//   warp 0  : stage bookkeeping -- waits for a free slot, arms the full
+//             barrier with the stage's byte count, loads the weight tile
+//   warp 1  : TMEM allocator + single-thread MMA issuer
+//   warps 2-5: gather issuers (8 gather4 each per K block, so the
+//             per-instruction ELECT/R2UR issue loop runs on all four SM
+//             sub-partitions in parallel), then the epilogue (warp w owns
+//             TMEM lanes 32*(w%4)..+31)
+constexpr int kGatherWarps = 4;
+constexpr int kThreadsTc = 64 + 32 * kGatherWarps;
+
 template <int DT, int VS, int CS>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsTc, 1)
     k_spmm_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
               TcParams p) {
     using WL = WeightLayout<VS>;
     constexpr int kStageBytes = kABytes + WL::kBytes;
     constexpr uint32_t kTmemCols = VS < 32 ? 32 : VS;
     constexpr uint32_t kIdesc = umma_idesc_f16(DT == SHFLBW_BF16 ? 1 : 0, kBlockN, VS);
+    using T = typename Elem<DT>::T;
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int stages = p.stages;
-    int32_t* meta_s = reinterpret_cast<int32_t*>(smem + stages * kStageBytes);  // kMetaBlocks*64
+    int32_t* meta_s = reinterpret_cast<int32_t*>(smem + stages * kStageBytes);  // [kMetaBlocks][64]
     int32_t* rows_s = meta_s + kMetaBlocks * kBlockK;                           // VS
     uint64_t* full = reinterpret_cast<uint64_t*>(rows_s + (VS < 2 ? 2 : VS));
     uint64_t* empty = full + stages;
@@ -115,85 +140,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gp = p.group_ptr[g];
     const int nkb = (p.group_ptr[g + 1] - gp) / kBlockK;
     const int vbase = static_cast<int>(rank) * VS;
+    const int cps = p.cps;
+    const int et = threadIdx.x - 64;  // gather/epilogue thread 0..127 (warps 2..5)
+    if (threadIdx.x == 0) trace_event(p.trace, 0);
 
-    // ---- prologue: everything here reads only the (static) sparse matrix,
-    //      so with PDL it overlaps the tail of the previous kernel ----------
+    // gather warps stage a window of column indices (all 64 per K block)
+    auto stage_meta = [&](int kb0) {
+        const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
+        const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + kb0 * kBlockK);
+        for (int i = et; i < nb * (kBlockK / 4); i += 128) reinterpret_cast<int4*>(meta_s)[i] = src[i];
+    };
+
+    // ---- prologue (reads only the static sparse matrix: overlaps the
+    //      previous kernel under PDL) ---------------------------------------
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1 + (cps > 0 ? 32 * kGatherWarps : 0));
             mbar_init(&empty[s], CS);
         }
         mbar_init(accum, 1);
         fence_mbar_init();
-    }
-    if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmW);
     }
-    if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
-    for (int v = threadIdx.x; v < VS; v += kThreads) {
-        const int64_t gr = static_cast<int64_t>(g) * p.V + vbase + v;
-        rows_s[v] = p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
-                              : p.row_indices[gr];
-    }
+    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
     tc_fence_before();
     if (CS > 1) cluster_sync();
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_d = *tmem_slot;
-    if (threadIdx.x == 0) grid_launch_dependents();
+    if (threadIdx.x == 0) {
+        grid_launch_dependents();
+        trace_event(p.trace, 1);
+    }
 
     if (warp == 0) {
-        // ---------------- producer ----------------
-        const int slab = lane >> 4, rg = lane & 15;
-        const bool issue_gather = CS == 1 || (lane % CS) == static_cast<int>(rank);
-        const int pre = nkb < stages ? nkb : stages;
-        // weights of the first `pre` stages and the first index window: no
-        // dependency on the previous grid
+        // ---------------- stage bookkeeping + weights ----------------
         if (lane == 0) {
-            for (int kb = 0; kb < pre; ++kb) {
-                mbar_arrive_expect_tx(&full[kb], kStageBytes);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % stages;
+                if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[s], (2 - cps) * (kABytes / 2) + WL::kBytes);
 #pragma unroll
                 for (int sl = 0; sl < WL::kSlabs; ++sl)
-                    tma_load_2d(smem + kb * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[kb],
+                    tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
                                 vbase + sl * 64, gp + kb * kBlockK);
             }
         }
-        auto stage_meta = [&](int kb) {  // next window of column indices, coalesced
-            const int nb = nkb - kb < kMetaBlocks ? nkb - kb : kMetaBlocks;
-            const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + kb * kBlockK);
-            for (int i = lane; i < nb * (kBlockK / 4); i += 32) reinterpret_cast<int4*>(meta_s)[i] = src[i];
-            __syncwarp();
-        };
-        if (nkb > 0) stage_meta(0);
-        grid_dependency_wait();  // B may be the previous kernel's output
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % stages;
-            const int win = kb % kMetaBlocks;
-            if (win == 0 && kb > 0) stage_meta(kb);
-            unsigned char* a_st = smem + s * kStageBytes;
-            if (kb >= pre) {
-                mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[s], kStageBytes);
-#pragma unroll
-                    for (int sl = 0; sl < WL::kSlabs; ++sl)
-                        tma_load_2d(a_st + kABytes + sl * WL::kSlabBytes, &tmW, &full[s], vbase + sl * 64,
-                                    gp + kb * kBlockK);
-                }
-                __syncwarp();
-            }
-            if (issue_gather) {
-                const int4 ci = reinterpret_cast<const int4*>(meta_s)[win * (kBlockK / 4) + rg];
-                void* dst = a_st + slab * (kABytes / 2) + rg * 512;
-                if (CS == 1)
-                    tma_gather4(dst, &tmB, &full[s], n0 + slab * 64, ci.x, ci.y, ci.z, ci.w);
-                else
-                    tma_gather4_mc(dst, &tmB, &full[s], static_cast<uint16_t>((1u << CS) - 1u),
-                                   n0 + slab * 64, ci.x, ci.y, ci.z, ci.w);
-            }
-            __syncwarp();
-        }
+        __syncwarp();
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
@@ -201,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = kb % stages;
                 mbar_wait(&full[s], (kb / stages) & 1);
                 tc_fence_after();
+                if (kb == 0) trace_event(p.trace, 3);
                 const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
                 const uint32_t w_addr = a_addr + kABytes;
 #pragma unroll
@@ -213,47 +208,142 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (CS == 1) umma_commit(&empty[s]);
                 else umma_commit_mc(&empty[s], static_cast<uint16_t>((1u << CS) - 1u));
             }
+            trace_event(p.trace, 4);
             if (nkb > 0) umma_commit(accum);
             else mbar_arrive(accum);
         }
         __syncwarp();
-    }
-
-    // ---------------- epilogue: TMEM -> permuted rows of C ----------------
-    mbar_wait(accum, 0);
-    tc_fence_after();
-    grid_dependency_wait();  // C may still be read by the previous kernel
-    const int m = warp * 32 + lane;
-    const int n = n0 + m;
-    const bool live = n < p.N;
-    const uint32_t t_row = tmem_d + (static_cast<uint32_t>(warp * 32) << 16);
-#pragma unroll
-    for (int c = 0; c < (VS + 31) / 32; ++c) {
-        constexpr int kW = VS < 32 ? VS : 32;
-        uint32_t r[32];
-        if (nkb > 0) {
-            if (kW == 32) tmem_ld32(t_row + c * 32, r);
-            else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
-            tmem_ld_wait();
-        } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = 0u;
+    } else {
+        // ---------------- activation producers ----------------
+        const int gw = warp - 2;
+        // TMA part: slabs [0, 2-cps): row group rg of slab sl, 16 row groups
+        // per slab, spread over the 4 warps' first lanes
+        const int tma_slabs = 2 - cps;
+        const int my_gathers = tma_slabs * 4;  // per warp per K block
+        const int t_sl = lane >> 2, t_rq = lane & 3, t_rg = gw * 4 + t_rq;
+        const int gi = gw * 8 + lane;
+        const bool t_issue = lane < my_gathers && (CS == 1 || (gi % CS) == static_cast<int>(rank));
+        // cp.async part: slabs [2-cps, 2): cps*512 16-byte chunks per K block
+        const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
+        const T* Bp = static_cast<const T*>(p.B);
+        if (nkb > 0) stage_meta(0);  // static metadata: before the dependency wait
+        grid_dependency_wait();  // B may be the previous kernel's output
+        if (et == 0) trace_event(p.trace, 2);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % stages;
+            const int win = kb % kMetaBlocks;
+            if (win == 0 && kb > 0) {
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // all done with the old window
+                stage_meta(kb);
+            }
+            if (win == 0) asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+            unsigned char* a_st = smem + s * kStageBytes;
+            const int32_t* mk = meta_s + win * kBlockK;
+            if (t_issue) {
+                const int4 ci = reinterpret_cast<const int4*>(mk)[t_rg];
+                void* dst = a_st + t_sl * (kABytes / 2) + t_rg * 512;
+                if (CS == 1)
+                    tma_gather4(dst, &tmB, &full[s], n0 + t_sl * 64, ci.x, ci.y, ci.z, ci.w);
+                else
+                    tma_gather4_mc(dst, &tmB, &full[s], static_cast<uint16_t>((1u << CS) - 1u),
+                                   n0 + t_sl * 64, ci.x, ci.y, ci.z, ci.w);
+            }
+            if (cps > 0) {
+                const uint32_t a_u32 = smem_u32(a_st);
+                for (int id = et; id < cps * 512; id += 128) {
+                    const int r = id >> cpr_log2, c = id & ((1 << cpr_log2) - 1);
+                    const int sl = tma_slabs + (c >> 3), cc = c & 7;
+                    const int col = mk[r];
+                    const int n = n0 + sl * 64 + cc * 8;
+                    const bool ok = col >= 0 && n < p.N;
+                    const T* src = ok ? Bp + static_cast<int64_t>(col) * p.ldb + n : Bp;
+                    cp_async16(a_u32 + sl * (kABytes / 2) + r * 128 + ((cc ^ (r & 7)) << 4), src, ok);
+                }
+                cp_async_arrive_noinc(&full[s]);
+            }
+            __syncwarp();
         }
-        if (live) {
+        // output row map for the epilogue, loaded while the MMAs run
+        for (int v = et; v < VS; v += 128) {
+            const int64_t gr = static_cast<int64_t>(g) * p.V + vbase + v;
+            rows_s[v] = p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
+                                  : p.row_indices[gr];
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+
+        // ---------------- epilogue: TMEM -> permuted rows of C ----------------
+        mbar_wait(accum, 0);
+        tc_fence_after();
+        if (et == 0) trace_event(p.trace, 5);
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int m = q * 32 + lane;
+        const int n = n0 + m;
+        const bool live = n < p.N;
+        const uint32_t t_row = tmem_d + (static_cast<uint32_t>(q * 32) << 16);
+        const int esz = p.c_dtype == SHFLBW_F32 ? 4 : 2;
+        // all MMAs are complete (accum), so the stage buffers are free: they
+        // hold the [VS][128] output tile for the bulk row stores
+        unsigned char* ctile = smem;
 #pragma unroll
-            for (int i = 0; i < kW; ++i) {
-                const int64_t off = static_cast<int64_t>(rows_s[c * 32 + i]) * p.ldc + n;
-                const float x = __uint_as_float(r[i]);
-                if (p.c_dtype == SHFLBW_F32) static_cast<float*>(p.C)[off] = x;
-                else if (p.c_dtype == SHFLBW_BF16) static_cast<__nv_bfloat16*>(p.C)[off] = __float2bfloat16_rn(x);
-                else static_cast<__half*>(p.C)[off] = __float2half_rn(x);
+        for (int c = 0; c < (VS + 31) / 32; ++c) {
+            constexpr int kW = VS < 32 ? VS : 32;
+            uint32_t r[32];
+            if (nkb > 0) {
+                if (kW == 32) tmem_ld32(t_row + c * 32, r);
+                else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) r[i] = 0u;
+            }
+            if (p.bulk_out) {
+#pragma unroll
+                for (int i = 0; i < kW; ++i) {
+                    const int v = c * 32 + i;
+                    const float x = __uint_as_float(r[i]);
+                    if (p.c_dtype == SHFLBW_F32)
+                        reinterpret_cast<float*>(ctile)[v * kBlockN + m] = x;
+                    else if (p.c_dtype == SHFLBW_BF16)
+                        reinterpret_cast<__nv_bfloat16*>(ctile)[v * kBlockN + m] = __float2bfloat16_rn(x);
+                    else
+                        reinterpret_cast<__half*>(ctile)[v * kBlockN + m] = __float2half_rn(x);
+                }
+            } else if (live) {
+#pragma unroll
+                for (int i = 0; i < kW; ++i) {
+                    const int64_t off = static_cast<int64_t>(rows_s[c * 32 + i]) * p.ldc + n;
+                    const float x = __uint_as_float(r[i]);
+                    if (p.c_dtype == SHFLBW_F32) static_cast<float*>(p.C)[off] = x;
+                    else if (p.c_dtype == SHFLBW_BF16)
+                        static_cast<__nv_bfloat16*>(p.C)[off] = __float2bfloat16_rn(x);
+                    else static_cast<__half*>(p.C)[off] = __float2half_rn(x);
+                }
+            }
+        }
+        if (p.bulk_out) {
+            // coalesced 16-byte stores of the staged tile: one output row is
+            // 128*esz bytes = 8 or 16... lanes; rows go through row_indices
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int lanes_per_row = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
+            const int rows_per_inst = 32 / lanes_per_row;
+            const int chunk = lane % lanes_per_row;
+            const int nn = n0 + chunk * (16 / esz);
+            for (int v = q * rows_per_inst + lane / lanes_per_row; v < VS; v += 4 * rows_per_inst) {
+                if (nn < p.N) {
+                    const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
+                    *reinterpret_cast<int4*>(static_cast<char*>(p.C) +
+                                             (static_cast<int64_t>(rows_s[v]) * p.ldc + nn) * esz) = x;
+                }
             }
         }
     }
+    if (et == 0) trace_event(p.trace, 6);
     tc_fence_before();
-    if (CS > 1) cluster_sync();
+    if (CS > 1) cluster_sync_relaxed();  // only smem lifetime matters here
     else __syncthreads();
-    if (warp == 2) tmem_dealloc(tmem_d, kTmemCols);
+    if (warp == 1) tmem_dealloc(tmem_d, kTmemCols);
+    if (threadIdx.x == 0) trace_event(p.trace, 7);
 }
 
 // ---------------- host side ----------------
@@ -316,7 +406,7 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_tiles * CS, groups, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.blockDim = dim3(kThreadsTc, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -392,6 +482,18 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.N = b.N;
     prm.c_dtype = c.dtype;
     prm.compact = c.compact;
+    prm.B = b.ptr;
+    prm.ldb = b.ldb;
+    prm.cps = static_cast<int>(option("cp_async_slabs"));
+    prm.trace = reinterpret_cast<unsigned long long*>(option("trace"));
+    {
+        const int esz = c.dtype == SHFLBW_F32 ? 4 : 2;
+        const bool aligned = (reinterpret_cast<uintptr_t>(c.ptr) % 16 == 0) && ((c.ldc * esz) % 16 == 0) &&
+                             ((static_cast<int64_t>(b.N) * esz) % 16 == 0);
+        prm.bulk_out = aligned && !option("no_bulk_out") ? 1 : 0;
+    }
+    if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
+    if (cs > 1 && prm.cps > 0) prm.cps = 0;  // multicast clusters use TMA gathers only
     int stages = static_cast<int>(option("stages"));
     if (stages <= 0) stages = vs >= 128 ? 3 : 4;
     const int max_kb = (a->cols + kBlockK - 1) / kBlockK;

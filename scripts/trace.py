@@ -1,0 +1,51 @@
+"""Per-CTA event timeline of one SpMM launch (development tool).
+
+Events (globaltimer ns): 0 entry, 1 setup done, 2 grid-dependency wait
+returned, 3 first stage full (MMA), 4 last MMA issued, 5 accumulator ready,
+6 epilogue stores done, 7 exit.  Prints percentiles relative to the
+earliest CTA entry.
+"""
+import argparse, os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import bench
+import paper_2203_05016_b200 as sb
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="ns")
+ap.add_argument("--opts", default="")
+args = ap.parse_args()
+wl = bench.WORKLOADS[args.workload]
+M, N, K, V, alpha = wl["M"], wl["N"], wl["K"], wl["V"], wl["alpha"]
+dev = torch.device("cuda", 0)
+cpg = int(round(alpha * K))
+mask = torch.from_numpy(bench.synth_mask(M, K, V, cpg, 1234)).to(dev)
+a = sb.compress_shflbw(bench.uniform_bf16(torch, (M, K), 100, dev), mask, V)
+B = bench.uniform_bf16(torch, (K, N), 200, dev)
+C = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+for kv in [x for x in args.opts.split(",") if x]:
+    k, v = kv.split("=")
+    sb.set_option(k, int(v))
+tr = torch.zeros(1 << 20, dtype=torch.int64, device=dev)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+for it in range(3):
+    flush.fill_(it)  # cold L2
+    torch.cuda.synchronize()
+    tr.zero_()
+    sb.set_option("trace", tr.data_ptr())
+    sb.spmm_execute(a, B, out=C)
+    torch.cuda.synchronize()
+    sb.set_option("trace", 0)
+t = tr.cpu().numpy().reshape(-1, 8)
+t = t[t[:, 0] > 0]
+t0 = t[:, 0].min()
+rel = (t - t0) / 1000.0
+names = ["entry", "setup", "dep_wait", "first_full", "last_mma", "accum", "epi_done", "exit"]
+print(f"{args.workload} {args.opts}: {len(t)} CTAs, span {rel[:, 7].max():.2f} us")
+for e, nm in enumerate(names):
+    col = rel[:, e]
+    col = col[t[:, e] > 0]
+    if len(col):
+        print(f"  {nm:10s} min {col.min():7.2f}  p50 {np.median(col):7.2f}  max {col.max():7.2f} us")

@@ -251,6 +251,24 @@ def test_spmm_tc_equals_simt_within_tolerance_and_split_is_bitwise(sb, oracle):
     assert oracle.rel_frobenius(outs[1], simt) <= TOL
 
 
+@pytest.mark.parametrize("N", [128, 200, 1000])
+def test_spmm_cp_async_producers_bitwise(sb, oracle, N):
+    """Activation tile filled by TMA gather4, by cp.async (manual 128B
+    swizzle), or half/half: identical operands -> identical bits."""
+    mask, W, B = synthetic(oracle, 1024, 1024, N, 64, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, 64)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("split", 1)
+    outs = []
+    for cps in (0, 1, 2):
+        sb.set_option("cp_async_slabs", cps)
+        outs.append(sb.spmm_execute(a, Bd).cpu().numpy())
+    sb.set_option("cp_async_slabs", 0)
+    sb.set_option("split", 0)
+    assert oracle.rel_frobenius(outs[0], oracle.spmm(p, B)) <= TOL
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
 @pytest.mark.parametrize("N", [8, 136, 200, 1000])
 def test_spmm_ragged_n(sb, oracle, N):
     mask, W, B = synthetic(oracle, 1024, 512, N, 64, 0.2)
