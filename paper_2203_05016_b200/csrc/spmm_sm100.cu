@@ -68,7 +68,10 @@ struct TcParams {
     const void* B;   // activations (cp.async path)
     int64_t ldb;
     unsigned long long* trace;  // optional per-CTA event timestamps (development)
-    int bulk_out;               // 1: C rows 16-byte aligned -> smem-staged bulk stores
+    int bulk_out;               // 1: C rows 16-byte aligned -> smem-staged vector stores
+    int bw;                     // MN block width of the activation tile (64 | 32 | 16 elements)
+    // implicit-GEMM conv geometry (KIND 1)
+    int Nb, H, W, RS, S, stride, pad, Q, PQ;
 };
 
 __device__ __forceinline__ void trace_event(unsigned long long* tr, int e) {
@@ -111,7 +114,7 @@ __device__ __forceinline__ void grid_launch_dependents() {
 constexpr int kGatherWarps = 4;
 constexpr int kThreadsTc = 64 + 32 * kGatherWarps;
 
-template <int DT, int VS, int CS>
+template <int DT, int VS, int CS, int KIND>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_spmm_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
               TcParams p) {
@@ -190,6 +193,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         __syncwarp();
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
+        // activation operand: MN-major, MN blocks of p.bw elements, swizzle = block row bytes
+        const uint32_t a_row = static_cast<uint32_t>(p.bw) * 2;
+        const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
         if (lane == 0) {
             for (int kb = 0; kb < nkb; ++kb) {
                 const int s = kb % stages;
@@ -200,7 +206,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 const uint32_t w_addr = a_addr + kABytes;
 #pragma unroll
                 for (int ks = 0; ks < kBlockK / 16; ++ks) {
-                    const uint64_t adesc = umma_smem_desc(a_addr + ks * 16 * 128, kABytes / 2, 1024, 2);
+                    const uint64_t adesc = umma_smem_desc(a_addr + ks * 16 * a_row, kBlockK * a_row, 8 * a_row,
+                                                          a_layout);
                     const uint64_t bdesc = umma_smem_desc(w_addr + ks * 16 * WL::kRowBytes,
                                                           WL::kSlabBytes, WL::kSBO, WL::kLayout);
                     umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
@@ -219,11 +226,32 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         // TMA part: slabs [0, 2-cps): row group rg of slab sl, 16 row groups
         // per slab, spread over the 4 warps' first lanes
         const int tma_slabs = 2 - cps;
-        const int my_gathers = tma_slabs * 4;  // per warp per K block
-        const int t_sl = lane >> 2, t_rq = lane & 3, t_rg = gw * 4 + t_rq;
-        const int gi = gw * 8 + lane;
-        const bool t_issue = lane < my_gathers && (CS == 1 || (gi % CS) == static_cast<int>(rank));
-        // cp.async part: slabs [2-cps, 2): cps*512 16-byte chunks per K block
+        const int nblk = KIND == 0 ? tma_slabs : kBlockN / p.bw;  // MN blocks filled by TMA
+        const int blk_bytes = kBlockK * p.bw * 2;
+        const int per_warp = 16 * nblk / kGatherWarps;              // gather4s per warp per K block
+        const int gi = gw * per_warp + lane;                        // this lane's gather
+        const int g_rg = gi & 15, g_b = gi >> 4;
+        const bool t_issue = lane < per_warp && (CS == 1 || (gi % CS) == static_cast<int>(rank));
+        // conv: this gather's output positions (fixed for the CTA)
+        int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
+        bool g_pos_ok = true;
+        if (KIND == 1) {
+            const int base_n = n0 + g_b * p.bw;
+            const int pos = base_n / p.Nb;
+            g_x = base_n - pos * p.Nb;
+            g_pos_ok = pos < p.PQ;
+            g_p0 = (pos / p.Q) * p.stride - p.pad;
+            g_q0 = (pos % p.Q) * p.stride - p.pad;
+        }
+        auto conv_row = [&](int c) -> int {
+            if (c < 0 || !g_pos_ok) return -1;
+            const int ch = c / p.RS, rs = c - ch * p.RS;
+            const int r = rs / p.S, sx = rs - r * p.S;
+            const int h = g_p0 + r, w = g_q0 + sx;
+            if (h < 0 || h >= p.H || w < 0 || w >= p.W) return -1;
+            return (ch * p.H + h) * p.W + w;
+        };
+        // cp.async part (SpMM only): slabs [2-cps, 2): cps*512 16-byte chunks per K block
         const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
         const T* Bp = static_cast<const T*>(p.B);
         if (nkb > 0) stage_meta(0);  // static metadata: before the dependency wait
@@ -241,13 +269,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             unsigned char* a_st = smem + s * kStageBytes;
             const int32_t* mk = meta_s + win * kBlockK;
             if (t_issue) {
-                const int4 ci = reinterpret_cast<const int4*>(mk)[t_rg];
-                void* dst = a_st + t_sl * (kABytes / 2) + t_rg * 512;
+                int4 ci = reinterpret_cast<const int4*>(mk)[g_rg];
+                if (KIND == 1) {
+                    ci.x = conv_row(ci.x);
+                    ci.y = conv_row(ci.y);
+                    ci.z = conv_row(ci.z);
+                    ci.w = conv_row(ci.w);
+                }
+                void* dst = a_st + g_b * blk_bytes + g_rg * (4 * p.bw * 2);
                 if (CS == 1)
-                    tma_gather4(dst, &tmB, &full[s], n0 + t_sl * 64, ci.x, ci.y, ci.z, ci.w);
+                    tma_gather4(dst, &tmB, &full[s], g_x, ci.x, ci.y, ci.z, ci.w);
                 else
-                    tma_gather4_mc(dst, &tmB, &full[s], static_cast<uint16_t>((1u << CS) - 1u),
-                                   n0 + t_sl * 64, ci.x, ci.y, ci.z, ci.w);
+                    tma_gather4_mc(dst, &tmB, &full[s], static_cast<uint16_t>((1u << CS) - 1u), g_x, ci.x,
+                                   ci.y, ci.z, ci.w);
             }
             if (cps > 0) {
                 const uint32_t a_u32 = smem_u32(a_st);
@@ -396,13 +430,13 @@ int num_sms() {
     return sms;
 }
 
-template <int DT, int VS, int CS>
+template <int DT, int VS, int CS, int KIND>
 int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
               cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
     const size_t smem = static_cast<size_t>(prm.stages) * kStage + 1024 + kMetaBlocks * kBlockK * 4 +
                         (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 2) * 8 + 16;
-    auto kern = k_spmm_tc<DT, VS, CS>;
+    auto kern = k_spmm_tc<DT, VS, CS, KIND>;
     SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_tiles * CS, groups, 1);
@@ -424,24 +458,25 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
 }
 
 template <int DT, int VS>
-int dispatch_cs(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles,
-                int groups, cudaStream_t s) {
+int dispatch_cs(int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm,
+                int n_tiles, int groups, cudaStream_t s) {
+    if (kind == 1) return launch_tc<DT, VS, 1, 1>(tmB, tmW, prm, n_tiles, groups, s);
     switch (cs) {
-        case 1: return launch_tc<DT, VS, 1>(tmB, tmW, prm, n_tiles, groups, s);
-        case 2: return launch_tc<DT, VS, 2>(tmB, tmW, prm, n_tiles, groups, s);
-        case 4: return launch_tc<DT, VS, 4>(tmB, tmW, prm, n_tiles, groups, s);
+        case 1: return launch_tc<DT, VS, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 2: return launch_tc<DT, VS, 2, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 4: return launch_tc<DT, VS, 4, 0>(tmB, tmW, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }
 
 template <int DT>
-int dispatch_vs(int vs, int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm,
+int dispatch_vs(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm,
                 int n_tiles, int groups, cudaStream_t s) {
     switch (vs) {
-        case 16: return dispatch_cs<DT, 16>(cs, tmB, tmW, prm, n_tiles, groups, s);
-        case 32: return dispatch_cs<DT, 32>(cs, tmB, tmW, prm, n_tiles, groups, s);
-        case 64: return dispatch_cs<DT, 64>(cs, tmB, tmW, prm, n_tiles, groups, s);
-        case 128: return dispatch_cs<DT, 128>(cs, tmB, tmW, prm, n_tiles, groups, s);
+        case 16: return dispatch_cs<DT, 16>(cs, kind, tmB, tmW, prm, n_tiles, groups, s);
+        case 32: return dispatch_cs<DT, 32>(cs, kind, tmB, tmW, prm, n_tiles, groups, s);
+        case 64: return dispatch_cs<DT, 64>(cs, kind, tmB, tmW, prm, n_tiles, groups, s);
+        case 128: return dispatch_cs<DT, 128>(cs, kind, tmB, tmW, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }
@@ -451,10 +486,18 @@ int dispatch_vs(int vs, int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, 
 int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b, const OutSpec& c,
             cudaStream_t s) {
     const int V = a->v;
-    if (b.kind != 0) return SHFLBW_UNSUPPORTED;
     if (V != 16 && V != 32 && V != 64 && V != 128) return SHFLBW_UNSUPPORTED;
-    if (b.ldb % 8 != 0 || (reinterpret_cast<uintptr_t>(b.ptr) & 15) != 0 || b.N <= 0 || b.K <= 0)
-        return SHFLBW_UNSUPPORTED;
+    if ((reinterpret_cast<uintptr_t>(b.ptr) & 15) != 0 || b.N <= 0 || b.K <= 0) return SHFLBW_UNSUPPORTED;
+    int bw = 64;
+    if (b.kind == 0) {
+        if (b.ldb % 8 != 0) return SHFLBW_UNSUPPORTED;
+    } else {
+        // conv: rows of the [C*H*W][Nb] view are Nb contiguous elements
+        if (b.Nb == 16 || b.Nb == 32) bw = b.Nb;
+        else if (b.Nb % 64 == 0) bw = 64;
+        else return SHFLBW_UNSUPPORTED;
+        if (static_cast<int64_t>(b.C) * b.H * b.W >= (1LL << 31)) return SHFLBW_UNSUPPORTED;
+    }
     const int groups = g_end - g_begin;
     if (groups <= 0) return SHFLBW_OK;
     if (groups > 65535) return SHFLBW_UNSUPPORTED;
@@ -467,6 +510,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const int64_t units = static_cast<int64_t>(n_tiles) * groups;
         while (cs < 4 && V / (cs * 2) >= 16 && units * cs * 2 <= num_sms()) cs *= 2;
     }
+    if (b.kind == 1) cs = 1;
     if (cs != 1 && cs != 2 && cs != 4) return fail(SHFLBW_BAD_PARAMS, "split must be 1, 2 or 4");
     if (V % cs != 0 || V / cs < 16) return SHFLBW_UNSUPPORTED;
     const int vs = V / cs;
@@ -484,7 +528,19 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.compact = c.compact;
     prm.B = b.ptr;
     prm.ldb = b.ldb;
-    prm.cps = static_cast<int>(option("cp_async_slabs"));
+    prm.bw = bw;
+    prm.Nb = b.Nb;
+    prm.H = b.H;
+    prm.W = b.W;
+    prm.RS = b.R * b.S;
+    prm.S = b.S;
+    prm.stride = b.stride;
+    prm.pad = b.pad;
+    prm.Q = b.Q;
+    prm.PQ = b.P * b.Q;
+    prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
+    if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
+    if (cs > 1 && prm.cps > 0) prm.cps = 0;  // multicast clusters use TMA gathers only
     prm.trace = reinterpret_cast<unsigned long long*>(option("trace"));
     {
         const int esz = c.dtype == SHFLBW_F32 ? 4 : 2;
@@ -492,8 +548,6 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
                              ((static_cast<int64_t>(b.N) * esz) % 16 == 0);
         prm.bulk_out = aligned && !option("no_bulk_out") ? 1 : 0;
     }
-    if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
-    if (cs > 1 && prm.cps > 0) prm.cps = 0;  // multicast clusters use TMA gathers only
     int stages = static_cast<int>(option("stages"));
     if (stages <= 0) stages = vs >= 128 ? 3 : 4;
     const int max_kb = (a->cols + kBlockK - 1) / kBlockK;
@@ -501,16 +555,21 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.stages = stages;
 
     CUtensorMap tmB, tmW;
-    int st = make_map_2d(&tmB, a->dtype, b.ptr, static_cast<uint64_t>(b.N), static_cast<uint64_t>(b.K),
+    int st;
+    if (b.kind == 0)
+        st = make_map_2d(&tmB, a->dtype, b.ptr, static_cast<uint64_t>(b.N), static_cast<uint64_t>(b.K),
                          static_cast<uint64_t>(b.ldb) * 2, 64, 1, 128);
+    else
+        st = make_map_2d(&tmB, a->dtype, b.ptr, static_cast<uint64_t>(b.Nb),
+                         static_cast<uint64_t>(b.C) * b.H * b.W, static_cast<uint64_t>(b.Nb) * 2, bw, 1, bw * 2);
     if (st) return st;
     const int wbox = vs < 64 ? vs : 64;
     const int64_t wrows = a->total_cols > 0 ? a->total_cols : 1;
     st = make_map_2d(&tmW, a->dtype, a->values, static_cast<uint64_t>(V), static_cast<uint64_t>(wrows),
                      static_cast<uint64_t>(V) * 2, wbox, kBlockK, wbox * 2);
     if (st) return st;
-    return a->dtype == SHFLBW_BF16 ? dispatch_vs<SHFLBW_BF16>(vs, cs, tmB, tmW, prm, n_tiles, groups, s)
-                                   : dispatch_vs<SHFLBW_F16>(vs, cs, tmB, tmW, prm, n_tiles, groups, s);
+    return a->dtype == SHFLBW_BF16 ? dispatch_vs<SHFLBW_BF16>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s)
+                                   : dispatch_vs<SHFLBW_F16>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s);
 }
 
 }  // namespace sbw

@@ -368,17 +368,39 @@ def test_conv_cases_bit_exact(sb, oracle):
         assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("C,H,Kf,R,pad,V,Nb", [(64, 56, 64, 3, 1, 64, 8), (32, 14, 128, 3, 1, 32, 4),
-                                               (64, 12, 256, 1, 0, 64, 16)])
-def test_conv_resnet_like(sb, oracle, C, H, Kf, R, pad, V, Nb):
+@pytest.mark.parametrize("C,H,Kf,R,pad,V,Nb,stride",
+                         [(64, 56, 64, 3, 1, 64, 8, 1), (32, 14, 128, 3, 1, 32, 4, 1), (64, 12, 256, 1, 0, 64, 16, 1),
+                          (64, 14, 64, 3, 1, 64, 32, 1), (32, 9, 128, 3, 0, 128, 16, 1), (16, 8, 64, 3, 1, 32, 64, 1),
+                          (16, 6, 64, 3, 1, 64, 128, 1), (32, 15, 64, 3, 1, 64, 32, 2), (24, 7, 32, 1, 0, 32, 32, 2)])
+def test_conv_matches_oracle(sb, oracle, C, H, Kf, R, pad, V, Nb, stride):
+    """Implicit-GEMM sparse conv: tcgen05 path when N_b in {16, 32} or a
+    multiple of 64, exact CUDA-core path otherwise; padding = TMA zero fill."""
     crs = C * R * R
     mask = oracle.random_shflbw_mask(Kf, crs, V, crs // 4, oracle.rng(1234))
     W = oracle.round16(oracle.random_dense(Kf, crs, 1))
     x = oracle.round16(oracle.fill_uniform(oracle.rng(7), C * H * H * Nb).reshape(C, H, H, Nb))
     a, p = compress_both(sb, oracle, W, mask, V)
-    got = sb.conv2d(a, dev(x, torch.bfloat16), sb.ConvGeometry(R, R, 1, pad)).cpu().numpy()
-    want = oracle.conv2d(p, x, R, R, 1, pad)
+    n0 = sb.launch_count()
+    got = sb.conv2d(a, dev(x, torch.bfloat16), sb.ConvGeometry(R, R, stride, pad)).cpu().numpy()
+    assert sb.launch_count() == n0 + 1
+    want = oracle.conv2d(p, x, R, R, stride, pad)
     assert oracle.rel_frobenius(got, want) <= TOL
+
+
+def test_conv_tc_equals_simt(sb, oracle):
+    C, H, Kf, V, Nb = 32, 10, 128, 64, 32
+    crs = C * 9
+    mask = oracle.random_shflbw_mask(Kf, crs, V, crs // 4, oracle.rng(3))
+    W = oracle.round16(oracle.random_dense(Kf, crs, 1))
+    x = oracle.round16(oracle.fill_uniform(oracle.rng(5), C * H * H * Nb).reshape(C, H, H, Nb))
+    a, p = compress_both(sb, oracle, W, mask, V)
+    xd = dev(x, torch.bfloat16)
+    tc = sb.conv2d(a, xd, sb.ConvGeometry(3, 3, 1, 1)).cpu().numpy()
+    sb.set_option("force_simt", 1)
+    simt = sb.conv2d(a, xd, sb.ConvGeometry(3, 3, 1, 1)).cpu().numpy()
+    sb.set_option("force_simt", 0)
+    assert np.array_equal(simt, oracle.conv2d(p, x, 3, 3, 1, 1))
+    assert oracle.rel_frobenius(tc, simt) <= TOL
 
 
 def test_conv_1x1_equals_spmm_bitwise(sb, oracle):
