@@ -154,7 +154,8 @@ int shflbw_cu_spmm_groups(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_
                           int32_t c_dtype, int64_t ldc, int32_t compact,
                           shflbw_stream_t stream);
 
-/* C[row_indices[r]][:] = C_perm[r][:] for r < M (2- or 4-byte elements). */
+/* C[row_indices[r]][:] = C_perm[r][:] for r < M (2- or 4-byte elements);
+ * rows with row_indices[r] < 0 (padding of an all-gathered buffer) are skipped. */
 int shflbw_cu_unpermute_rows(const int32_t* row_indices, int32_t M, int32_t N,
                              const void* C_perm, int64_t ld_perm, void* C, int64_t ldc,
                              int32_t dtype, shflbw_stream_t stream);

@@ -142,6 +142,7 @@ __global__ void k_unpermute(const int32_t* __restrict__ ri, int N, const U* __re
                             int64_t lds, U* __restrict__ dst, int64_t ldd) {
     const int r = blockIdx.x;
     const int64_t out_row = ri[r];
+    if (out_row < 0) return;  // padding row of a sharded all-gather
     for (int n = threadIdx.x; n < N; n += blockDim.x) dst[out_row * ldd + n] = src[r * lds + n];
 }
 }  // namespace

@@ -1,0 +1,94 @@
+"""Multi-GPU row-group sharding of one Shfl-BW layer.
+
+Row groups are independent and write disjoint output rows
+(/root/reference/proj/src/spmm.cpp:133-134), so a layer shards by groups
+with no collective in the data path.  Rank p of P owns groups
+[p*G//P, (p+1)*G//P) -- the reference's worker split
+(src/spmm.cpp:137-142) -- and computes them with
+``shflbw_cu_spmm_groups(compact=1)`` into contiguous rows.  Only when the
+consumer needs the full output does an all-gather run (NCCL over NVLink on
+the GPU box; ranks' chunks are padded to equal size), followed by
+``shflbw_cu_unpermute_rows`` through a precomputed gathered-row -> output-row
+map (-1 for padding rows).
+
+``ShardPlan`` is pure host logic (tested with gloo on CPU);
+``ShardedSpMM`` binds it to the CUDA kernels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    groups: int
+    v: int
+    world: int
+
+    def range(self, rank: int) -> tuple[int, int]:
+        """The reference's static split: [G*w/W, G*(w+1)/W)."""
+        return self.groups * rank // self.world, self.groups * (rank + 1) // self.world
+
+    @property
+    def chunk_groups(self) -> int:
+        """Groups per rank after padding to equal all-gather counts."""
+        return max(self.range(r)[1] - self.range(r)[0] for r in range(self.world))
+
+    @property
+    def chunk_rows(self) -> int:
+        return self.chunk_groups * self.v
+
+    def gathered_row_map(self, row_indices: torch.Tensor) -> torch.Tensor:
+        """Row r' of the all-gathered (padded, group-ordered) buffer -> output
+        row, or -1 for a padding row.  row_indices: the matrix's [M] map."""
+        out = torch.full((self.world * self.chunk_rows,), -1, dtype=torch.int32, device=row_indices.device)
+        for r in range(self.world):
+            g0, g1 = self.range(r)
+            n = (g1 - g0) * self.v
+            out[r * self.chunk_rows: r * self.chunk_rows + n] = row_indices[g0 * self.v: g1 * self.v].to(torch.int32)
+        return out
+
+
+def gather_rows(plan: ShardPlan, local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather each rank's compact rows (padded to plan.chunk_rows) into
+    the [world*chunk_rows, N] group-ordered buffer."""
+    import torch.distributed as dist
+    if local.shape[0] != plan.chunk_rows:
+        pad = torch.zeros((plan.chunk_rows - local.shape[0], local.shape[1]), dtype=local.dtype,
+                          device=local.device)
+        local = torch.cat([local, pad])
+    out = torch.empty((plan.world * plan.chunk_rows, local.shape[1]), dtype=local.dtype, device=local.device)
+    if local.is_cuda:
+        dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    else:
+        dist.all_gather(list(out.chunk(plan.world)), local.contiguous(), group=group)
+    return out
+
+
+class ShardedSpMM:
+    """One rank's share of C = decompress(A) @ B, optionally all-gathered."""
+
+    def __init__(self, a, rank: int, world: int, group=None):
+        from . import shflbw as sb
+        self.sb = sb
+        self.a = a
+        self.plan = ShardPlan(a.group_count(), a.v, world)
+        self.rank = rank
+        self.group = group
+        self.g0, self.g1 = self.plan.range(rank)
+        ri, _, _, _ = a.to_host()
+        self.row_map = self.plan.gathered_row_map(torch.from_numpy(ri.astype("int32")).cuda())
+
+    def local(self, b: torch.Tensor, out_dtype=torch.bfloat16, out: torch.Tensor | None = None) -> torch.Tensor:
+        """This rank's rows, group order (compact)."""
+        if out is None:
+            out = torch.empty((self.plan.chunk_rows, b.shape[1]), dtype=out_dtype, device=b.device)
+        return self.sb.spmm_groups(self.a, self.g0, self.g1, b, out, compact=True)
+
+    def full(self, b: torch.Tensor, out_dtype=torch.bfloat16) -> torch.Tensor:
+        """All ranks' rows gathered and un-permuted into the full [M, N] output."""
+        gathered = gather_rows(self.plan, self.local(b, out_dtype), self.group)
+        c = torch.empty((self.a.rows, b.shape[1]), dtype=out_dtype, device=b.device)
+        return self.sb.unpermute_rows(self.row_map.data_ptr(), gathered, c)
