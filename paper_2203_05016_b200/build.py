@@ -70,6 +70,8 @@ def _compile(src: str, force: bool) -> str:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    if os.environ.get("SBW_TRACE"):
+        NVCC_FLAGS.append("-DSBW_TRACE")
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))

@@ -72,15 +72,22 @@ struct TcParams {
     int bw;                     // MN block width of the activation tile (64 | 32 | 16 elements)
     // implicit-GEMM conv geometry (KIND 1)
     int Nb, H, W, RS, S, stride, pad, Q, PQ;
+    int ksplit;  // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
 };
 
+// Development timeline (scripts/trace.py): compiled in only with -DSBW_TRACE.
 __device__ __forceinline__ void trace_event(unsigned long long* tr, int e) {
+#ifdef SBW_TRACE
     if (tr) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         const int cta = blockIdx.y * gridDim.x + blockIdx.x;
-        tr[cta * 8 + e] = t;
+        tr[cta * 32 + e] = t;
     }
+#else
+    (void)tr;
+    (void)e;
+#endif
 }
 
 template <int VS>
@@ -103,6 +110,77 @@ __device__ __forceinline__ void grid_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+template <class OT> __device__ __forceinline__ OT to_out(float x);
+template <> __device__ __forceinline__ float to_out<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ __half to_out<__half>(float x) { return __float2half_rn(x); }
+
+// Epilogue for one output type: TMEM -> (staged tile -> 16-byte stores) or
+// direct stores, through the row map.  Kept as one straight-line routine per
+// type so the compiler never lowers the type switch per element.
+template <class OT, int VS>
+__device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row, int nkb, int m, int q, int lane,
+                                              int n0, const int32_t* rows_s, unsigned char* ctile) {
+    constexpr int esz = sizeof(OT);
+    const int n = n0 + m;
+    const bool live = n < p.N;
+#pragma unroll
+    for (int c = 0; c < (VS + 31) / 32; ++c) {
+        constexpr int kW = VS < 32 ? VS : 32;
+        uint32_t r[32];
+        if (nkb > 0) {
+            if (kW == 32) tmem_ld32(t_row + c * 32, r);
+            else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tmem_ld_wait();
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (p.bulk_out) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                reinterpret_cast<OT*>(ctile)[(c * 32 + i) * kBlockN + m] = to_out<OT>(__uint_as_float(r[i]));
+        } else if (live) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[c * 32 + i]) * p.ldc + n] =
+                    to_out<OT>(__uint_as_float(r[i]));
+        }
+    }
+    if (p.bulk_out) {
+        // coalesced 16-byte stores of the staged tile, one output row = 128*esz bytes
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        constexpr int kLanesPerRow = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
+        constexpr int kRowsPerInst = 32 / kLanesPerRow;
+        const int chunk = lane % kLanesPerRow;
+        const int nn = n0 + chunk * (16 / esz);
+        if (nn < p.N) {
+#pragma unroll 4
+            for (int v = q * kRowsPerInst + lane / kLanesPerRow; v < VS; v += 4 * kRowsPerInst) {
+                const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
+                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(rows_s[v]) * p.ldc + nn) * esz) = x;
+            }
+        }
+    }
+}
+
+template <class OT, int VS, int CS>
+__device__ __forceinline__ void ksplit_reduce_rows(const TcParams& p, const float* red, const float* recv, int rank,
+                                                   int m, int n0, const int32_t* rows_s) {
+    constexpr int kRowsPer = VS / CS;
+    const int n = n0 + m;
+    const int v0 = rank * kRowsPer;
+    if (n >= p.N) return;
+#pragma unroll 4
+    for (int i = 0; i < kRowsPer; ++i) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < CS; ++c)  // rank order: deterministic
+            acc += c == rank ? red[(v0 + i) * kBlockN + m] : recv[(c * kRowsPer + i) * kBlockN + m];
+        static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = to_out<OT>(acc);
+    }
+}
+
 // warp roles (192 threads):
 //   warp 0  : stage bookkeeping -- waits for a free slot, arms the full
 //             barrier with the stage's byte count, loads the weight tile
@@ -114,7 +192,7 @@ __device__ __forceinline__ void grid_launch_dependents() {
 constexpr int kGatherWarps = 4;
 constexpr int kThreadsTc = 64 + 32 * kGatherWarps;
 
-template <int DT, int VS, int CS, int KIND>
+template <int DT, int VS, int CS, int KIND, int KSPLIT>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_spmm_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
               TcParams p) {
@@ -128,12 +206,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int stages = p.stages;
-    int32_t* meta_s = reinterpret_cast<int32_t*>(smem + stages * kStageBytes);  // [kMetaBlocks][64]
+    // K split: partial rows pushed here by the other CTAs, [CS][VS/CS][128] fp32
+    float* recv = reinterpret_cast<float*>(smem + stages * kStageBytes);
+    constexpr bool kKSplit = CS > 1 && KSPLIT;
+    constexpr bool mcast = CS > 1 && !KSPLIT;
+    const int recv_bytes = kKSplit ? VS * kBlockN * 4 : 0;
+    int32_t* meta_s = reinterpret_cast<int32_t*>(smem + stages * kStageBytes + recv_bytes);  // [kMetaBlocks][64]
     int32_t* rows_s = meta_s + kMetaBlocks * kBlockK;                           // VS
     uint64_t* full = reinterpret_cast<uint64_t*>(rows_s + (VS < 2 ? 2 : VS));
     uint64_t* empty = full + stages;
     uint64_t* accum = empty + stages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+    uint64_t* recv_bar = accum + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
@@ -141,8 +225,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int n0 = n_tile * kBlockN;
     const int g = p.g_begin + blockIdx.y;
     const int gp = p.group_ptr[g];
-    const int nkb = (p.group_ptr[g + 1] - gp) / kBlockK;
-    const int vbase = static_cast<int>(rank) * VS;
+    const int nkb_all = (p.group_ptr[g + 1] - gp) / kBlockK;
+    // K split: this CTA's K blocks [kbase, kbase + nkb); V split: its V rows
+    const int kbase = kKSplit ? nkb_all * static_cast<int>(rank) / CS : 0;
+    const int nkb = kKSplit ? nkb_all * (static_cast<int>(rank) + 1) / CS - kbase : nkb_all;
+    const int vbase = kKSplit ? 0 : static_cast<int>(rank) * VS;
+    const uint16_t cmask = static_cast<uint16_t>((1u << CS) - 1u);
     const int cps = p.cps;
     const int et = threadIdx.x - 64;  // gather/epilogue thread 0..127 (warps 2..5)
     if (threadIdx.x == 0) trace_event(p.trace, 0);
@@ -150,7 +238,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     // gather warps stage a window of column indices (all 64 per K block)
     auto stage_meta = [&](int kb0) {
         const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
-        const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + kb0 * kBlockK);
+        const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + (kbase + kb0) * kBlockK);
         for (int i = et; i < nb * (kBlockK / 4); i += 128) reinterpret_cast<int4*>(meta_s)[i] = src[i];
     };
 
@@ -159,9 +247,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1 + (cps > 0 ? 32 * kGatherWarps : 0));
-            mbar_init(&empty[s], CS);
+            mbar_init(&empty[s], mcast ? CS : 1);
         }
         mbar_init(accum, 1);
+        mbar_init(recv_bar, 1);
+        if (kKSplit)  // the CS-1 peers' partial rows for this CTA
+            mbar_arrive_expect_tx(recv_bar, (CS - 1) * (VS / CS) * kBlockN * 4);
         fence_mbar_init();
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmW);
@@ -187,7 +278,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
                 for (int sl = 0; sl < WL::kSlabs; ++sl)
                     tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
-                                vbase + sl * 64, gp + kb * kBlockK);
+                                vbase + sl * 64, gp + (kbase + kb) * kBlockK);
             }
         }
         __syncwarp();
@@ -202,6 +293,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                 mbar_wait(&full[s], (kb / stages) & 1);
                 tc_fence_after();
                 if (kb == 0) trace_event(p.trace, 3);
+                if (kb < 8) trace_event(p.trace, 8 + kb);
                 const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
                 const uint32_t w_addr = a_addr + kABytes;
 #pragma unroll
@@ -212,8 +304,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                                                           WL::kSlabBytes, WL::kSBO, WL::kLayout);
                     umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
                 }
-                if (CS == 1) umma_commit(&empty[s]);
-                else umma_commit_mc(&empty[s], static_cast<uint16_t>((1u << CS) - 1u));
+                if constexpr (!mcast) umma_commit(&empty[s]);
+                else umma_commit_mc(&empty[s], cmask);
             }
             trace_event(p.trace, 4);
             if (nkb > 0) umma_commit(accum);
@@ -230,8 +322,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int blk_bytes = kBlockK * p.bw * 2;
         const int per_warp = 16 * nblk / kGatherWarps;              // gather4s per warp per K block
         const int gi = gw * per_warp + lane;                        // this lane's gather
-        const int g_rg = gi & 15, g_b = gi >> 4;
-        const bool t_issue = lane < per_warp && (CS == 1 || (gi % CS) == static_cast<int>(rank));
+        // a warp owns 4 row groups (16 rows) in every MN block, so both halves
+        // of an activation row are requested together
+        const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
+        const bool t_issue = lane < per_warp && (!mcast || (gi % CS) == static_cast<int>(rank));
         // conv: this gather's output positions (fixed for the CTA)
         int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
         bool g_pos_ok = true;
@@ -266,6 +360,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
             if (win == 0) asm volatile("bar.sync 2, 128;" ::: "memory");
             if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+            if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
             unsigned char* a_st = smem + s * kStageBytes;
             const int32_t* mk = meta_s + win * kBlockK;
             if (t_issue) {
@@ -277,11 +372,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                     ci.w = conv_row(ci.w);
                 }
                 void* dst = a_st + g_b * blk_bytes + g_rg * (4 * p.bw * 2);
-                if (CS == 1)
+                if constexpr (!mcast)
                     tma_gather4(dst, &tmB, &full[s], g_x, ci.x, ci.y, ci.z, ci.w);
                 else
-                    tma_gather4_mc(dst, &tmB, &full[s], static_cast<uint16_t>((1u << CS) - 1u), g_x, ci.x,
-                                   ci.y, ci.z, ci.w);
+                    tma_gather4_mc(dst, &tmB, &full[s], cmask, g_x, ci.x, ci.y, ci.z, ci.w);
             }
             if (cps > 0) {
                 const uint32_t a_u32 = smem_u32(a_st);
@@ -312,64 +406,92 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (et == 0) trace_event(p.trace, 5);
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int m = q * 32 + lane;
-        const int n = n0 + m;
-        const bool live = n < p.N;
         const uint32_t t_row = tmem_d + (static_cast<uint32_t>(q * 32) << 16);
-        const int esz = p.c_dtype == SHFLBW_F32 ? 4 : 2;
         // all MMAs are complete (accum), so the stage buffers are free: they
         // hold the [VS][128] output tile for the bulk row stores
         unsigned char* ctile = smem;
+        if constexpr (kKSplit) {
+            // K split: CTA r finalises rows [r*VS/CS, (r+1)*VS/CS).  This
+            // thread owns output column m: push the other ranks' rows of its
+            // partial straight from registers into their `recv` slot
+            // (st.async: remote stores that complete on the receiver's
+            // mbarrier), then sum the CS partials of its own rows in rank
+            // order (deterministic).
+            constexpr int kRP = VS / CS;
+            float vals[VS];
 #pragma unroll
-        for (int c = 0; c < (VS + 31) / 32; ++c) {
-            constexpr int kW = VS < 32 ? VS : 32;
-            uint32_t r[32];
-            if (nkb > 0) {
-                if (kW == 32) tmem_ld32(t_row + c * 32, r);
-                else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
-                tmem_ld_wait();
-            } else {
+            for (int c = 0; c < (VS + 31) / 32; ++c) {
+                constexpr int kW = VS < 32 ? VS : 32;
+                uint32_t r[32];
+                if (nkb > 0) {
+                    if (kW == 32) tmem_ld32(t_row + c * 32, r);
+                    else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+                    tmem_ld_wait();
+                } else {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) r[i] = 0u;
-            }
-            if (p.bulk_out) {
-#pragma unroll
-                for (int i = 0; i < kW; ++i) {
-                    const int v = c * 32 + i;
-                    const float x = __uint_as_float(r[i]);
-                    if (p.c_dtype == SHFLBW_F32)
-                        reinterpret_cast<float*>(ctile)[v * kBlockN + m] = x;
-                    else if (p.c_dtype == SHFLBW_BF16)
-                        reinterpret_cast<__nv_bfloat16*>(ctile)[v * kBlockN + m] = __float2bfloat16_rn(x);
-                    else
-                        reinterpret_cast<__half*>(ctile)[v * kBlockN + m] = __float2half_rn(x);
+                    for (int i = 0; i < 32; ++i) r[i] = 0u;
                 }
-            } else if (live) {
 #pragma unroll
-                for (int i = 0; i < kW; ++i) {
-                    const int64_t off = static_cast<int64_t>(rows_s[c * 32 + i]) * p.ldc + n;
-                    const float x = __uint_as_float(r[i]);
-                    if (p.c_dtype == SHFLBW_F32) static_cast<float*>(p.C)[off] = x;
-                    else if (p.c_dtype == SHFLBW_BF16)
-                        static_cast<__nv_bfloat16*>(p.C)[off] = __float2bfloat16_rn(x);
-                    else static_cast<__half*>(p.C)[off] = __float2half_rn(x);
+                for (int i = 0; i < kW; ++i) vals[c * 32 + i] = __uint_as_float(r[i]);
+            }
+            const uint32_t slot = smem_u32(recv) + static_cast<uint32_t>((rank * kBlockN + m) * kRP * 4);
+#pragma unroll
+            for (int c = 0; c < CS; ++c) {
+                if (c == static_cast<int>(rank)) continue;
+                const uint32_t dst = mapa_shared(slot, c), bar = mapa_shared(smem_u32(recv_bar), c);
+#pragma unroll
+                for (int j = 0; j < kRP; j += 4)
+                    asm volatile(
+                        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                            dst + j * 4),
+                        "f"(vals[c * kRP + j]), "f"(vals[c * kRP + j + 1]), "f"(vals[c * kRP + j + 2]),
+                        "f"(vals[c * kRP + j + 3]), "r"(bar)
+                        : "memory");
+            }
+            if (et == 0) trace_event(p.trace, 24);
+            mbar_wait(recv_bar, 0);
+            if (et == 0) trace_event(p.trace, 25);
+            float out[kRP];
+#pragma unroll
+            for (int i = 0; i < kRP; ++i) out[i] = 0.0f;
+#pragma unroll
+            for (int c = 0; c < CS; ++c) {  // rank order
+                if (c == static_cast<int>(rank)) {
+#pragma unroll
+                    for (int i = 0; i < kRP; ++i) out[i] += vals[c * kRP + i];
+                } else {
+                    const float4* src = reinterpret_cast<const float4*>(recv + (c * kBlockN + m) * kRP);
+#pragma unroll
+                    for (int j = 0; j < kRP / 4; ++j) {
+                        const float4 x = src[j];
+                        out[4 * j] += x.x;
+                        out[4 * j + 1] += x.y;
+                        out[4 * j + 2] += x.z;
+                        out[4 * j + 3] += x.w;
+                    }
                 }
             }
-        }
-        if (p.bulk_out) {
-            // coalesced 16-byte stores of the staged tile: one output row is
-            // 128*esz bytes = 8 or 16... lanes; rows go through row_indices
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int lanes_per_row = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
-            const int rows_per_inst = 32 / lanes_per_row;
-            const int chunk = lane % lanes_per_row;
-            const int nn = n0 + chunk * (16 / esz);
-            for (int v = q * rows_per_inst + lane / lanes_per_row; v < VS; v += 4 * rows_per_inst) {
-                if (nn < p.N) {
-                    const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
-                    *reinterpret_cast<int4*>(static_cast<char*>(p.C) +
-                                             (static_cast<int64_t>(rows_s[v]) * p.ldc + nn) * esz) = x;
+            const int n = n0 + m;
+            if (n < p.N) {
+                const int v0 = static_cast<int>(rank) * kRP;
+                if (p.c_dtype == SHFLBW_F32) {
+#pragma unroll
+                    for (int i = 0; i < kRP; ++i) static_cast<float*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = out[i];
+                } else if (p.c_dtype == SHFLBW_BF16) {
+#pragma unroll
+                    for (int i = 0; i < kRP; ++i)
+                        static_cast<__nv_bfloat16*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = __float2bfloat16_rn(out[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kRP; ++i)
+                        static_cast<__half*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = __float2half_rn(out[i]);
                 }
             }
+        } else {
+            if (p.c_dtype == SHFLBW_F32) epilogue_rows<float, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+            else if (p.c_dtype == SHFLBW_BF16)
+                epilogue_rows<__nv_bfloat16, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+            else epilogue_rows<__half, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
         }
     }
     if (et == 0) trace_event(p.trace, 6);
@@ -430,13 +552,14 @@ int num_sms() {
     return sms;
 }
 
-template <int DT, int VS, int CS, int KIND>
+template <int DT, int VS, int CS, int KIND, int KSPLIT>
 int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
               cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
-    const size_t smem = static_cast<size_t>(prm.stages) * kStage + 1024 + kMetaBlocks * kBlockK * 4 +
-                        (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 2) * 8 + 16;
-    auto kern = k_spmm_tc<DT, VS, CS, KIND>;
+    const size_t recv = (CS > 1 && KSPLIT) ? static_cast<size_t>(VS) * kBlockN * 4 : 0;
+    const size_t smem = static_cast<size_t>(prm.stages) * kStage + recv + 1024 + kMetaBlocks * kBlockK * 4 +
+                        (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 3) * 8 + 16;
+    auto kern = k_spmm_tc<DT, VS, CS, KIND, KSPLIT>;
     SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_tiles * CS, groups, 1);
@@ -460,11 +583,13 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
 template <int DT, int VS>
 int dispatch_cs(int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm,
                 int n_tiles, int groups, cudaStream_t s) {
-    if (kind == 1) return launch_tc<DT, VS, 1, 1>(tmB, tmW, prm, n_tiles, groups, s);
-    switch (cs) {
-        case 1: return launch_tc<DT, VS, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 2: return launch_tc<DT, VS, 2, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 4: return launch_tc<DT, VS, 4, 0>(tmB, tmW, prm, n_tiles, groups, s);
+    if (kind == 1) return launch_tc<DT, VS, 1, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
+    switch (cs * 2 + prm.ksplit) {
+        case 2: case 3: return launch_tc<DT, VS, 1, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 4: return launch_tc<DT, VS, 2, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 5: return launch_tc<DT, VS, 2, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 8: return launch_tc<DT, VS, 4, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 9: return launch_tc<DT, VS, 4, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }
@@ -503,17 +628,28 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     if (groups > 65535) return SHFLBW_UNSUPPORTED;
     const int n_tiles = (b.N + kBlockN - 1) / kBlockN;
 
-    // cluster split of V: smallest CS that gives ~one CTA per SM, VS >= 16
+    // Cluster split for grids that would leave SMs idle: CS CTAs share one
+    // (group, column tile).  K split (default): each gathers 1/CS of the K
+    // blocks -- 1/CS of the activation bytes per SM -- and the partials are
+    // reduced through DSMEM.  V split ("split_mode" = 2): each owns V/CS rows
+    // and the activation tile is multicast to all CS CTAs.
+    const int min_kb = 2;  // K blocks per CTA worth splitting for
+    const int kb_all = (a->cols + kBlockK - 1) / kBlockK;
     int cs = static_cast<int>(option("split"));
+    const bool vsplit = option("split_mode") != 1;  // V split (multicast) unless K split is requested
     if (cs <= 0) {
         cs = 1;
         const int64_t units = static_cast<int64_t>(n_tiles) * groups;
-        while (cs < 4 && V / (cs * 2) >= 16 && units * cs * 2 <= num_sms()) cs *= 2;
+        if (vsplit) {
+            while (cs < 4 && V / (cs * 2) >= 16 && units * cs * 2 <= num_sms()) cs *= 2;
+        } else {
+            while (cs < 4 && units * cs * 2 <= num_sms() && kb_all / (cs * 2) >= min_kb) cs *= 2;
+        }
     }
     if (b.kind == 1) cs = 1;
     if (cs != 1 && cs != 2 && cs != 4) return fail(SHFLBW_BAD_PARAMS, "split must be 1, 2 or 4");
-    if (V % cs != 0 || V / cs < 16) return SHFLBW_UNSUPPORTED;
-    const int vs = V / cs;
+    if (vsplit && (V % cs != 0 || V / cs < 16)) return SHFLBW_UNSUPPORTED;
+    const int vs = vsplit ? V / cs : V;
 
     TcParams prm{};
     prm.row_indices = a->row_indices;
@@ -538,9 +674,10 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.pad = b.pad;
     prm.Q = b.Q;
     prm.PQ = b.P * b.Q;
+    prm.ksplit = (cs > 1 && !vsplit) ? 1 : 0;
     prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
     if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
-    if (cs > 1 && prm.cps > 0) prm.cps = 0;  // multicast clusters use TMA gathers only
+    if (vsplit && cs > 1 && prm.cps > 0) prm.cps = 0;  // multicast clusters use TMA gathers only
     prm.trace = reinterpret_cast<unsigned long long*>(option("trace"));
     {
         const int esz = c.dtype == SHFLBW_F32 ? 4 : 2;
@@ -550,7 +687,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     }
     int stages = static_cast<int>(option("stages"));
     if (stages <= 0) stages = vs >= 128 ? 3 : 4;
-    const int max_kb = (a->cols + kBlockK - 1) / kBlockK;
+    const int max_kb = prm.ksplit ? (kb_all + cs - 1) / cs : kb_all;  // K blocks per CTA
     if (stages > max_kb) stages = max_kb < 2 ? 2 : max_kb;
     prm.stages = stages;
 

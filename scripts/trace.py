@@ -38,13 +38,16 @@ for it in range(3):
     sb.spmm_execute(a, B, out=C)
     torch.cuda.synchronize()
     sb.set_option("trace", 0)
-t = tr.cpu().numpy().reshape(-1, 8)
+t = tr.cpu().numpy().reshape(-1, 32)
 t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
 names = ["entry", "setup", "dep_wait", "first_full", "last_mma", "accum", "epi_done", "exit"]
+names += [f"full[{k}]" for k in range(8)] + [f"issue[{k}]" for k in range(8)] + ["partial_ok", "recv_ok"]
 print(f"{args.workload} {args.opts}: {len(t)} CTAs, span {rel[:, 7].max():.2f} us")
 for e, nm in enumerate(names):
+    if not nm:
+        continue
     col = rel[:, e]
     col = col[t[:, e] > 0]
     if len(col):

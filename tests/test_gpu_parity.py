@@ -28,9 +28,8 @@ def sb():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2203_05016_b200 as sb
-    sb.set_option("force_simt", 0)
-    sb.set_option("split", 0)
-    sb.set_option("stages", 0)
+    for k, v in (("force_simt", 0), ("split", 0), ("stages", 0), ("split_mode", 0), ("cp_async_slabs", 0)):
+        sb.set_option(k, v)
     return sb
 
 
@@ -235,20 +234,55 @@ def test_spmm_tc_matches_oracle(sb, oracle, M, N, K, V, alpha):
 
 
 def test_spmm_tc_equals_simt_within_tolerance_and_split_is_bitwise(sb, oracle):
+    """V-split clusters (multicast) are bit-identical to one CTA per tile;
+    K-split clusters (DSMEM reduction in rank order) are deterministic and
+    within tolerance."""
     mask, W, B = synthetic(oracle, 2048, 1024, 256, 64, 0.25)
     a, p = compress_both(sb, oracle, W, mask, 64)
     Bd = dev(B, torch.bfloat16)
-    outs = {}
-    for split in (1, 2, 4):
+    want = oracle.spmm(p, B)
+    sb.set_option("split", 1)
+    base = sb.spmm_execute(a, Bd).cpu().numpy()
+    sb.set_option("split_mode", 2)
+    for split in (2, 4):
         sb.set_option("split", split)
-        outs[split] = sb.spmm_execute(a, Bd).cpu().numpy()
+        assert np.array_equal(sb.spmm_execute(a, Bd).cpu().numpy(), base)
+    sb.set_option("split_mode", 1)
+    for split in (2, 4):
+        sb.set_option("split", split)
+        k1 = sb.spmm_execute(a, Bd).cpu().numpy()
+        k2 = sb.spmm_execute(a, Bd).cpu().numpy()
+        assert np.array_equal(k1, k2)
+        assert oracle.rel_frobenius(k1, want) <= TOL
     sb.set_option("split", 0)
+    sb.set_option("split_mode", 0)
     sb.set_option("force_simt", 1)
     simt = sb.spmm_execute(a, Bd).cpu().numpy()
     sb.set_option("force_simt", 0)
-    assert np.array_equal(simt, oracle.spmm(p, B))  # CUDA-core path is bit-exact
-    assert np.array_equal(outs[1], outs[2]) and np.array_equal(outs[1], outs[4])
-    assert oracle.rel_frobenius(outs[1], simt) <= TOL
+    assert np.array_equal(simt, want)  # CUDA-core path is bit-exact
+    assert oracle.rel_frobenius(base, simt) <= TOL
+
+
+@pytest.mark.parametrize("split", [2, 4])
+def test_spmm_ksplit_ragged(sb, oracle, split):
+    """K split with groups whose K-block count is not a multiple of the split
+    (and empty groups)."""
+    rs = np.random.RandomState(21)
+    M, K, V, N = 64 * 12, 900, 64, 256
+    supports = [np.sort(rs.choice(K, [0, 1, 65, 130, 300, 700][g % 6], replace=False)) for g in range(M // V)]
+    perm = rs.permutation(M)
+    mask = np.zeros((M, K), np.uint8)
+    for r in range(M):
+        mask[perm[r], supports[r // V]] = 1
+    W = oracle.round16(oracle.random_dense(M, K, 5))
+    B = oracle.round16(oracle.random_dense(K, N, 6))
+    a, p = compress_both(sb, oracle, W, mask, V)
+    sb.set_option("split", split)
+    sb.set_option("split_mode", 1)
+    got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
+    sb.set_option("split", 0)
+    sb.set_option("split_mode", 0)
+    assert oracle.rel_frobenius(got, oracle.spmm(p, B)) <= TOL
 
 
 @pytest.mark.parametrize("N", [128, 200, 1000])
