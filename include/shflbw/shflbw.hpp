@@ -12,12 +12,12 @@
 //     (csrc/convert.cu); spmm_execute / conv2d run the sm_100a kernels
 //     (csrc/spmm_sm100.cu, csrc/spmm_simt.cu).  `threads` is accepted and
 //     ignored; TileConfig is validated exactly as before.
-//   * Arithmetic: operands are rounded to the device value type
-//     (SHFLBW_DEVICE_DTYPE = bf16 (default) | f16) and products accumulate in
-//     fp32.  On inputs that are already representable in that type, the
-//     CUDA-core path (V not in {16,32,64,128}) is bit-identical to the
-//     reference and the tensor-core path is within 1e-5 relative Frobenius
-//     error; see DESIGN.md "Numerics".
+//   * Arithmetic: by default (SHFLBW_DEVICE_DTYPE unset or f32) the exact
+//     CUDA-core kernel -- products rounded then added in ascending k, so
+//     results are bit-identical to the reference.  SHFLBW_DEVICE_DTYPE=bf16
+//     or f16 rounds operands to 16 bits and runs the tcgen05 tensor-core
+//     kernel (fp32 accumulation, within the reference's 1e-5 relative
+//     Frobenius --check bar on 16-bit-exact inputs); see DESIGN.md.
 //   * spmm_dense_oracle / stitch_tile / tile_mma also run on the device, in
 //     the reference's pinned order (mul then add, ascending k).
 #pragma once

@@ -57,8 +57,9 @@ typedef struct shflbw_cu_matrix {
     int32_t cols;        /* K (C*R*S for conv weights)                    */
     int32_t v;           /* V, rows per group                             */
     int32_t groups;      /* G = M / V                                     */
-    int32_t dtype;       /* SHFLBW_BF16 / SHFLBW_F16; SHFLBW_F32 = storage
-                            only (exact host round trips), not computable */
+    int32_t dtype;       /* SHFLBW_BF16 / SHFLBW_F16: tensor cores;
+                            SHFLBW_F32: exact CUDA-core path (bit-identical
+                            to the reference's fp32 arithmetic)             */
     int32_t k_tile;      /* SHFLBW_K_TILE                                 */
     int64_t total_cols;  /* group_ptr[groups]                             */
     int32_t* row_indices; /* [dev] M: compressed row r -> original row    */
@@ -138,7 +139,10 @@ int shflbw_cu_decompress(const shflbw_cu_matrix* m, float* dense, shflbw_stream_
  *      src/spmm.cpp:76-146) ---------------------------------------------- */
 
 /* C[row_indices[g*V+r]][n] = sum_j values[g][j][r] * B[col_idx[g][j]][n].
- * B [dev] K_b x N, row stride ldb elements, dtype == a->dtype.
+ * B [dev] K_b x N, row stride ldb elements, dtype == a->dtype.  BF16/F16
+ * matrices run the tcgen05 kernel (V in {16,32,64,128}, ldb % 8 == 0) or the
+ * exact CUDA-core kernel; F32 matrices run the CUDA-core kernel, bit-identical
+ * to spmm_execute.
  * C [dev] M x N, row stride ldc, c_dtype F32 or BF16/F16.
  * ShapeMismatch if K_b != a->cols.  Asynchronous. */
 int shflbw_cu_spmm(const shflbw_cu_matrix* a, const void* B, int32_t K_b, int32_t N,

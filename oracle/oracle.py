@@ -63,11 +63,17 @@ class Packed:
         return self.values[off * self.V: (off + int(self.group_ncols[g])) * self.V]
 
 
-def build(force: bool = False) -> None:
-    """Compile liboracle.so (and _ref when /root/reference is present)."""
-    if force or not os.path.exists(ORACLE_SO) or (
+REF_TESTS = os.path.join(HERE, "_ref", "reference_unit_tests_b200")
+
+
+def build(force: bool = False, with_ref_tests: bool = False) -> None:
+    """Compile liboracle.so (and _ref when /root/reference is present; with
+    with_ref_tests also the reference's own unit tests linked against
+    libshflbw_b200.so)."""
+    targets = ["all"] + (["ref_tests"] if with_ref_tests else [])
+    if force or with_ref_tests or not os.path.exists(ORACLE_SO) or (
             os.path.isdir("/root/reference/proj") and not os.path.exists(REF_SO)):
-        subprocess.run(["make", "-s", "-C", HERE], check=True)
+        subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
 class _Rng:

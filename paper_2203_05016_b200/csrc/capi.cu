@@ -50,12 +50,7 @@ int check_matrix(const shflbw_cu_matrix* a) {
     return SHFLBW_OK;
 }
 
-int check_compute_matrix(const shflbw_cu_matrix* a) {
-    if (int st = check_matrix(a)) return st;
-    if (a->dtype == SHFLBW_F32)
-        return fail(SHFLBW_BAD_PARAMS, "SpMM / conv need BF16 or F16 matrix values (F32 is storage only)");
-    return SHFLBW_OK;
-}
+int check_compute_matrix(const shflbw_cu_matrix* a) { return check_matrix(a); }
 
 int check_out_dtype(int dt) {
     if (dt != SHFLBW_F32 && dt != SHFLBW_BF16 && dt != SHFLBW_F16)
@@ -66,7 +61,7 @@ int check_out_dtype(int dt) {
 int run_spmm(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b, const OutSpec& c,
              cudaStream_t s) {
     if (g_end <= g_begin || b.N == 0) return SHFLBW_OK;
-    if (!option("force_simt")) {
+    if (!option("force_simt") && a->dtype != SHFLBW_F32) {  // fp32: the exact CUDA-core path
         const int st = spmm_tc(a, g_begin, g_end, b, c, s);
         if (st != SHFLBW_UNSUPPORTED) return st;
     }

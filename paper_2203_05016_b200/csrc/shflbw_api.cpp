@@ -50,14 +50,20 @@ void check_cuda(cudaError_t e, const char* where) {
     if (e != cudaSuccess) throw Error(std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-// device value type used for SpMM / conv operands
+// device value type used for SpMM / conv operands.  Default f32: the exact
+// CUDA-core path, bit-identical to the reference (its unit tests pass
+// unchanged).  SHFLBW_DEVICE_DTYPE=bf16|f16 selects the tcgen05 tensor-core
+// path (operands rounded to 16 bits, fp32 accumulation).
 int compute_dtype() {
     static const int dt = [] {
         const char* e = std::getenv("SHFLBW_DEVICE_DTYPE");
-        return (e && (!std::strcmp(e, "f16") || !std::strcmp(e, "fp16"))) ? SHFLBW_F16 : SHFLBW_BF16;
+        if (e && (!std::strcmp(e, "f16") || !std::strcmp(e, "fp16"))) return static_cast<int>(SHFLBW_F16);
+        if (e && !std::strcmp(e, "bf16")) return static_cast<int>(SHFLBW_BF16);
+        return static_cast<int>(SHFLBW_F32);
     }();
     return dt;
 }
+int dtype_size(int dt) { return dt == SHFLBW_F32 ? 4 : 2; }
 
 struct DeviceBuffer {
     void* p = nullptr;
@@ -117,18 +123,18 @@ DeviceOperand upload_operand(const float* src, size_t rows, size_t cols, int dty
     op.ld = static_cast<int64_t>((cols + 7) / 8 * 8);
     DeviceBuffer staging(rows * cols * sizeof(float));
     upload_host(src, staging, rows * cols * sizeof(float));
-    op.buf = std::make_unique<DeviceBuffer>(rows * op.ld * 2);
+    op.buf = std::make_unique<DeviceBuffer>(rows * op.ld * dtype_size(dtype));
     if (rows && cols) {
         if (static_cast<size_t>(op.ld) == cols) {
             check(shflbw_cu_convert(staging.p, SHFLBW_F32, op.buf->p, dtype, static_cast<int64_t>(rows * cols),
                                     sstream()),
                   "convert");
         } else {
-            check_cuda(cudaMemsetAsync(op.buf->p, 0, rows * op.ld * 2, stream()), "memset");
+            check_cuda(cudaMemsetAsync(op.buf->p, 0, rows * op.ld * dtype_size(dtype), stream()), "memset");
             for (size_t r = 0; r < rows; ++r)
                 check(shflbw_cu_convert(staging.as<float>() + r * cols, SHFLBW_F32,
-                                        op.buf->as<char>() + r * op.ld * 2, dtype, static_cast<int64_t>(cols),
-                                        sstream()),
+                                        op.buf->as<char>() + r * op.ld * dtype_size(dtype), dtype,
+                                        static_cast<int64_t>(cols), sstream()),
                       "convert");
         }
     }
@@ -477,7 +483,7 @@ Tensor4 conv2d(const ShflBWMatrix& weights, const Tensor4& input, const ConvGeom
     DeviceMatrix dm;
     upload_matrix(weights, dt, dm);
     Tensor4 out(weights.core.rows, P, Q, input.n);
-    DeviceBuffer staging(input.values.size() * 4), din(input.values.size() * 2 + 16),
+    DeviceBuffer staging(input.values.size() * 4), din(input.values.size() * dtype_size(dt) + 16),
         dout(out.values.size() * 4);
     upload_host(input.values.data(), staging, input.values.size() * 4);
     check(shflbw_cu_convert(staging.p, SHFLBW_F32, din.p, dt, static_cast<int64_t>(input.values.size()), sstream()),

@@ -6,7 +6,10 @@
 // order exactly: every output element is a chain of fmaf in ascending k from
 // 0.0f, which for 16-bit operands equals the reference's separately rounded
 // multiply-add (src/spmm.cpp:60-74) because each product is exact in fp32.
-// So on bf16/fp16 inputs this path is BIT-IDENTICAL to spmm_execute/conv2d.
+// Products are rounded and then added (__fmul_rn / __fadd_rn, never a fused
+// FMA -- the reference builds with -ffp-contract=off), so this path is
+// BIT-IDENTICAL to spmm_execute / conv2d for fp32 operands (SHFLBW_F32
+// matrices, the C++ drop-in's default) as well as for bf16/fp16 ones.
 //
 // Block = one group x 128 output columns; thread = one output column.  The
 // group's weights and column indices are staged through shared memory in
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm_simt(
                                 : 0.0f;
                     }
 #pragma unroll
-                    for (int u = 0; u < kVC; ++u) acc[u] = __fmaf_rn(w_s[jj][u], x, acc[u]);
+                    for (int u = 0; u < kVC; ++u) acc[u] = __fadd_rn(acc[u], __fmul_rn(w_s[jj][u], x));
                 }
             }
         }
@@ -132,6 +135,7 @@ int spmm_simt(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& 
         }
         return SHFLBW_OK;
     }
+    if (a->dtype == SHFLBW_F32) return launch<SHFLBW_F32>(a, g_begin, g_end, b, c, s);
     return a->dtype == SHFLBW_BF16 ? launch<SHFLBW_BF16>(a, g_begin, g_end, b, c, s)
                                    : launch<SHFLBW_F16>(a, g_begin, g_end, b, c, s);
 }
