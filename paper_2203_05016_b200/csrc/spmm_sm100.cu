@@ -40,6 +40,7 @@
 // tools/shflbw.cpp:33).
 #include <cuda.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -522,8 +523,50 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
+// Encoding a tensor map costs ~1-2 us of host time; repeated calls on the same
+// buffers (weights every call, activations in steady state) hit this small
+// per-thread direct-mapped cache instead.
+struct MapKey {
+    const void* ptr;
+    uint64_t inner, outer, stride;
+    uint32_t box_inner, box_outer;
+    int dt, swz;
+    bool operator==(const MapKey& o) const {
+        return ptr == o.ptr && inner == o.inner && outer == o.outer && stride == o.stride &&
+               box_inner == o.box_inner && box_outer == o.box_outer && dt == o.dt && swz == o.swz;
+    }
+};
+struct MapEntry {
+    MapKey key{};
+    CUtensorMap map;
+    bool valid = false;
+};
+
+int encode_map_2d(CUtensorMap* map, int dt, const void* ptr, uint64_t inner, uint64_t outer,
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
+
 int make_map_2d(CUtensorMap* map, int dt, const void* ptr, uint64_t inner, uint64_t outer,
                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+    thread_local MapEntry cache[16];
+    const MapKey key{ptr, inner, outer, row_stride_bytes, box_inner, box_outer, dt, swizzle_bytes};
+    const size_t h = (reinterpret_cast<uintptr_t>(ptr) >> 8 ^ inner * 31 ^ outer * 17 ^ box_inner * 7 ^
+                      static_cast<size_t>(swizzle_bytes)) & 15;
+    MapEntry& e = cache[h];
+    if (e.valid && e.key == key) {
+        *map = e.map;
+        return SHFLBW_OK;
+    }
+    const int st = encode_map_2d(map, dt, ptr, inner, outer, row_stride_bytes, box_inner, box_outer, swizzle_bytes);
+    if (st == SHFLBW_OK) {
+        e.key = key;
+        e.map = *map;
+        e.valid = true;
+    }
+    return st;
+}
+
+int encode_map_2d(CUtensorMap* map, int dt, const void* ptr, uint64_t inner, uint64_t outer,
+                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return fail(SHFLBW_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t dims[2] = {inner, outer};
@@ -560,7 +603,11 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     const size_t smem = static_cast<size_t>(prm.stages) * kStage + recv + 1024 + kMetaBlocks * kBlockK * 4 +
                         (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 3) * 8 + 16;
     auto kern = k_spmm_tc<DT, VS, CS, KIND, KSPLIT>;
-    SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    static std::atomic<size_t> configured{0};  // per instantiation: raise the smem cap once
+    if (smem > configured.load(std::memory_order_relaxed)) {
+        SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured.store(smem, std::memory_order_relaxed);
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_tiles * CS, groups, 1);
     cfg.blockDim = dim3(kThreadsTc, 1, 1);
@@ -677,7 +724,6 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.ksplit = (cs > 1 && !vsplit) ? 1 : 0;
     prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
     if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
-    if (vsplit && cs > 1 && prm.cps > 0) prm.cps = 0;  // multicast clusters use TMA gathers only
     prm.trace = reinterpret_cast<unsigned long long*>(option("trace"));
     {
         const int esz = c.dtype == SHFLBW_F32 ? 4 : 2;

@@ -111,6 +111,7 @@ class ShflBWMatrix:
 
     def __init__(self, cm: L.CuMatrix):
         self._m = cm
+        self._ref = C.byref(cm)
 
     def __del__(self):
         try:
@@ -146,7 +147,8 @@ class ShflBWMatrix:
 
     @property
     def ptr(self):
-        return C.byref(self._m)
+        return self._ref
+
 
     def to_host(self):
         """-> (row_indices u32[M], group_ncols u32[G], cols u32[sum n_g],
@@ -251,13 +253,16 @@ def _check_b(a: ShflBWMatrix, b: torch.Tensor) -> torch.Tensor:
 def spmm_execute(a: ShflBWMatrix, b: torch.Tensor, cfg: TileConfig | None = None, threads: int = 1,
                  out_dtype: torch.dtype = torch.float32, out: torch.Tensor | None = None) -> torch.Tensor:
     """C = decompress(a) @ b with the permuted write-back (src/spmm.cpp:76-146)."""
-    (cfg or TileConfig()).validate()
+    if cfg is not None:  # the default TileConfig is valid by construction
+        cfg.validate()
     b = _check_b(a, b)
     N = b.shape[1]
     if out is None:
         out = torch.zeros((a.rows, N), dtype=out_dtype, device=b.device)
-    _check(_lib().shflbw_cu_spmm(a.ptr, b.data_ptr(), b.shape[0], N, b.stride(0), out.data_ptr(),
-                                 _dt(out.dtype), out.stride(0), _stream()))
+    st = _lib().shflbw_cu_spmm(a.ptr, b.data_ptr(), b.shape[0], N, b.stride(0), out.data_ptr(),
+                               _DT[out.dtype], out.stride(0), torch.cuda.current_stream().cuda_stream)
+    if st:
+        _check(st)
     return out
 
 
