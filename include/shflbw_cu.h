@@ -69,6 +69,9 @@ typedef struct shflbw_cu_matrix {
     void* values;         /* [dev] total_cols * v 16-bit values            */
     int32_t device;       /* CUDA device ordinal                           */
     int32_t owns;         /* 1: free with shflbw_cu_matrix_free            */
+    int32_t max_group_cols; /* max_g (group_ptr[g+1]-group_ptr[g]); 0 = unknown
+                               (kernels then size pipelines from `cols`)    */
+    int32_t reserved;
 } shflbw_cu_matrix;
 
 /* ---- library ---------------------------------------------------------- */

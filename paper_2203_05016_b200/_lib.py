@@ -25,6 +25,7 @@ class CuMatrix(C.Structure):
         ("dtype", C.c_int32), ("k_tile", C.c_int32), ("total_cols", C.c_int64),
         ("row_indices", C.c_void_p), ("group_ptr", C.c_void_p), ("group_ncols", C.c_void_p),
         ("col_idx", C.c_void_p), ("values", C.c_void_p), ("device", C.c_int32), ("owns", C.c_int32),
+        ("max_group_cols", C.c_int32), ("reserved", C.c_int32),
     ]
 
 

@@ -209,6 +209,20 @@ __global__ void k_total(const int* __restrict__ in, const int* __restrict__ ex, 
     *total = n ? ex[n - 1] + in[n - 1] : 0;
 }
 
+// out[0] = max(in[0..n)), single block
+__global__ void k_max(const int* __restrict__ in, int n, int* __restrict__ out) {
+    __shared__ int s[256];
+    int m = 0;
+    for (int i = threadIdx.x; i < n; i += 256) m = max(m, in[i]);
+    s[threadIdx.x] = m;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (threadIdx.x < o) s[threadIdx.x] = max(s[threadIdx.x], s[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = s[0];
+}
+
 // ---- runs / groups ---------------------------------------------------------
 
 __device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_t x) {
@@ -718,9 +732,14 @@ int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M
                                               leader.as<int32_t>(), out->group_ncols, padded.as<int>());
     SBW_LAUNCHED("k_assign");
     if ((st = scan_exclusive(padded.as<int>(), out->group_ptr, G, out->group_ptr + G, s))) return cleanup(st);
-    int total_cols = 0;
-    SBW_CUDA(cudaMemcpyAsync(&total_cols, out->group_ptr + G, sizeof(int), cudaMemcpyDeviceToHost, s));
+    k_max<<<1, 256, 0, s>>>(padded.as<int>(), G, total.as<int>());
+    SBW_LAUNCHED("k_max");
+    int sizes[2] = {0, 0};
+    SBW_CUDA(cudaMemcpyAsync(&sizes[0], out->group_ptr + G, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaMemcpyAsync(&sizes[1], total.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     SBW_CUDA(cudaStreamSynchronize(s));
+    const int total_cols = sizes[0];
+    out->max_group_cols = sizes[1];
     if ((st = alloc_data(out, total_cols))) return cleanup(st);
     if (G > 0) {
         k_pack_cols<<<G, 128, 0, s>>>(p.words.as<uint64_t>(), p.W, leader.as<int32_t>(), out->group_ptr,
@@ -788,13 +807,21 @@ int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t
     }
     if ((st = scan_exclusive(out->group_ncols, d_off.as<int>(), G, nullptr, s))) return cleanup(st);
     if ((st = scan_exclusive(d_pad.as<int>(), out->group_ptr, G, out->group_ptr + G, s))) return cleanup(st);
-    int total_cols = 0;
+    if (G > 0) {
+        k_max<<<1, 256, 0, s>>>(d_pad.as<int>(), G, d_pad.as<int>() + G);
+        SBW_LAUNCHED("k_max");
+    } else {
+        SBW_CUDA(cudaMemsetAsync(d_pad.as<int>(), 0, sizeof(int), s));
+    }
+    int total_cols = 0, max_cols = 0;
     uint32_t hf[4];
+    SBW_CUDA(cudaMemcpyAsync(&max_cols, d_pad.as<int>() + G, sizeof(int), cudaMemcpyDeviceToHost, s));
     SBW_CUDA(cudaMemcpyAsync(&total_cols, out->group_ptr + G, sizeof(int), cudaMemcpyDeviceToHost, s));
     SBW_CUDA(cudaMemcpyAsync(hf, flags.p, 16, cudaMemcpyDeviceToHost, s));
     SBW_CUDA(cudaStreamSynchronize(s));
     if (hf[0]) return cleanup(fail(SHFLBW_SHAPE_MISMATCH, "spmm: row index out of range"));
     if (hf[3]) return cleanup(fail(SHFLBW_BAD_PARAMS, "group column count exceeds K"));
+    out->max_group_cols = max_cols;
     if ((st = alloc_data(out, total_cols))) return cleanup(st);
     if (G > 0 && total_cols > 0) {
         dim3 grid(grid_for(static_cast<int64_t>(K + SHFLBW_K_TILE) * V, 256 * 4), G);

@@ -733,7 +733,8 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     }
     int stages = static_cast<int>(option("stages"));
     if (stages <= 0) stages = vs >= 128 ? 3 : 4;
-    const int max_kb = prm.ksplit ? (kb_all + cs - 1) / cs : kb_all;  // K blocks per CTA
+    const int kb_grp = a->max_group_cols > 0 ? a->max_group_cols / kBlockK : kb_all;  // widest group
+    const int max_kb = prm.ksplit ? (kb_grp + cs - 1) / cs : kb_grp;                   // K blocks per CTA
     if (stages > max_kb) stages = max_kb < 2 ? 2 : max_kb;
     prm.stages = stages;
 
