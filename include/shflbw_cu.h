@@ -84,7 +84,16 @@ int shflbw_cu_version(void);
  * sparse matrix, overlaps the previous kernel on the stream; the activation
  * B and the output C are touched only after the previous grid completes, so
  * a matrix must not be written by work still in flight when an SpMM using it
- * is enqueued -- shflbw_cu_compress / _upload return with it complete).
+ * is enqueued -- shflbw_cu_compress / _upload return with it complete),
+ * "split_mode" (cluster split kind: 0 = auto, 1 = K split with a DSMEM
+ * reduction of fp32 partials, 2 = 2 x 2: V split over a CTA pair and K split
+ * over two pairs, 3 = V split with multicast activation tiles; with mode 0 an
+ * explicit "split" means V split), "persistent" (1: the
+ * persistent-CTA kernel that loops over (group, column tile) units; default
+ * 0 = one CTA per unit), "cp_async_slabs" (0..2 activation slabs filled by
+ * cp.async instead of TMA gather4), "no_bulk_out" (1: per-element output
+ * stores).  All variants give results within the same tolerance; V split,
+ * cp.async and persistent are bit-identical to the default.
  * Unknown key: BAD_PARAMS. */
 int shflbw_cu_set_option(const char* key, int64_t value);
 /* Number of kernels this library launched on the calling thread so far. */

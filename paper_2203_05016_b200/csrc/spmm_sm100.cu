@@ -40,6 +40,7 @@
 // tools/shflbw.cpp:33).
 #include <cuda.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 
@@ -73,7 +74,8 @@ struct TcParams {
     int bw;                     // MN block width of the activation tile (64 | 32 | 16 elements)
     // implicit-GEMM conv geometry (KIND 1)
     int Nb, H, W, RS, S, stride, pad, Q, PQ;
-    int ksplit;  // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
+    int ksplit;      // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
+    int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
 };
 
 // Development timeline (scripts/trace.py): compiled in only with -DSBW_TRACE.
@@ -116,13 +118,31 @@ template <> __device__ __forceinline__ float to_out<float>(float x) { return x; 
 template <> __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
 template <> __device__ __forceinline__ __half to_out<__half>(float x) { return __float2half_rn(x); }
 
+// Coalesced 16-byte stores of a staged [ROWS][128] tile of OT through the row
+// map: one output row = 128*sizeof(OT) bytes, 16 or 32 lanes per row.
+template <class OT, int ROWS>
+__device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigned char* ctile, const int32_t* rows,
+                                                int q, int lane, int n0) {
+    constexpr int esz = sizeof(OT);
+    constexpr int kLanesPerRow = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
+    constexpr int kRowsPerInst = 32 / kLanesPerRow;
+    const int chunk = lane % kLanesPerRow;
+    const int nn = n0 + chunk * (16 / esz);
+    if (nn < p.N) {
+#pragma unroll 4
+        for (int v = q * kRowsPerInst + lane / kLanesPerRow; v < ROWS; v += 4 * kRowsPerInst) {
+            const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
+            *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(rows[v]) * p.ldc + nn) * esz) = x;
+        }
+    }
+}
+
 // Epilogue for one output type: TMEM -> (staged tile -> 16-byte stores) or
 // direct stores, through the row map.  Kept as one straight-line routine per
 // type so the compiler never lowers the type switch per element.
 template <class OT, int VS>
 __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row, int nkb, int m, int q, int lane,
                                               int n0, const int32_t* rows_s, unsigned char* ctile) {
-    constexpr int esz = sizeof(OT);
     const int n = n0 + m;
     const bool live = n < p.N;
 #pragma unroll
@@ -149,36 +169,71 @@ __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row,
         }
     }
     if (p.bulk_out) {
-        // coalesced 16-byte stores of the staged tile, one output row = 128*esz bytes
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        constexpr int kLanesPerRow = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
-        constexpr int kRowsPerInst = 32 / kLanesPerRow;
-        const int chunk = lane % kLanesPerRow;
-        const int nn = n0 + chunk * (16 / esz);
-        if (nn < p.N) {
-#pragma unroll 4
-            for (int v = q * kRowsPerInst + lane / kLanesPerRow; v < VS; v += 4 * kRowsPerInst) {
-                const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
-                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(rows_s[v]) * p.ldc + nn) * esz) = x;
-            }
-        }
+        store_tile_rows<OT, VS>(p, ctile, rows_s, q, lane, n0);
     }
 }
 
-template <class OT, int VS, int CS>
-__device__ __forceinline__ void ksplit_reduce_rows(const TcParams& p, const float* red, const float* recv, int rank,
-                                                   int m, int n0, const int32_t* rows_s) {
-    constexpr int kRowsPer = VS / CS;
-    const int n = n0 + m;
-    const int v0 = rank * kRowsPer;
-    if (n >= p.N) return;
-#pragma unroll 4
-    for (int i = 0; i < kRowsPer; ++i) {
+// K-split epilogue (KSF K ranks x VSF V ranks per cluster): K rank kr
+// finalises rows [kr*kRP, (kr+1)*kRP) of the VS slice.  Thread m (output
+// column n0+m) pushes the other K ranks' rows of its fp32 partial straight
+// from registers into their `recv` buffer with st.async (remote stores that
+// complete on the receiver's mbarrier), then sums the KSF partials of its own
+// rows in K-rank order (deterministic) and stores them through the staged
+// 16-byte path.  recv is [KSF][kRP][128] fp32: a warp's 32 threads touch 128
+// contiguous bytes per row, both for the remote stores and the local reads.
+template <class OT, int VS, int KSF, int VSF>
+__device__ __forceinline__ void ksplit_epilogue(const TcParams& p, uint32_t t_row, int nkb, int m, int q, int lane,
+                                                int n0, int kr, int vr, const int32_t* rows_s, float* recv,
+                                                uint64_t* recv_bar, unsigned char* ctile) {
+    constexpr int kRP = VS / KSF;
+    float vals[VS];
+#pragma unroll
+    for (int c = 0; c < (VS + 31) / 32; ++c) {
+        constexpr int kW = VS < 32 ? VS : 32;
+        uint32_t r[32];
+        if (nkb > 0) {
+            if (kW == 32) tmem_ld32(t_row + c * 32, r);
+            else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tmem_ld_wait();
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kW; ++i) vals[c * 32 + i] = __uint_as_float(r[i]);
+    }
+    const uint32_t slot = smem_u32(recv) + static_cast<uint32_t>((kr * kRP * kBlockN + m) * 4);
+#pragma unroll
+    for (int c = 0; c < KSF; ++c) {
+        if (c == kr) continue;
+        const uint32_t peer = static_cast<uint32_t>(c * VSF + vr);
+        const uint32_t dst = mapa_shared(slot, peer), bar = mapa_shared(smem_u32(recv_bar), peer);
+#pragma unroll
+        for (int i = 0; i < kRP; ++i)
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                             dst + i * kBlockN * 4),
+                         "r"(__float_as_uint(vals[c * kRP + i])), "r"(bar)
+                         : "memory");
+    }
+    if (m == 0) trace_event(p.trace, 24);
+    mbar_wait(recv_bar, 0);
+    if (m == 0) trace_event(p.trace, 25);
+#pragma unroll
+    for (int i = 0; i < kRP; ++i) {
         float acc = 0.0f;
 #pragma unroll
-        for (int c = 0; c < CS; ++c)  // rank order: deterministic
-            acc += c == rank ? red[(v0 + i) * kBlockN + m] : recv[(c * kRowsPer + i) * kBlockN + m];
-        static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = to_out<OT>(acc);
+        for (int c = 0; c < KSF; ++c)  // K-rank order
+            acc += c == kr ? vals[c * kRP + i] : recv[(c * kRP + i) * kBlockN + m];
+        if (p.bulk_out) {
+            reinterpret_cast<OT*>(ctile)[i * kBlockN + m] = to_out<OT>(acc);
+        } else if (n0 + m < p.N) {
+            static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[kr * kRP + i]) * p.ldc + n0 + m] = to_out<OT>(acc);
+        }
+    }
+    if (p.bulk_out) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        store_tile_rows<OT, kRP>(p, ctile, rows_s + kr * kRP, q, lane, n0);
     }
 }
 
@@ -207,10 +262,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int stages = p.stages;
-    // K split: partial rows pushed here by the other CTAs, [CS][VS/CS][128] fp32
+    // cluster = KSF (K split) x VSF (V split) CTAs: KSPLIT 0 -> V split by
+    // CS, 1 -> K split by CS, 2 -> 2 x 2 (CS = 4).  Rank = kr * VSF + vr.
+    constexpr int KSF = KSPLIT == 1 ? CS : (KSPLIT == 2 ? 2 : 1);
+    constexpr int VSF = CS / KSF;
+    static_assert(KSF * VSF == CS, "cluster shape");
+    // K split: partial rows pushed here by the K peers, [KSF][128][VS/KSF] fp32
     float* recv = reinterpret_cast<float*>(smem + stages * kStageBytes);
-    constexpr bool kKSplit = CS > 1 && KSPLIT;
-    constexpr bool mcast = CS > 1 && !KSPLIT;
+    constexpr bool kKSplit = KSF > 1;
+    constexpr bool mcast = VSF > 1;
     const int recv_bytes = kKSplit ? VS * kBlockN * 4 : 0;
     int32_t* meta_s = reinterpret_cast<int32_t*>(smem + stages * kStageBytes + recv_bytes);  // [kMetaBlocks][64]
     int32_t* rows_s = meta_s + kMetaBlocks * kBlockK;                           // VS
@@ -228,10 +288,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int gp = p.group_ptr[g];
     const int nkb_all = (p.group_ptr[g + 1] - gp) / kBlockK;
     // K split: this CTA's K blocks [kbase, kbase + nkb); V split: its V rows
-    const int kbase = kKSplit ? nkb_all * static_cast<int>(rank) / CS : 0;
-    const int nkb = kKSplit ? nkb_all * (static_cast<int>(rank) + 1) / CS - kbase : nkb_all;
-    const int vbase = kKSplit ? 0 : static_cast<int>(rank) * VS;
-    const uint16_t cmask = static_cast<uint16_t>((1u << CS) - 1u);
+    const int kr = static_cast<int>(rank) / VSF, vr = static_cast<int>(rank) % VSF;
+    const int kbase = kKSplit ? nkb_all * kr / KSF : 0;
+    const int nkb = kKSplit ? nkb_all * (kr + 1) / KSF - kbase : nkb_all;
+    const int vbase = vr * VS;
+    // multicast group: the VSF CTAs that share this CTA's K blocks
+    const uint16_t cmask = static_cast<uint16_t>(((1u << VSF) - 1u) << (kr * VSF));
     const int cps = p.cps;
     const int et = threadIdx.x - 64;  // gather/epilogue thread 0..127 (warps 2..5)
     if (threadIdx.x == 0) trace_event(p.trace, 0);
@@ -248,12 +310,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1 + (cps > 0 ? 32 * kGatherWarps : 0));
-            mbar_init(&empty[s], mcast ? CS : 1);
+            mbar_init(&empty[s], mcast ? VSF : 1);
         }
         mbar_init(accum, 1);
         mbar_init(recv_bar, 1);
-        if (kKSplit)  // the CS-1 peers' partial rows for this CTA
-            mbar_arrive_expect_tx(recv_bar, (CS - 1) * (VS / CS) * kBlockN * 4);
+        if (kKSplit)  // the KSF-1 K peers' partial rows for this CTA
+            mbar_arrive_expect_tx(recv_bar, (KSF - 1) * (VS / KSF) * kBlockN * 4);
         fence_mbar_init();
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmW);
@@ -326,7 +388,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         // a warp owns 4 row groups (16 rows) in every MN block, so both halves
         // of an activation row are requested together
         const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
-        const bool t_issue = lane < per_warp && (!mcast || (gi % CS) == static_cast<int>(rank));
+        const bool t_issue = lane < per_warp && (!mcast || (gi % VSF) == vr);
         // conv: this gather's output positions (fixed for the CTA)
         int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
         bool g_pos_ok = true;
@@ -412,82 +474,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         // hold the [VS][128] output tile for the bulk row stores
         unsigned char* ctile = smem;
         if constexpr (kKSplit) {
-            // K split: CTA r finalises rows [r*VS/CS, (r+1)*VS/CS).  This
-            // thread owns output column m: push the other ranks' rows of its
-            // partial straight from registers into their `recv` slot
-            // (st.async: remote stores that complete on the receiver's
-            // mbarrier), then sum the CS partials of its own rows in rank
-            // order (deterministic).
-            constexpr int kRP = VS / CS;
-            float vals[VS];
-#pragma unroll
-            for (int c = 0; c < (VS + 31) / 32; ++c) {
-                constexpr int kW = VS < 32 ? VS : 32;
-                uint32_t r[32];
-                if (nkb > 0) {
-                    if (kW == 32) tmem_ld32(t_row + c * 32, r);
-                    else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
-                    tmem_ld_wait();
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) r[i] = 0u;
-                }
-#pragma unroll
-                for (int i = 0; i < kW; ++i) vals[c * 32 + i] = __uint_as_float(r[i]);
-            }
-            const uint32_t slot = smem_u32(recv) + static_cast<uint32_t>((rank * kBlockN + m) * kRP * 4);
-#pragma unroll
-            for (int c = 0; c < CS; ++c) {
-                if (c == static_cast<int>(rank)) continue;
-                const uint32_t dst = mapa_shared(slot, c), bar = mapa_shared(smem_u32(recv_bar), c);
-#pragma unroll
-                for (int j = 0; j < kRP; j += 4)
-                    asm volatile(
-                        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                            dst + j * 4),
-                        "f"(vals[c * kRP + j]), "f"(vals[c * kRP + j + 1]), "f"(vals[c * kRP + j + 2]),
-                        "f"(vals[c * kRP + j + 3]), "r"(bar)
-                        : "memory");
-            }
-            if (et == 0) trace_event(p.trace, 24);
-            mbar_wait(recv_bar, 0);
-            if (et == 0) trace_event(p.trace, 25);
-            float out[kRP];
-#pragma unroll
-            for (int i = 0; i < kRP; ++i) out[i] = 0.0f;
-#pragma unroll
-            for (int c = 0; c < CS; ++c) {  // rank order
-                if (c == static_cast<int>(rank)) {
-#pragma unroll
-                    for (int i = 0; i < kRP; ++i) out[i] += vals[c * kRP + i];
-                } else {
-                    const float4* src = reinterpret_cast<const float4*>(recv + (c * kBlockN + m) * kRP);
-#pragma unroll
-                    for (int j = 0; j < kRP / 4; ++j) {
-                        const float4 x = src[j];
-                        out[4 * j] += x.x;
-                        out[4 * j + 1] += x.y;
-                        out[4 * j + 2] += x.z;
-                        out[4 * j + 3] += x.w;
-                    }
-                }
-            }
-            const int n = n0 + m;
-            if (n < p.N) {
-                const int v0 = static_cast<int>(rank) * kRP;
-                if (p.c_dtype == SHFLBW_F32) {
-#pragma unroll
-                    for (int i = 0; i < kRP; ++i) static_cast<float*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = out[i];
-                } else if (p.c_dtype == SHFLBW_BF16) {
-#pragma unroll
-                    for (int i = 0; i < kRP; ++i)
-                        static_cast<__nv_bfloat16*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = __float2bfloat16_rn(out[i]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < kRP; ++i)
-                        static_cast<__half*>(p.C)[static_cast<int64_t>(rows_s[v0 + i]) * p.ldc + n] = __float2half_rn(out[i]);
-                }
-            }
+            if (p.c_dtype == SHFLBW_F32)
+                ksplit_epilogue<float, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar, ctile);
+            else if (p.c_dtype == SHFLBW_BF16)
+                ksplit_epilogue<__nv_bfloat16, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv,
+                                                             recv_bar, ctile);
+            else
+                ksplit_epilogue<__half, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar,
+                                                      ctile);
         } else {
             if (p.c_dtype == SHFLBW_F32) epilogue_rows<float, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
             else if (p.c_dtype == SHFLBW_BF16)
@@ -501,6 +495,258 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     else __syncthreads();
     if (warp == 1) tmem_dealloc(tmem_d, kTmemCols);
     if (threadIdx.x == 0) trace_event(p.trace, 7);
+}
+
+// ===========================================================================
+// Persistent variant: one CTA (cluster) per SM slot loops over (group,
+// column tile) units; the full/empty ring runs on across units and two TMEM
+// accumulators (ping-pong) let the epilogue of unit i overlap the loads and
+// MMAs of unit i+1.  Roles (320 threads): warp 0 weights + stage arming,
+// warp 1 TMEM + MMA, warps 2-5 activation gathers, warps 6-9 epilogue.
+// Used when the grid would need more than one wave of CTAs.
+// ===========================================================================
+constexpr int kThreadsPersist = 320;
+
+template <class OT, int VS>
+__device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc, int nkb, int m, int q, int lane,
+                                              int n0, const int32_t* rows_s, unsigned char* ctile,
+                                              uint64_t* acc_empty) {
+    const int n = n0 + m;
+    const bool live = n < p.N;
+#pragma unroll
+    for (int c = 0; c < (VS + 31) / 32; ++c) {
+        constexpr int kW = VS < 32 ? VS : 32;
+        uint32_t r[32];
+        if (nkb > 0) {
+            if (kW == 32) tmem_ld32(t_acc + c * 32, r);
+            else tmem_ld16(t_acc + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tmem_ld_wait();
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (p.bulk_out) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                reinterpret_cast<OT*>(ctile)[(c * 32 + i) * kBlockN + m] = to_out<OT>(__uint_as_float(r[i]));
+        } else if (live) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[c * 32 + i]) * p.ldc + n] =
+                    to_out<OT>(__uint_as_float(r[i]));
+        }
+    }
+    // accumulator drained: the MMA warp may start the next unit in it
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_empty);
+    if (p.bulk_out) {
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        store_tile_rows<OT, VS>(p, ctile, rows_s, q, lane, n0);
+    }
+}
+
+template <int DT, int VS, int CS, int KIND>
+__global__ void __launch_bounds__(kThreadsPersist, 1)
+    k_spmm_persist(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW, TcParams p,
+                   int units, int n_tiles) {
+    using WL = WeightLayout<VS>;
+    constexpr int kStageBytes = kABytes + WL::kBytes;
+    constexpr uint32_t kAccCols = VS < 32 ? 32 : VS;
+    constexpr uint32_t kTmemCols = 2 * kAccCols;
+    constexpr uint32_t kIdesc = umma_idesc_f16(DT == SHFLBW_BF16 ? 1 : 0, kBlockN, VS);
+    constexpr bool mcast = CS > 1;
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int stages = p.stages;
+    unsigned char* ctile = smem + stages * kStageBytes;                                 // [VS][128] out
+    int32_t* meta_s = reinterpret_cast<int32_t*>(ctile + VS * kBlockN * 4);            // [kMetaBlocks][64]
+    int32_t* rows_s = meta_s + kMetaBlocks * kBlockK;                                  // VS
+    uint64_t* full = reinterpret_cast<uint64_t*>(rows_s + (VS < 2 ? 2 : VS));
+    uint64_t* empty = full + stages;
+    uint64_t* acc_full = empty + stages;  // [2]
+    uint64_t* acc_empty = acc_full + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
+    const int cid = blockIdx.x / CS, nclusters = gridDim.x / CS;
+    const int vbase = static_cast<int>(rank) * VS;
+    const uint16_t cmask = static_cast<uint16_t>((1u << CS) - 1u);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], mcast ? CS : 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmW);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    if (CS > 1) cluster_sync();
+    else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) grid_launch_dependents();
+
+    if (warp == 0) {
+        // ---------------- stage arming + weights ----------------
+        if (lane == 0) {
+            int kbg = 0;
+            for (int u = cid; u < units; u += nclusters) {
+                const int g = p.g_begin + u / n_tiles;
+                const int gp = p.group_ptr[g];
+                const int nkb = (p.group_ptr[g + 1] - gp) / kBlockK;
+                for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                    const int s = kbg % stages;
+                    if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], kStageBytes);
+#pragma unroll
+                    for (int sl = 0; sl < WL::kSlabs; ++sl)
+                        tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
+                                    vbase + sl * 64, gp + kb * kBlockK);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t a_row = KIND == 0 ? 128u : static_cast<uint32_t>(p.bw) * 2;
+        const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
+        if (lane == 0) {
+            int kbg = 0, i = 0;
+            for (int u = cid; u < units; u += nclusters, ++i) {
+                const int g = p.g_begin + u / n_tiles;
+                const int nkb = (p.group_ptr[g + 1] - p.group_ptr[g]) / kBlockK;
+                const int b = i & 1;
+                mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + b * kAccCols;
+                for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                    const int s = kbg % stages;
+                    mbar_wait(&full[s], (kbg / stages) & 1);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
+                    const uint32_t w_addr = a_addr + kABytes;
+#pragma unroll
+                    for (int ks = 0; ks < kBlockK / 16; ++ks) {
+                        const uint64_t adesc = umma_smem_desc(a_addr + ks * 16 * a_row, kBlockK * a_row, 8 * a_row,
+                                                              a_layout);
+                        const uint64_t bdesc = umma_smem_desc(w_addr + ks * 16 * WL::kRowBytes, WL::kSlabBytes,
+                                                              WL::kSBO, WL::kLayout);
+                        umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
+                    }
+                    if constexpr (!mcast) umma_commit(&empty[s]);
+                    else umma_commit_mc(&empty[s], cmask);
+                }
+                if (nkb > 0) umma_commit(&acc_full[b]);
+                else mbar_arrive(&acc_full[b]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < 6) {
+        // ---------------- activation gathers ----------------
+        const int gw = warp - 2, et = threadIdx.x - 64;  // et 0..127
+        const int bw = KIND == 0 ? 64 : p.bw;
+        const int nblk = kBlockN / bw;
+        const int blk_bytes = kBlockK * bw * 2;
+        const int per_warp = 16 * nblk / kGatherWarps;
+        const int gi = gw * per_warp + lane;
+        const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
+        const bool t_issue = lane < per_warp && (!mcast || (gi % CS) == static_cast<int>(rank));
+        grid_dependency_wait();  // B may be the previous kernel's output
+        int kbg = 0;
+        for (int u = cid; u < units; u += nclusters) {
+            const int g = p.g_begin + u / n_tiles;
+            const int n0 = (u % n_tiles) * kBlockN;
+            const int gp = p.group_ptr[g];
+            const int nkb = (p.group_ptr[g + 1] - gp) / kBlockK;
+            int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
+            bool g_pos_ok = true;
+            if (KIND == 1) {
+                const int base_n = n0 + g_b * p.bw;
+                const int pos = base_n / p.Nb;
+                g_x = base_n - pos * p.Nb;
+                g_pos_ok = pos < p.PQ;
+                g_p0 = (pos / p.Q) * p.stride - p.pad;
+                g_q0 = (pos % p.Q) * p.stride - p.pad;
+            }
+            for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                const int s = kbg % stages;
+                const int win = kb % kMetaBlocks;
+                if (win == 0) {  // stage this unit's next window of column indices
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    const int nb = nkb - kb < kMetaBlocks ? nkb - kb : kMetaBlocks;
+                    const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + kb * kBlockK);
+                    for (int x = et; x < nb * (kBlockK / 4); x += 128) reinterpret_cast<int4*>(meta_s)[x] = src[x];
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                }
+                if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
+                if (t_issue) {
+                    int4 ci = reinterpret_cast<const int4*>(meta_s + win * kBlockK)[g_rg];
+                    if (KIND == 1) {
+                        auto conv_row = [&](int c) -> int {
+                            if (c < 0 || !g_pos_ok) return -1;
+                            const int ch = c / p.RS, rs = c - ch * p.RS;
+                            const int r = rs / p.S, sx = rs - r * p.S;
+                            const int h = g_p0 + r, w = g_q0 + sx;
+                            if (h < 0 || h >= p.H || w < 0 || w >= p.W) return -1;
+                            return (ch * p.H + h) * p.W + w;
+                        };
+                        ci.x = conv_row(ci.x);
+                        ci.y = conv_row(ci.y);
+                        ci.z = conv_row(ci.z);
+                        ci.w = conv_row(ci.w);
+                    }
+                    void* dst = smem + s * kStageBytes + g_b * blk_bytes + g_rg * (4 * bw * 2);
+                    if constexpr (!mcast)
+                        tma_gather4(dst, &tmB, &full[s], g_x, ci.x, ci.y, ci.z, ci.w);
+                    else
+                        tma_gather4_mc(dst, &tmB, &full[s], cmask, g_x, ci.x, ci.y, ci.z, ci.w);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ---------------- epilogue ----------------
+        const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - 192;
+        grid_dependency_wait();  // C may still be read by the previous kernel
+        int i = 0;
+        for (int u = cid; u < units; u += nclusters, ++i) {
+            const int g = p.g_begin + u / n_tiles;
+            const int n0 = (u % n_tiles) * kBlockN;
+            const int nkb = (p.group_ptr[g + 1] - p.group_ptr[g]) / kBlockK;
+            const int b = i & 1;
+            asm volatile("bar.sync 3, 128;" ::: "memory");  // previous unit done with rows_s / ctile
+            for (int v = et; v < VS; v += 128) {
+                const int64_t gr = static_cast<int64_t>(g) * p.V + vbase + v;
+                rows_s[v] = p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
+                                      : p.row_indices[gr];
+            }
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            mbar_wait(&acc_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            const uint32_t t_acc = tmem_base + b * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+            if (p.c_dtype == SHFLBW_F32)
+                persist_store<float, VS>(p, t_acc, nkb, m, q, lane, n0, rows_s, ctile, &acc_empty[b]);
+            else if (p.c_dtype == SHFLBW_BF16)
+                persist_store<__nv_bfloat16, VS>(p, t_acc, nkb, m, q, lane, n0, rows_s, ctile, &acc_empty[b]);
+            else
+                persist_store<__half, VS>(p, t_acc, nkb, m, q, lane, n0, rows_s, ctile, &acc_empty[b]);
+        }
+    }
+    tc_fence_before();
+    if (CS > 1) cluster_sync_relaxed();
+    else __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
 }
 
 // ---------------- host side ----------------
@@ -627,9 +873,52 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     return SHFLBW_OK;
 }
 
+
+template <int DT, int VS, int CS, int KIND>
+int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+                   cudaStream_t s) {
+    constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
+    const size_t smem = static_cast<size_t>(prm.stages) * kStage + static_cast<size_t>(VS) * kBlockN * 4 + 1024 +
+                        kMetaBlocks * kBlockK * 4 + (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 5) * 8 + 16;
+    auto kern = k_spmm_persist<DT, VS, CS, KIND>;
+    static std::atomic<size_t> configured{0};
+    if (smem > configured.load(std::memory_order_relaxed)) {
+        SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured.store(smem, std::memory_order_relaxed);
+    }
+    const int units = n_tiles * groups;
+    const int clusters = std::min(units, num_sms() / CS);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * CS, 1, 1);
+    cfg.blockDim = dim3(kThreadsPersist, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = option("pdl") ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, prm, units, n_tiles));
+    count_launch();
+    return SHFLBW_OK;
+}
+
 template <int DT, int VS>
 int dispatch_cs(int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm,
                 int n_tiles, int groups, cudaStream_t s) {
+    if (prm.persistent) {
+        if (kind == 1) return launch_persist<DT, VS, 1, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        switch (cs) {
+            case 1: return launch_persist<DT, VS, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 2: return launch_persist<DT, VS, 2, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 4: return launch_persist<DT, VS, 4, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        }
+        return SHFLBW_UNSUPPORTED;
+    }
     if (kind == 1) return launch_tc<DT, VS, 1, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
     switch (cs * 2 + prm.ksplit) {
         case 2: case 3: return launch_tc<DT, VS, 1, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
@@ -637,6 +926,7 @@ int dispatch_cs(int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW
         case 5: return launch_tc<DT, VS, 2, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
         case 8: return launch_tc<DT, VS, 4, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
         case 9: return launch_tc<DT, VS, 4, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 10: return launch_tc<DT, VS, 4, 0, 2>(tmB, tmW, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }
@@ -676,27 +966,59 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     const int n_tiles = (b.N + kBlockN - 1) / kBlockN;
 
     // Cluster split for grids that would leave SMs idle: CS CTAs share one
-    // (group, column tile).  K split (default): each gathers 1/CS of the K
-    // blocks -- 1/CS of the activation bytes per SM -- and the partials are
-    // reduced through DSMEM.  V split ("split_mode" = 2): each owns V/CS rows
-    // and the activation tile is multicast to all CS CTAs.
+    // (group, column tile).  Each SM fills its activation tiles at the TMA
+    // gather rate (~20 B/cycle received, multicast or not -- DESIGN.md §5),
+    // so splitting K is what shortens a deep group's main loop.  Modes
+    // ("split_mode"):
+    //   3  V split: each CTA owns V/CS rows; the activation tile is multicast
+    //      to all CS CTAs (bit-identical to CS = 1);
+    //   1  K split: each gathers 1/CS of the K blocks, fp32 partials reduced
+    //      through DSMEM;
+    //   2  2 x 2 (CS = 4): V split over a CTA pair (multicast) and K split
+    //      over two pairs -- half the gathers per SM, VS/2 rows per CTA cross
+    //      DSMEM;
+    //   0  auto (default): an explicit "split" means V split; otherwise, when
+    //      4 CTAs per unit fit on the GPU, by the widest group's K blocks
+    //      (measured): >= 24 -> K split by 4, >= 8 (V >= 64) ->
+    //      2 x 2, else V split.
     const int min_kb = 2;  // K blocks per CTA worth splitting for
     const int kb_all = (a->cols + kBlockK - 1) / kBlockK;
+    const int kb_grp = a->max_group_cols > 0 ? a->max_group_cols / kBlockK : kb_all;  // widest group
     int cs = static_cast<int>(option("split"));
-    const bool vsplit = option("split_mode") != 1;  // V split (multicast) unless K split is requested
-    if (cs <= 0) {
+    int64_t mode = option("split_mode");
+    if (mode < 0 || mode > 3) return fail(SHFLBW_BAD_PARAMS, "split_mode must be 0..3");
+    const int64_t units = static_cast<int64_t>(n_tiles) * groups;
+    if (mode == 0) {
+        mode = 3;
+        if (cs <= 0 && units * 4 <= num_sms() && b.kind == 0) {
+            if (kb_grp >= 24) {
+                mode = 1;
+                cs = 4;
+            } else if (kb_grp >= 8 && V >= 64) {
+                mode = 2;
+            }
+        }
+    }
+    bool hybrid = mode == 2 && V >= 32 && (cs == 4 || (cs <= 0 && units * 4 <= num_sms()));
+    const bool vsplit = mode != 1 && !hybrid;
+    if (hybrid) {
+        cs = 4;
+    } else if (cs <= 0) {
         cs = 1;
-        const int64_t units = static_cast<int64_t>(n_tiles) * groups;
         if (vsplit) {
             while (cs < 4 && V / (cs * 2) >= 16 && units * cs * 2 <= num_sms()) cs *= 2;
         } else {
             while (cs < 4 && units * cs * 2 <= num_sms() && kb_all / (cs * 2) >= min_kb) cs *= 2;
         }
     }
-    if (b.kind == 1) cs = 1;
+    if (b.kind == 1) {
+        cs = 1;
+        hybrid = false;
+    }
     if (cs != 1 && cs != 2 && cs != 4) return fail(SHFLBW_BAD_PARAMS, "split must be 1, 2 or 4");
     if (vsplit && (V % cs != 0 || V / cs < 16)) return SHFLBW_UNSUPPORTED;
-    const int vs = vsplit ? V / cs : V;
+    const int vs = hybrid ? V / 2 : (vsplit ? V / cs : V);
+    const int ksf = hybrid ? 2 : (vsplit ? 1 : cs);  // K split factor
 
     TcParams prm{};
     prm.row_indices = a->row_indices;
@@ -721,7 +1043,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.pad = b.pad;
     prm.Q = b.Q;
     prm.PQ = b.P * b.Q;
-    prm.ksplit = (cs > 1 && !vsplit) ? 1 : 0;
+    prm.ksplit = hybrid ? 2 : ((cs > 1 && !vsplit) ? 1 : 0);
     prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
     if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
     prm.trace = reinterpret_cast<unsigned long long*>(option("trace"));
@@ -731,10 +1053,15 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
                              ((static_cast<int64_t>(b.N) * esz) % 16 == 0);
         prm.bulk_out = aligned && !option("no_bulk_out") ? 1 : 0;
     }
+    // persistent when one wave of CTAs cannot cover the units (option
+    // "persistent": -1 never, 1 always, 0 auto)
+    {
+        const int64_t opt = option("persistent");
+        prm.persistent = !prm.ksplit && opt > 0 ? 1 : 0;  // opt-in: slower than 2 CTAs/SM so far
+    }
     int stages = static_cast<int>(option("stages"));
-    if (stages <= 0) stages = vs >= 128 ? 3 : 4;
-    const int kb_grp = a->max_group_cols > 0 ? a->max_group_cols / kBlockK : kb_all;  // widest group
-    const int max_kb = prm.ksplit ? (kb_grp + cs - 1) / cs : kb_grp;                   // K blocks per CTA
+    if (stages <= 0) stages = prm.persistent ? (vs >= 128 ? 4 : 6) : (vs >= 128 ? 3 : 4);
+    const int max_kb = (kb_grp + ksf - 1) / ksf;                                        // K blocks per CTA
     if (stages > max_kb) stages = max_kb < 2 ? 2 : max_kb;
     prm.stages = stages;
 

@@ -56,7 +56,7 @@ def main():
         "split=0,stages=2", "split=0,stages=6"]
     print(f"workload M={M} N={N} K={K} V={V} alpha={alpha} sets={nsets}")
     for cfg in configs:
-        opts = {"split": 0, "pdl": 1, "stages": 0, "force_simt": 0, "cp_async_slabs": 0, "split_mode": 0}
+        opts = {"split": 0, "pdl": 1, "stages": 0, "force_simt": 0, "cp_async_slabs": 0, "split_mode": 0, "persistent": 0}
         for kv in cfg.split(","):
             k, v = kv.split("=")
             opts[k] = int(v)
@@ -66,7 +66,7 @@ def main():
         us = ms / args.steps * 1e3
         print(f"{cfg:32s} {us:8.2f} us/step  {2 * M * N * K / (us * 1e-6) / 1e12:8.1f} dense-eq TFLOP/s",
               flush=True)
-    for k, v in {"split": 0, "pdl": 1, "stages": 0, "force_simt": 0, "cp_async_slabs": 0, "split_mode": 0}.items():
+    for k, v in {"split": 0, "pdl": 1, "stages": 0, "force_simt": 0, "cp_async_slabs": 0, "split_mode": 0, "persistent": 0}.items():
         sb.set_option(k, v)
 
 

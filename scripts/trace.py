@@ -16,15 +16,22 @@ import paper_2203_05016_b200 as sb
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="ns")
 ap.add_argument("--opts", default="")
+ap.add_argument("--K", type=int, default=0)
+ap.add_argument("--chain", type=int, default=0, help="launch this many SpMMs back to back on rotating "
+                "operand sets (warm, PDL-overlapped) and trace the last one")
 args = ap.parse_args()
-wl = bench.WORKLOADS[args.workload]
+wl = dict(bench.WORKLOADS[args.workload])
+if args.K:
+    wl["K"] = args.K
 M, N, K, V, alpha = wl["M"], wl["N"], wl["K"], wl["V"], wl["alpha"]
 dev = torch.device("cuda", 0)
 cpg = int(round(alpha * K))
 mask = torch.from_numpy(bench.synth_mask(M, K, V, cpg, 1234)).to(dev)
-a = sb.compress_shflbw(bench.uniform_bf16(torch, (M, K), 100, dev), mask, V)
-B = bench.uniform_bf16(torch, (K, N), 200, dev)
-C = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+nset = max(1, args.chain)
+mats = [sb.compress_shflbw(bench.uniform_bf16(torch, (M, K), 100 + i, dev), mask, V) for i in range(nset)]
+Bs = [bench.uniform_bf16(torch, (K, N), 200 + i, dev) for i in range(nset)]
+Cs = [torch.empty((M, N), dtype=torch.bfloat16, device=dev) for i in range(nset)]
+a, B, C = mats[0], Bs[0], Cs[0]
 for kv in [x for x in args.opts.split(",") if x]:
     k, v = kv.split("=")
     sb.set_option(k, int(v))
@@ -35,7 +42,11 @@ for it in range(3):
     torch.cuda.synchronize()
     tr.zero_()
     sb.set_option("trace", tr.data_ptr())
-    sb.spmm_execute(a, B, out=C)
+    if args.chain:
+        for i in range(args.chain):
+            sb.spmm_execute(mats[i], Bs[i], out=Cs[i])
+    else:
+        sb.spmm_execute(a, B, out=C)
     torch.cuda.synchronize()
     sb.set_option("trace", 0)
 t = tr.cpu().numpy().reshape(-1, 32)
@@ -44,7 +55,8 @@ t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
 names = ["entry", "setup", "dep_wait", "first_full", "last_mma", "accum", "epi_done", "exit"]
 names += [f"full[{k}]" for k in range(8)] + [f"issue[{k}]" for k in range(8)] + ["partial_ok", "recv_ok"]
-print(f"{args.workload} {args.opts}: {len(t)} CTAs, span {rel[:, 7].max():.2f} us")
+print(f"{args.workload} K={K} {args.opts} chain={args.chain}: {len(t)} CTAs, span {rel[:, 7].max():.2f} us, "
+      f"dep_wait(min)->exit(max) {rel[:, 7].max() - rel[t[:, 2] > 0, 2].min():.2f} us")
 for e, nm in enumerate(names):
     if not nm:
         continue

@@ -28,7 +28,8 @@ def sb():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2203_05016_b200 as sb
-    for k, v in (("force_simt", 0), ("split", 0), ("stages", 0), ("split_mode", 0), ("cp_async_slabs", 0)):
+    for k, v in (("force_simt", 0), ("split", 0), ("stages", 0), ("split_mode", 0), ("cp_async_slabs", 0),
+                 ("persistent", 0)):
         sb.set_option(k, v)
     return sb
 
@@ -217,7 +218,8 @@ def test_spmm_acceptance_instances(sb, oracle):
 @pytest.mark.parametrize("M,N,K,V,alpha", [(2048, 128, 2048, 64, 0.25), (2048, 128, 2048, 32, 0.25),
                                            (2048, 128, 2048, 128, 0.25), (4096, 128, 1024, 64, 0.25),
                                            (512, 4096, 2048, 64, 0.25), (2048, 512, 512, 32, 0.5),
-                                           (512, 256, 512, 16, 0.5)])
+                                           (512, 256, 512, 16, 0.5), (2048, 128, 8192, 64, 0.25),
+                                           (2048, 256, 4096, 128, 0.1)])
 def test_spmm_tc_matches_oracle(sb, oracle, M, N, K, V, alpha):
     mask, W, B = synthetic(oracle, M, K, N, V, alpha)
     a, p = compress_both(sb, oracle, W, mask, V)
@@ -243,17 +245,24 @@ def test_spmm_tc_equals_simt_within_tolerance_and_split_is_bitwise(sb, oracle):
     want = oracle.spmm(p, B)
     sb.set_option("split", 1)
     base = sb.spmm_execute(a, Bd).cpu().numpy()
-    sb.set_option("split_mode", 2)
+    sb.set_option("split_mode", 0)
     for split in (2, 4):
         sb.set_option("split", split)
         assert np.array_equal(sb.spmm_execute(a, Bd).cpu().numpy(), base)
     sb.set_option("split_mode", 1)
+    ks = {}
     for split in (2, 4):
         sb.set_option("split", split)
         k1 = sb.spmm_execute(a, Bd).cpu().numpy()
         k2 = sb.spmm_execute(a, Bd).cpu().numpy()
         assert np.array_equal(k1, k2)
         assert oracle.rel_frobenius(k1, want) <= TOL
+        ks[split] = k1
+    # 2 x 2: the same two K halves as K split by 2, summed in the same order
+    sb.set_option("split_mode", 2)
+    sb.set_option("split", 4)
+    h = sb.spmm_execute(a, Bd).cpu().numpy()
+    assert np.array_equal(h, ks[2])
     sb.set_option("split", 0)
     sb.set_option("split_mode", 0)
     sb.set_option("force_simt", 1)
@@ -263,8 +272,8 @@ def test_spmm_tc_equals_simt_within_tolerance_and_split_is_bitwise(sb, oracle):
     assert oracle.rel_frobenius(base, simt) <= TOL
 
 
-@pytest.mark.parametrize("split", [2, 4])
-def test_spmm_ksplit_ragged(sb, oracle, split):
+@pytest.mark.parametrize("split,mode", [(2, 1), (4, 1), (4, 2)])
+def test_spmm_ksplit_ragged(sb, oracle, split, mode):
     """K split with groups whose K-block count is not a multiple of the split
     (and empty groups)."""
     rs = np.random.RandomState(21)
@@ -278,11 +287,31 @@ def test_spmm_ksplit_ragged(sb, oracle, split):
     B = oracle.round16(oracle.random_dense(K, N, 6))
     a, p = compress_both(sb, oracle, W, mask, V)
     sb.set_option("split", split)
-    sb.set_option("split_mode", 1)
+    sb.set_option("split_mode", mode)
     got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
     sb.set_option("split", 0)
     sb.set_option("split_mode", 0)
     assert oracle.rel_frobenius(got, oracle.spmm(p, B)) <= TOL
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_spmm_ksplit_unaligned_output(sb, oracle, mode, out_dtype):
+    """K-split epilogues with per-element stores (output rows not 16-byte
+    aligned, so the staged vector-store path is off): same values as the
+    aligned path."""
+    mask, W, B = synthetic(oracle, 1024, 2048, 136, 64, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, 64)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("split", 4)
+    sb.set_option("split_mode", mode)
+    aligned = sb.spmm_execute(a, Bd, out_dtype=out_dtype)
+    big = torch.zeros((1024, 137), dtype=out_dtype, device="cuda")
+    sb.spmm_execute(a, Bd, out=big[:, 1:])
+    sb.set_option("split", 0)
+    sb.set_option("split_mode", 0)
+    assert torch.equal(big[:, 1:], aligned)
+    assert oracle.rel_frobenius(aligned.float().cpu().numpy(), oracle.spmm(p, B)) <= (TOL if out_dtype == torch.float32 else 1e-2)
 
 
 @pytest.mark.parametrize("N", [128, 200, 1000])
@@ -456,3 +485,42 @@ def test_conv_geometry_errors(sb, oracle):
         sb.conv2d(a, torch.zeros(2, 6, 6, 1, device="cuda"), sb.ConvGeometry(3, 3))
     with pytest.raises(sb.BadGeometry):  # (6-3) % 2 != 0
         sb.conv2d(a, torch.zeros(3, 6, 6, 1, device="cuda"), sb.ConvGeometry(3, 3, 2))
+
+
+@pytest.mark.parametrize("M,N,K,V,alpha,split", [(2048, 4096, 512, 64, 0.25, 0), (512, 2048, 2048, 128, 0.25, 0),
+                                                 (1024, 1000, 700, 32, 0.3, 0), (2048, 256, 1024, 64, 0.25, 4),
+                                                 (256, 520, 300, 16, 0.5, 0)])
+def test_persistent_kernel_bitwise(sb, oracle, M, N, K, V, alpha, split):
+    """The persistent kernel (units looped inside a CTA, ping-pong TMEM
+    accumulators) computes every unit with the same MMA sequence as the
+    one-CTA-per-unit kernel: identical bits, fp32 and bf16 out."""
+    mask, W, B = synthetic(oracle, M, K, N, V, alpha)
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("split", split)
+    outs = {}
+    for mode in (-1, 1):
+        sb.set_option("persistent", mode)
+        outs[mode] = (sb.spmm_execute(a, Bd).cpu().numpy(),
+                      sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
+    sb.set_option("persistent", 0)
+    sb.set_option("split", 0)
+    assert oracle.rel_frobenius(outs[1][0], oracle.spmm(p, B)) <= TOL
+    assert np.array_equal(outs[1][0], outs[-1][0]) and np.array_equal(outs[1][1], outs[-1][1])
+
+
+def test_persistent_conv(sb, oracle):
+    C, H, Kf, V, Nb = 32, 12, 128, 64, 32
+    crs = C * 9
+    mask = oracle.random_shflbw_mask(Kf, crs, V, crs // 4, oracle.rng(8))
+    W = oracle.round16(oracle.random_dense(Kf, crs, 1))
+    x = oracle.round16(oracle.fill_uniform(oracle.rng(9), C * H * H * Nb).reshape(C, H, H, Nb))
+    a, p = compress_both(sb, oracle, W, mask, V)
+    xd = dev(x, torch.bfloat16)
+    sb.set_option("persistent", 1)
+    got = sb.conv2d(a, xd, sb.ConvGeometry(3, 3, 1, 1)).cpu().numpy()
+    sb.set_option("persistent", -1)
+    ref = sb.conv2d(a, xd, sb.ConvGeometry(3, 3, 1, 1)).cpu().numpy()
+    sb.set_option("persistent", 0)
+    assert np.array_equal(got, ref)
+    assert oracle.rel_frobenius(got, oracle.conv2d(p, x, 3, 3, 1, 1)) <= TOL
