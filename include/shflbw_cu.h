@@ -71,8 +71,12 @@ typedef struct shflbw_cu_matrix {
     int32_t owns;         /* 1: free with shflbw_cu_matrix_free            */
     int32_t max_group_cols; /* max_g (group_ptr[g+1]-group_ptr[g]); 0 = unknown
                                (kernels then size pipelines from `cols`)    */
-    int32_t reserved;
+    int32_t reserved;   /* flags: SHFLBW_FOLDED                          */
 } shflbw_cu_matrix;
+
+/* shflbw_cu_matrix.reserved bit: col_idx were remapped by
+ * shflbw_cu_fold_input_permutation (SpMM input in the producer's group order) */
+#define SHFLBW_FOLDED 1
 
 /* ---- library ---------------------------------------------------------- */
 const char* shflbw_cu_last_error(void);
@@ -88,9 +92,10 @@ int shflbw_cu_version(void);
  * "split_mode" (cluster split kind: 0 = auto, 1 = K split with a DSMEM
  * reduction of fp32 partials, 2 = 2 x 2: V split over a CTA pair and K split
  * over two pairs, 3 = V split with multicast activation tiles; with mode 0 an
- * explicit "split" means V split), "persistent" (1: the
- * persistent-CTA kernel that loops over (group, column tile) units; default
- * 0 = one CTA per unit), "cp_async_slabs" (0..2 activation slabs filled by
+ * explicit "split" means V split), "persistent" (N = 1 or 2: the persistent
+ * kernel, N CTAs per SM looping over (group, column tile) units; -1: one CTA
+ * per unit; 0 = auto: persistent with 2 CTAs per SM once the grid holds two
+ * full waves of units), "cp_async_slabs" (0..2 activation slabs filled by
  * cp.async instead of TMA gather4), "no_bulk_out" (1: per-element output
  * stores).  All variants give results within the same tolerance; V split,
  * cp.async and persistent are bit-identical to the default.
@@ -142,7 +147,7 @@ int shflbw_cu_matrix_download(const shflbw_cu_matrix* m, uint32_t* row_indices,
  * layout checks and serialisers).
  * Synchronises `stream`. */
 int shflbw_cu_matrix_export_raw(const shflbw_cu_matrix* m, int32_t* group_ptr, int32_t* col_idx,
-                                uint16_t* values, shflbw_stream_t stream);
+                                void* values, shflbw_stream_t stream);
 
 /* decompress(ShflBWMatrix), src/formats.cpp:195-206: dense [dev] M*K f32. */
 int shflbw_cu_decompress(const shflbw_cu_matrix* m, float* dense, shflbw_stream_t stream);
@@ -169,6 +174,22 @@ int shflbw_cu_spmm_groups(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_
                           const void* B, int32_t K_b, int32_t N, int64_t ldb, void* C,
                           int32_t c_dtype, int64_t ldc, int32_t compact,
                           shflbw_stream_t stream);
+
+/* Permutation folding (the paper's layout fusion,
+ * PAPER.md:181-183).  A layer whose SpMM wrote group-ordered rows
+ * (shflbw_cu_spmm_groups over all groups with compact = 1: row i holds logical
+ * row producer_rows[i], producer_rows = that layer's row_indices) feeds the
+ * next layer `a` directly once a's column indices are remapped through the
+ * inverse permutation, col -> i with producer_rows[i] == col.  No un-permute
+ * pass, and under sharding no scatter after the all-gather.  Rewrites
+ * a->col_idx in place; values and accumulation order are unchanged, so every
+ * result is bit-identical to the unfolded chain.  producer_rows [dev] holds
+ * a->cols entries and must be a permutation of 0..a->cols-1 (else
+ * BAD_PARAMS, matrix unchanged).  Sets SHFLBW_FOLDED in a->reserved; conv2d
+ * and matrix_download reject folded matrices (decompress returns the weight
+ * over the folded input order, W[:, producer_rows]).  Synchronises `stream`. */
+int shflbw_cu_fold_input_permutation(shflbw_cu_matrix* a, const int32_t* producer_rows,
+                                     shflbw_stream_t stream);
 
 /* C[row_indices[r]][:] = C_perm[r][:] for r < M (2- or 4-byte elements);
  * rows with row_indices[r] < 0 (padding of an all-gathered buffer) are skipped. */

@@ -8,10 +8,10 @@ package is a thin host mirror of the reference interface over that ABI
 """
 from .shflbw import (BadGeometry, BadParams, ConvGeometry, Error, NonConformantMask, ShapeMismatch,
                      ShflBWMatrix, TileConfig, compress_shflbw, conv2d, conv_output_size, decompress,
-                     launch_count, set_option, spmm_execute, spmm_groups, unpermute_rows, upload,
-                     validate_pattern)
+                     fold_input_permutation, launch_count, set_option, spmm_execute, spmm_groups,
+                     unpermute_rows, upload, validate_pattern)
 
 __all__ = ["BadGeometry", "BadParams", "ConvGeometry", "Error", "NonConformantMask", "ShapeMismatch",
            "ShflBWMatrix", "TileConfig", "compress_shflbw", "conv2d", "conv_output_size", "decompress",
-           "launch_count", "set_option", "spmm_execute", "spmm_groups", "unpermute_rows", "upload",
-           "validate_pattern"]
+           "fold_input_permutation", "launch_count", "set_option", "spmm_execute", "spmm_groups",
+           "unpermute_rows", "upload", "validate_pattern"]

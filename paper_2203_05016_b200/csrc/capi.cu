@@ -147,11 +147,12 @@ int shflbw_cu_matrix_upload(int32_t M, int32_t K, int32_t V, const uint32_t* row
 int shflbw_cu_matrix_download(const shflbw_cu_matrix* m, uint32_t* row_indices, uint32_t* group_ncols,
                               uint32_t* cols, float* values, shflbw_stream_t stream) {
     if (int st = check_matrix(m)) return st;
+    if (m->reserved & SHFLBW_FOLDED) return fail(SHFLBW_BAD_PARAMS, "matrix has a folded input permutation");
     return download_impl(m, row_indices, group_ncols, cols, values, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int shflbw_cu_matrix_export_raw(const shflbw_cu_matrix* m, int32_t* group_ptr, int32_t* col_idx,
-                                uint16_t* values, shflbw_stream_t stream) {
+                                void* values, shflbw_stream_t stream) {
     if (int st = check_matrix(m)) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     SBW_CUDA(cudaMemcpyAsync(group_ptr, m->group_ptr, sizeof(int32_t) * (m->groups + 1), cudaMemcpyDeviceToHost, s));
@@ -211,6 +212,7 @@ int shflbw_cu_conv2d(const shflbw_cu_matrix* w, const void* input, int32_t C, in
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (int st = check_compute_matrix(w)) return st;
     if (int st = check_out_dtype(out_dtype)) return st;
+    if (w->reserved & SHFLBW_FOLDED) return fail(SHFLBW_BAD_PARAMS, "conv2d: matrix has a folded input permutation");
     int32_t P = 0, Q = 0;
     if (int st = shflbw_cu_conv_output_size(H, W, R, S, stride, pad, &P, &Q)) return st;
     if (static_cast<int64_t>(w->cols) != static_cast<int64_t>(C) * R * S)

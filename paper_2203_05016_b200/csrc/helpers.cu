@@ -56,6 +56,24 @@ __global__ void k_tile_mma(float* __restrict__ acc, const float* __restrict__ a_
     }
 }
 
+// permutation folding (shflbw_cu_fold_input_permutation)
+__global__ void k_invert_perm(const int32_t* __restrict__ perm, int n, int32_t* __restrict__ inv,
+                              uint32_t* __restrict__ flag) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int32_t p = perm[i];
+        if (p < 0 || p >= n) atomicOr(flag, 1u);
+        else if (atomicExch(&inv[p], i) != -1) atomicOr(flag, 2u);  // duplicate entry
+    }
+}
+
+__global__ void k_fold_cols(int32_t* __restrict__ col_idx, int64_t total, const int32_t* __restrict__ inv) {
+    for (int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; j < total;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t c = col_idx[j];
+        if (c >= 0) col_idx[j] = inv[c];  // pad entries (-1) stay pads
+    }
+}
+
 int blocks_for(int64_t n) {
     const int64_t b = (n + 255) / 256;
     return static_cast<int>(b < 1 ? 1 : (b > 65536 ? 65536 : b));
@@ -112,3 +130,34 @@ int shflbw_cu_tile_mma(float* acc, const float* a_tile, const float* b_tile, int
 }
 
 }  // extern "C"
+
+int shflbw_cu_fold_input_permutation(shflbw_cu_matrix* a, const int32_t* producer_rows, shflbw_stream_t stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!a || !a->group_ptr || a->cols < 0) return fail(SHFLBW_BAD_PARAMS, "fold: invalid matrix");
+    if (a->reserved & SHFLBW_FOLDED) return fail(SHFLBW_BAD_PARAMS, "fold: input permutation already folded");
+    const int n = a->cols;
+    if (n > 0 && !producer_rows) return fail(SHFLBW_BAD_PARAMS, "fold: producer_rows is null");
+    if (n > 0) {
+        int32_t* inv = nullptr;
+        uint32_t* flag = nullptr;
+        SBW_CUDA(cudaMallocAsync(&inv, static_cast<size_t>(n) * sizeof(int32_t), s));
+        SBW_CUDA(cudaMallocAsync(&flag, sizeof(uint32_t), s));
+        SBW_CUDA(cudaMemsetAsync(inv, 0xff, static_cast<size_t>(n) * sizeof(int32_t), s));
+        SBW_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t), s));
+        k_invert_perm<<<blocks_for(n), 256, 0, s>>>(producer_rows, n, inv, flag);
+        SBW_LAUNCHED("k_invert_perm");
+        uint32_t h = 0;
+        SBW_CUDA(cudaMemcpyAsync(&h, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        SBW_CUDA(cudaStreamSynchronize(s));
+        if (!h && a->total_cols > 0) {
+            k_fold_cols<<<blocks_for(a->total_cols), 256, 0, s>>>(a->col_idx, a->total_cols, inv);
+            SBW_LAUNCHED("k_fold_cols");
+        }
+        SBW_CUDA(cudaFreeAsync(inv, s));
+        SBW_CUDA(cudaFreeAsync(flag, s));
+        SBW_CUDA(cudaStreamSynchronize(s));
+        if (h) return fail(SHFLBW_BAD_PARAMS, "fold: producer_rows is not a permutation of 0..cols-1");
+    }
+    a->reserved |= SHFLBW_FOLDED;
+    return SHFLBW_OK;
+}

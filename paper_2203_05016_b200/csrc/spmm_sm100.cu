@@ -41,6 +41,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <atomic>
 #include <mutex>
 
@@ -76,6 +77,7 @@ struct TcParams {
     int Nb, H, W, RS, S, stride, pad, Q, PQ;
     int ksplit;      // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
+    int per_sm;      // persistent: resident CTAs per SM
 };
 
 // Development timeline (scripts/trace.py): compiled in only with -DSBW_TRACE.
@@ -547,7 +549,7 @@ __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc,
 }
 
 template <int DT, int VS, int CS, int KIND>
-__global__ void __launch_bounds__(kThreadsPersist, 1)
+__global__ void __launch_bounds__(kThreadsPersist, 2)
     k_spmm_persist(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW, TcParams p,
                    int units, int n_tiles) {
     using WL = WeightLayout<VS>;
@@ -561,10 +563,13 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int stages = p.stages;
-    unsigned char* ctile = smem + stages * kStageBytes;                                 // [VS][128] out
-    int32_t* meta_s = reinterpret_cast<int32_t*>(ctile + VS * kBlockN * 4);            // [kMetaBlocks][64]
-    int32_t* rows_s = meta_s + kMetaBlocks * kBlockK;                                  // VS
-    uint64_t* full = reinterpret_cast<uint64_t*>(rows_s + (VS < 2 ? 2 : VS));
+    const int ngroups = (units + n_tiles - 1) / n_tiles;
+    const int out_esz = p.c_dtype == SHFLBW_F32 ? 4 : 2;
+    unsigned char* ctile = smem + stages * kStageBytes;  // [VS][128] out (staged stores only)
+    int32_t* meta_s = reinterpret_cast<int32_t*>(ctile + (p.bulk_out ? VS * kBlockN * out_esz : 0));  // [2][kMetaBlocks][64]
+    int32_t* rows_s = meta_s + 2 * kMetaBlocks * kBlockK;                              // VS
+    int32_t* gptr_s = rows_s + (VS < 4 ? 4 : VS);                                      // ngroups + 1
+    uint64_t* full = reinterpret_cast<uint64_t*>(gptr_s + ((ngroups + 2) & ~1));
     uint64_t* empty = full + stages;
     uint64_t* acc_full = empty + stages;  // [2]
     uint64_t* acc_empty = acc_full + 2;   // [2]
@@ -576,6 +581,10 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
     const int vbase = static_cast<int>(rank) * VS;
     const uint16_t cmask = static_cast<uint16_t>((1u << CS) - 1u);
 
+    if (threadIdx.x == 0) trace_event(p.trace, 0);
+    // this launch's group offsets (static: before the dependency wait), so no
+    // role stalls on a global load at a unit boundary
+    for (int x = threadIdx.x; x <= ngroups; x += blockDim.x) gptr_s[x] = p.group_ptr[p.g_begin + x];
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
@@ -595,16 +604,20 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (threadIdx.x == 0) grid_launch_dependents();
+    if (threadIdx.x == 0) {
+        grid_launch_dependents();
+        trace_event(p.trace, 1);
+    }
+    auto unit_nkb = [&](int u) { const int gl = u / n_tiles; return (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK; };
 
     if (warp == 0) {
         // ---------------- stage arming + weights ----------------
         if (lane == 0) {
             int kbg = 0;
             for (int u = cid; u < units; u += nclusters) {
-                const int g = p.g_begin + u / n_tiles;
-                const int gp = p.group_ptr[g];
-                const int nkb = (p.group_ptr[g + 1] - gp) / kBlockK;
+                const int gl = u / n_tiles;
+                const int gp = gptr_s[gl];
+                const int nkb = (gptr_s[gl + 1] - gp) / kBlockK;
                 for (int kb = 0; kb < nkb; ++kb, ++kbg) {
                     const int s = kbg % stages;
                     if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
@@ -624,11 +637,11 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
         if (lane == 0) {
             int kbg = 0, i = 0;
             for (int u = cid; u < units; u += nclusters, ++i) {
-                const int g = p.g_begin + u / n_tiles;
-                const int nkb = (p.group_ptr[g + 1] - p.group_ptr[g]) / kBlockK;
+                const int nkb = unit_nkb(u);
                 const int b = i & 1;
                 mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
+                if (i < 8) trace_event(p.trace, 8 + i);  // MMA: accumulator free for unit i
                 const uint32_t tmem_d = tmem_base + b * kAccCols;
                 for (int kb = 0; kb < nkb; ++kb, ++kbg) {
                     const int s = kbg % stages;
@@ -662,13 +675,36 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
         const int gi = gw * per_warp + lane;
         const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
         const bool t_issue = lane < per_warp && (!mcast || (gi % CS) == static_cast<int>(rank));
+        // column-index windows: meta_s[buf] holds kMetaBlocks K blocks of a
+        // unit; the first window of unit i+1 is prefetched (cp.async) into the
+        // other buffer while unit i issues its gathers
+        auto load_window = [&](int u, int kb0, int buf, bool async) {
+            const int gl = u / n_tiles;
+            const int nkb = (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK;
+            const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
+            const int32_t* src = p.col_idx + gptr_s[gl] + kb0 * kBlockK;
+            int32_t* dst = meta_s + buf * kMetaBlocks * kBlockK;
+            for (int x = et; x < nb * (kBlockK / 4); x += 128) {
+                if (async) cp_async16(smem_u32(dst + 4 * x), src + 4 * x, true);
+                else reinterpret_cast<int4*>(dst)[x] = reinterpret_cast<const int4*>(src)[x];
+            }
+        };
+        if (cid < units) load_window(cid, 0, 0, false);
+        asm volatile("bar.sync 2, 128;" ::: "memory");
         grid_dependency_wait();  // B may be the previous kernel's output
-        int kbg = 0;
-        for (int u = cid; u < units; u += nclusters) {
-            const int g = p.g_begin + u / n_tiles;
+        if (et == 0) trace_event(p.trace, 2);
+        int kbg = 0, i = 0;
+        for (int u = cid; u < units; u += nclusters, ++i) {
+            const int buf = i & 1;
+            if (et == 0 && i < 8) trace_event(p.trace, 16 + i);  // gathers: unit i starts issuing
+            const int un = u + nclusters;
+            if (un < units) {  // the other buffer was released by the bar.sync ending unit i-1
+                load_window(un, 0, buf ^ 1, true);
+                cp_async_commit();
+            }
             const int n0 = (u % n_tiles) * kBlockN;
-            const int gp = p.group_ptr[g];
-            const int nkb = (p.group_ptr[g + 1] - gp) / kBlockK;
+            const int nkb = unit_nkb(u);
+            const int32_t* mbuf = meta_s + buf * kMetaBlocks * kBlockK;
             int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
             bool g_pos_ok = true;
             if (KIND == 1) {
@@ -682,16 +718,14 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
             for (int kb = 0; kb < nkb; ++kb, ++kbg) {
                 const int s = kbg % stages;
                 const int win = kb % kMetaBlocks;
-                if (win == 0) {  // stage this unit's next window of column indices
+                if (win == 0 && kb > 0) {  // deep group: later windows of this unit, synchronously
                     asm volatile("bar.sync 2, 128;" ::: "memory");
-                    const int nb = nkb - kb < kMetaBlocks ? nkb - kb : kMetaBlocks;
-                    const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + kb * kBlockK);
-                    for (int x = et; x < nb * (kBlockK / 4); x += 128) reinterpret_cast<int4*>(meta_s)[x] = src[x];
+                    load_window(u, kb, buf, false);
                     asm volatile("bar.sync 2, 128;" ::: "memory");
                 }
                 if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
                 if (t_issue) {
-                    int4 ci = reinterpret_cast<const int4*>(meta_s + win * kBlockK)[g_rg];
+                    int4 ci = reinterpret_cast<const int4*>(mbuf + win * kBlockK)[g_rg];
                     if (KIND == 1) {
                         auto conv_row = [&](int c) -> int {
                             if (c < 0 || !g_pos_ok) return -1;
@@ -714,26 +748,31 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
                 }
                 __syncwarp();
             }
+            cp_async_wait<0>();
+            asm volatile("bar.sync 2, 128;" ::: "memory");  // next unit's window visible; this buffer free
         }
     } else {
         // ---------------- epilogue ----------------
         const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - 192;
+        auto row_of = [&](int u, int v) -> int32_t {
+            const int g = p.g_begin + u / n_tiles;
+            return p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
+                             : p.row_indices[static_cast<int64_t>(g) * p.V + vbase + v];
+        };
+        int32_t next_row = (cid < units && et < VS) ? row_of(cid, et) : 0;  // static: before the wait
         grid_dependency_wait();  // C may still be read by the previous kernel
         int i = 0;
         for (int u = cid; u < units; u += nclusters, ++i) {
-            const int g = p.g_begin + u / n_tiles;
             const int n0 = (u % n_tiles) * kBlockN;
-            const int nkb = (p.group_ptr[g + 1] - p.group_ptr[g]) / kBlockK;
+            const int nkb = unit_nkb(u);
             const int b = i & 1;
             asm volatile("bar.sync 3, 128;" ::: "memory");  // previous unit done with rows_s / ctile
-            for (int v = et; v < VS; v += 128) {
-                const int64_t gr = static_cast<int64_t>(g) * p.V + vbase + v;
-                rows_s[v] = p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
-                                      : p.row_indices[gr];
-            }
+            if (et < VS) rows_s[et] = next_row;
             asm volatile("bar.sync 3, 128;" ::: "memory");
+            if (u + nclusters < units && et < VS) next_row = row_of(u + nclusters, et);  // in flight meanwhile
             mbar_wait(&acc_full[b], (i >> 1) & 1);
             tc_fence_after();
+            if (et == 0 && i < 8) trace_event(p.trace, 24 + i);  // epilogue: unit i accumulated
             const uint32_t t_acc = tmem_base + b * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
             if (p.c_dtype == SHFLBW_F32)
                 persist_store<float, VS>(p, t_acc, nkb, m, q, lane, n0, rows_s, ctile, &acc_empty[b]);
@@ -747,6 +786,7 @@ __global__ void __launch_bounds__(kThreadsPersist, 1)
     if (CS > 1) cluster_sync_relaxed();
     else __syncthreads();
     if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+    if (threadIdx.x == 0) trace_event(p.trace, 7);
 }
 
 // ---------------- host side ----------------
@@ -878,16 +918,23 @@ template <int DT, int VS, int CS, int KIND>
 int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
                    cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
-    const size_t smem = static_cast<size_t>(prm.stages) * kStage + static_cast<size_t>(VS) * kBlockN * 4 + 1024 +
-                        kMetaBlocks * kBlockK * 4 + (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 5) * 8 + 16;
+    const size_t out_esz = prm.c_dtype == SHFLBW_F32 ? 4 : 2;
+    const size_t smem = static_cast<size_t>(prm.stages) * kStage +
+                        (prm.bulk_out ? static_cast<size_t>(VS) * kBlockN * out_esz : 0) + 1024 +
+                        2 * kMetaBlocks * kBlockK * 4 + (VS < 4 ? 4 : VS) * 4 + ((groups + 2) & ~1) * 4 +
+                        (2 * prm.stages + 5) * 8 + 16;
     auto kern = k_spmm_persist<DT, VS, CS, KIND>;
     static std::atomic<size_t> configured{0};
     if (smem > configured.load(std::memory_order_relaxed)) {
         SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         configured.store(smem, std::memory_order_relaxed);
     }
     const int units = n_tiles * groups;
-    const int clusters = std::min(units, num_sms() / CS);
+    const int per_sm = prm.per_sm;
+    // per_sm CTAs must be co-resident: launch bounds (320, 2) keep registers
+    // <= 102 and the host sizes stages so per_sm CTAs fit in shared memory
+    const int clusters = std::min(units, per_sm * num_sms() / CS);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * CS, 1, 1);
     cfg.blockDim = dim3(kThreadsPersist, 1, 1);
@@ -1046,7 +1093,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.ksplit = hybrid ? 2 : ((cs > 1 && !vsplit) ? 1 : 0);
     prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
     if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
-    prm.trace = reinterpret_cast<unsigned long long*>(option("trace"));
+    prm.trace = option("trace") > 1 ? reinterpret_cast<unsigned long long*>(option("trace")) : nullptr;
     {
         const int esz = c.dtype == SHFLBW_F32 ? 4 : 2;
         const bool aligned = (reinterpret_cast<uintptr_t>(c.ptr) % 16 == 0) && ((c.ldc * esz) % 16 == 0) &&
@@ -1056,13 +1103,38 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     // persistent when one wave of CTAs cannot cover the units (option
     // "persistent": -1 never, 1 always, 0 auto)
     {
-        const int64_t opt = option("persistent");
-        prm.persistent = !prm.ksplit && opt > 0 ? 1 : 0;  // opt-in: slower than 2 CTAs/SM so far
+        // "persistent": N > 0 -> persistent kernel with N CTAs per SM, -1 never,
+        // 0 auto: 2 per SM once the grid holds >= 2 full waves of units (the
+        // per-CTA prologue/epilogue then no longer hides behind the co-resident
+        // CTA; measured)
+        int64_t opt = option("persistent");
+        if (opt == 0) opt = (units * cs >= 4LL * num_sms()) ? 2 : -1;
+        prm.persistent = !prm.ksplit && opt > 0 && groups <= 4096 ? 1 : 0;
+        prm.per_sm = static_cast<int>(std::min<int64_t>(2, std::max<int64_t>(1, opt)));  // launch bounds: 2
     }
     int stages = static_cast<int>(option("stages"));
-    if (stages <= 0) stages = prm.persistent ? (vs >= 128 ? 4 : 6) : (vs >= 128 ? 3 : 4);
-    const int max_kb = (kb_grp + ksf - 1) / ksf;                                        // K blocks per CTA
-    if (stages > max_kb) stages = max_kb < 2 ? 2 : max_kb;
+    if (prm.persistent) {
+        // "persistent" = N resident CTAs per SM (1..4).  Gather throughput per
+        // SM grows with the number of issuing CTAs; each gets
+        // as many stages as its share of shared memory holds (>= 2), with the
+        // staged output tile dropped when it would cost a stage.
+        const int64_t budget = 232448 / prm.per_sm - 1024;
+        const int64_t tile = static_cast<int64_t>(vs) * kBlockN * (c.dtype == SHFLBW_F32 ? 4 : 2);
+        const int64_t fixed = 1024 + 2 * kMetaBlocks * kBlockK * 4 + 4 * 128 + 4 * (groups + 2) + 512;
+        const int64_t stage = kABytes + static_cast<int64_t>(kBlockK) * vs * 2;
+        const int64_t with_tile = (budget - fixed - tile) / stage, without = (budget - fixed) / stage;
+        if (prm.bulk_out && with_tile < 2) prm.bulk_out = 0;  // the staged epilogue is worth a stage
+        const int64_t fit = prm.bulk_out ? with_tile : without;
+        if (fit < 2) prm.persistent = 0;
+        else if (stages <= 0 || stages > fit) stages = static_cast<int>(std::min<int64_t>(12, fit));
+    }
+    if (stages <= 0 && prm.persistent) {
+        stages = 2;
+    } else if (stages <= 0) {
+        stages = vs >= 128 ? 3 : 4;
+    }
+    const int max_kb = (kb_grp + ksf - 1) / ksf;  // K blocks per CTA
+    if (!prm.persistent && stages > max_kb) stages = max_kb < 2 ? 2 : max_kb;  // the ring spans units otherwise
     prm.stages = stages;
 
     CUtensorMap tmB, tmW;

@@ -165,11 +165,12 @@ class ShflBWMatrix:
         return ri[:M], gn[:G], cols[:nnzc], vals[: nnzc * V]
 
     def raw(self):
-        """-> (group_ptr i32[G+1], col_idx i32[total], values u16[total*V]): the device layout."""
+        """-> (group_ptr i32[G+1], col_idx i32[total], values u16[total*V] (u32 bit patterns for F32
+        matrices)): the device layout."""
         G, V, T = self.group_count(), self.v, self.total_cols
         gp = np.zeros(G + 1, np.int32)
         ci = np.zeros(max(T, 1), np.int32)
-        vv = np.zeros(max(T * V, 1), np.uint16)
+        vv = np.zeros(max(T * V, 1), np.uint32 if self.dtype == torch.float32 else np.uint16)
         _check(_lib().shflbw_cu_matrix_export_raw(self.ptr, gp.ctypes.data, ci.ctypes.data, vv.ctypes.data,
                                                   _stream()))
         return gp, ci[:T], vv[: T * V]
@@ -251,19 +252,49 @@ def _check_b(a: ShflBWMatrix, b: torch.Tensor) -> torch.Tensor:
 
 
 def spmm_execute(a: ShflBWMatrix, b: torch.Tensor, cfg: TileConfig | None = None, threads: int = 1,
-                 out_dtype: torch.dtype = torch.float32, out: torch.Tensor | None = None) -> torch.Tensor:
-    """C = decompress(a) @ b with the permuted write-back (src/spmm.cpp:76-146)."""
+                 out_dtype: torch.dtype = torch.float32, out: torch.Tensor | None = None,
+                 permuted_output: bool = False) -> torch.Tensor:
+    """C = decompress(a) @ b with the permuted write-back (src/spmm.cpp:76-146).
+
+    permuted_output=True skips the write-back permutation: row i of the
+    result is logical row a.row_indices[i] (group order), the input a layer
+    folded with fold_input_permutation(next, a) consumes directly."""
     if cfg is not None:  # the default TileConfig is valid by construction
         cfg.validate()
     b = _check_b(a, b)
     N = b.shape[1]
     if out is None:
         out = torch.zeros((a.rows, N), dtype=out_dtype, device=b.device)
-    st = _lib().shflbw_cu_spmm(a.ptr, b.data_ptr(), b.shape[0], N, b.stride(0), out.data_ptr(),
-                               _DT[out.dtype], out.stride(0), torch.cuda.current_stream().cuda_stream)
+    if permuted_output:
+        st = _lib().shflbw_cu_spmm_groups(a.ptr, 0, a.group_count(), b.data_ptr(), b.shape[0], N, b.stride(0),
+                                          out.data_ptr(), _DT[out.dtype], out.stride(0), 1,
+                                          torch.cuda.current_stream().cuda_stream)
+    else:
+        st = _lib().shflbw_cu_spmm(a.ptr, b.data_ptr(), b.shape[0], N, b.stride(0), out.data_ptr(),
+                                   _DT[out.dtype], out.stride(0), torch.cuda.current_stream().cuda_stream)
     if st:
         _check(st)
     return out
+
+
+def fold_input_permutation(a: ShflBWMatrix, producer) -> ShflBWMatrix:
+    """Remap a's column indices so it consumes the group-ordered output of
+    `producer` (a ShflBWMatrix run with permuted_output=True, or a device
+    int32 tensor of its row_indices).  In place; results stay bit-identical
+    to the unpermuted chain."""
+    if isinstance(producer, ShflBWMatrix):
+        if producer.rows != a.cols:
+            raise ShapeMismatch(f"producer rows {producer.rows} != consumer cols {a.cols}")
+        rows_ptr = producer._m.row_indices
+    else:
+        if not (isinstance(producer, torch.Tensor) and producer.is_cuda and producer.dtype == torch.int32
+                and producer.dim() == 1 and producer.is_contiguous()):
+            raise BadParams("producer must be a ShflBWMatrix or a contiguous CUDA int32 vector")
+        if producer.numel() != a.cols:
+            raise ShapeMismatch(f"producer rows {producer.numel()} != consumer cols {a.cols}")
+        rows_ptr = producer.data_ptr()
+    _check(_lib().shflbw_cu_fold_input_permutation(a.ptr, rows_ptr, _stream()))
+    return a
 
 
 def spmm_groups(a: ShflBWMatrix, g_begin: int, g_end: int, b: torch.Tensor, out: torch.Tensor,

@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT
 SBW_TRACE=1 python -m paper_2203_05016_b200.build --force > gpurun_out/tr_build.log 2>&1 || { tail gpurun_out/tr_build.log; exit 1; }
-for cfg in "--K 2048 --opts split=0" "--K 2048 --opts split=4,split_mode=2" "--K 256 --opts split=0" "--K 256 --opts split=1" "--K 256 --opts split=4,split_mode=2" "--K 8192 --opts split=0"; do
-  timeout -k 10 120 python scripts/trace.py --chain 8 $cfg 2>&1 | tail -30
-done > gpurun_out/trace.log
-cat gpurun_out/trace.log
+for cfg in "--workload ffn --opts persistent=1 --persist" "--workload ffn --opts persistent=-1" "--workload lf --opts persistent=1 --persist"; do
+  timeout -k 10 200 python scripts/trace.py $cfg 2>&1 | tail -40
+done > gpurun_out/ptrace.log
+cat gpurun_out/ptrace.log

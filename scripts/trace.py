@@ -19,6 +19,7 @@ ap.add_argument("--opts", default="")
 ap.add_argument("--K", type=int, default=0)
 ap.add_argument("--chain", type=int, default=0, help="launch this many SpMMs back to back on rotating "
                 "operand sets (warm, PDL-overlapped) and trace the last one")
+ap.add_argument("--persist", action="store_true", help="print the persistent kernel's per-unit events")
 args = ap.parse_args()
 wl = dict(bench.WORKLOADS[args.workload])
 if args.K:
@@ -64,3 +65,14 @@ for e, nm in enumerate(names):
     col = col[t[:, e] > 0]
     if len(col):
         print(f"  {nm:10s} min {col.min():7.2f}  p50 {np.median(col):7.2f}  max {col.max():7.2f} us")
+
+if args.persist:
+    dep = rel[:, 2]
+    print("  per unit i (median over CTAs, us after the CTA's dependency wait): gathers start / MMA start / "
+          "accumulated")
+    for i in range(8):
+        cols = [rel[:, 16 + i] - dep, rel[:, 8 + i] - dep, rel[:, 24 + i] - dep]
+        ok = t[:, 24 + i] > 0
+        if ok.sum() == 0:
+            break
+        print(f"  unit {i}: " + "  ".join(f"{np.median(c[ok]):7.2f}" for c in cols))

@@ -29,7 +29,7 @@ def sb():
         pytest.skip("no CUDA device")
     import paper_2203_05016_b200 as sb
     for k, v in (("force_simt", 0), ("split", 0), ("stages", 0), ("split_mode", 0), ("cp_async_slabs", 0),
-                 ("persistent", 0)):
+                 ("persistent", 0), ("no_bulk_out", 0)):
         sb.set_option(k, v)
     return sb
 
@@ -499,14 +499,20 @@ def test_persistent_kernel_bitwise(sb, oracle, M, N, K, V, alpha, split):
     Bd = dev(B, torch.bfloat16)
     sb.set_option("split", split)
     outs = {}
-    for mode in (-1, 1):
+    for mode in (-1, 1, 2, 0):  # one CTA per unit, persistent x1 / x2 per SM, auto
         sb.set_option("persistent", mode)
         outs[mode] = (sb.spmm_execute(a, Bd).cpu().numpy(),
                       sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
+    sb.set_option("persistent", 2)  # per-element epilogue stores
+    sb.set_option("no_bulk_out", 1)
+    outs["nb"] = (sb.spmm_execute(a, Bd).cpu().numpy(),
+                  sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
+    sb.set_option("no_bulk_out", 0)
     sb.set_option("persistent", 0)
     sb.set_option("split", 0)
     assert oracle.rel_frobenius(outs[1][0], oracle.spmm(p, B)) <= TOL
-    assert np.array_equal(outs[1][0], outs[-1][0]) and np.array_equal(outs[1][1], outs[-1][1])
+    for mode in (1, 2, 0, "nb"):
+        assert np.array_equal(outs[mode][0], outs[-1][0]) and np.array_equal(outs[mode][1], outs[-1][1]), mode
 
 
 def test_persistent_conv(sb, oracle):
@@ -517,10 +523,79 @@ def test_persistent_conv(sb, oracle):
     x = oracle.round16(oracle.fill_uniform(oracle.rng(9), C * H * H * Nb).reshape(C, H, H, Nb))
     a, p = compress_both(sb, oracle, W, mask, V)
     xd = dev(x, torch.bfloat16)
-    sb.set_option("persistent", 1)
-    got = sb.conv2d(a, xd, sb.ConvGeometry(3, 3, 1, 1)).cpu().numpy()
-    sb.set_option("persistent", -1)
-    ref = sb.conv2d(a, xd, sb.ConvGeometry(3, 3, 1, 1)).cpu().numpy()
+    got = {}
+    for mode in (1, 2, -1):
+        sb.set_option("persistent", mode)
+        got[mode] = sb.conv2d(a, xd, sb.ConvGeometry(3, 3, 1, 1)).cpu().numpy()
     sb.set_option("persistent", 0)
-    assert np.array_equal(got, ref)
+    ref = got[-1]
+    assert np.array_equal(got[1], ref) and np.array_equal(got[2], ref)
+    got = got[1]
     assert oracle.rel_frobenius(got, oracle.conv2d(p, x, 3, 3, 1, 1)) <= TOL
+
+
+# ------------------------------------------------- permutation folding (§8 f2)
+
+@pytest.mark.parametrize("dtype,V1,V2", [(torch.bfloat16, 64, 32), (torch.float32, 8, 16), (torch.float16, 128, 64)])
+def test_fold_input_permutation_chain_bitwise(sb, oracle, dtype, V1, V2):
+    """Two chained layers: layer 1 writes group-ordered rows (no write-back
+    permutation), layer 2 has row_indices_1 folded into its column indices.
+    The final output is bit-identical to the unfolded chain (same gathered
+    values, same accumulation order), and on the exact fp32 path equal to the
+    oracle chain."""
+    M1, K1, M2, N = 1024, 768, 512, 192
+    mask1 = oracle.random_shflbw_mask(M1, K1, V1, K1 // 4, oracle.rng(31))
+    mask2 = oracle.random_shflbw_mask(M2, M1, V2, M1 // 4, oracle.rng(32))
+    W1 = oracle.round16(oracle.random_dense(M1, K1, 33))
+    W2 = oracle.round16(oracle.random_dense(M2, M1, 34))
+    B = oracle.round16(oracle.random_dense(K1, N, 35))
+    a1 = sb.compress_shflbw(dev(W1), dev(mask1), V1, dtype=dtype)
+    a2 = sb.compress_shflbw(dev(W2), dev(mask2), V2, dtype=dtype)
+    a2f = sb.compress_shflbw(dev(W2), dev(mask2), V2, dtype=dtype)
+    Bd = dev(B, dtype)
+    odt = torch.float32 if dtype == torch.float32 else dtype
+    # unfolded: scatter write-back, then layer 2
+    c1 = sb.spmm_execute(a1, Bd, out_dtype=odt)
+    want = sb.spmm_execute(a2, c1).cpu().numpy()
+    # folded: group-ordered layer-1 rows feed the folded layer 2
+    c1p = sb.spmm_execute(a1, Bd, out_dtype=odt, permuted_output=True)
+    ri1 = a1.to_host()[0].astype(np.int64)
+    assert torch.equal(c1p, c1[torch.from_numpy(ri1).cuda()])
+    sb.fold_input_permutation(a2f, a1)
+    got = sb.spmm_execute(a2f, c1p).cpu().numpy()
+    assert np.array_equal(got, want)
+    if dtype == torch.float32:
+        p1, p2 = oracle.compress(W1, mask1, V1), oracle.compress(W2, mask2, V2)
+        assert np.array_equal(got, oracle.spmm(p2, oracle.spmm(p1, B)))
+    # the folded device layout is exactly inv[cols] of the unfolded one
+    gp, ci, _ = a2.raw()
+    _, cif, _ = a2f.raw()
+    inv = np.empty(M1, np.int64)
+    inv[ri1] = np.arange(M1)
+    assert np.array_equal(cif, np.where(ci >= 0, inv[np.maximum(ci, 0)], -1))
+
+
+def test_fold_input_permutation_errors(sb, oracle):
+    mask = oracle.random_shflbw_mask(128, 256, 32, 64, oracle.rng(3))
+    W = oracle.round16(oracle.random_dense(128, 256, 4))
+    a = sb.compress_shflbw(dev(W).to(torch.bfloat16), dev(mask), 32)
+    before = a.raw()[1].copy()
+    bad = torch.arange(256, dtype=torch.int32, device="cuda")
+    bad[7] = 3  # duplicate
+    with pytest.raises(sb.BadParams):
+        sb.fold_input_permutation(a, bad)
+    bad[7] = 256  # out of range
+    with pytest.raises(sb.BadParams):
+        sb.fold_input_permutation(a, bad)
+    with pytest.raises(sb.ShapeMismatch):
+        sb.fold_input_permutation(a, torch.arange(255, dtype=torch.int32, device="cuda"))
+    assert np.array_equal(a.raw()[1], before)  # unchanged on error
+    perm = torch.randperm(256, generator=torch.Generator().manual_seed(0)).to(torch.int32).cuda()
+    sb.fold_input_permutation(a, perm)
+    with pytest.raises(sb.BadParams):  # twice
+        sb.fold_input_permutation(a, perm)
+    with pytest.raises(sb.BadParams):  # reference-layout download of a folded matrix
+        a.to_host()
+    x = torch.zeros((16, 4, 4, 32), dtype=torch.bfloat16, device="cuda")  # 16*4*4... C*R*S = 256 = 16*4*4
+    with pytest.raises(sb.BadParams):
+        sb.conv2d(a, x, sb.ConvGeometry(4, 4, 1, 0))
