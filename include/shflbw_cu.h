@@ -77,6 +77,10 @@ typedef struct shflbw_cu_matrix {
 /* shflbw_cu_matrix.reserved bit: col_idx were remapped by
  * shflbw_cu_fold_input_permutation (SpMM input in the producer's group order) */
 #define SHFLBW_FOLDED 1
+/* shflbw_cu_matrix.reserved bit: columns in conv order (shflbw_cu_conv_prepare);
+ * bits 8..15 hold the filter width S it was prepared for */
+#define SHFLBW_CONV_ORDER 2
+#define SHFLBW_CONV_ORDER_S(reserved) (((reserved) >> 8) & 0xff)
 
 /* ---- library ---------------------------------------------------------- */
 const char* shflbw_cu_last_error(void);
@@ -174,6 +178,19 @@ int shflbw_cu_spmm_groups(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_
                           const void* B, int32_t K_b, int32_t N, int64_t ldb, void* C,
                           int32_t c_dtype, int64_t ldc, int32_t compact,
                           shflbw_stream_t stream);
+
+/* Conv weight layout (cf. a library's one-time filter reorder): *out = a copy
+ * of w whose columns are, per group, ordered by filter column s = c % S
+ * (ascending c within each s) with every s-run padded to a multiple of 4 by
+ * pad columns (index SHFLBW_PAD_COLUMN, zero values).  shflbw_cu_conv2d then
+ * fetches each activation row as 64/Nb adjacent output positions x Nb
+ * (128 bytes) instead of one position (Nb*2 bytes) when stride = 1,
+ * Nb in {16, 32} and 64/Nb divides Q.  Same values, so conv2d (and spmm) stay
+ * within the 1e-5 tolerance; only the fp32 summation order changes.
+ * matrix_download rejects the result (its columns are not ascending).
+ * S in 1..32.  Synchronises `stream`. */
+int shflbw_cu_conv_prepare(const shflbw_cu_matrix* w, int32_t S, shflbw_cu_matrix* out,
+                           shflbw_stream_t stream);
 
 /* Permutation folding (the paper's layout fusion,
  * PAPER.md:181-183).  A layer whose SpMM wrote group-ordered rows

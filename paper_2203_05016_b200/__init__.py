@@ -7,11 +7,12 @@ package is a thin host mirror of the reference interface over that ABI
 (``shflbw``) plus the multi-GPU row-group sharding (``sharded``).
 """
 from .shflbw import (BadGeometry, BadParams, ConvGeometry, Error, NonConformantMask, ShapeMismatch,
-                     ShflBWMatrix, TileConfig, compress_shflbw, conv2d, conv_output_size, decompress,
-                     fold_input_permutation, launch_count, set_option, spmm_execute, spmm_groups,
+                     ShflBWMatrix, TileConfig, compress_shflbw, conv2d, conv_output_size, conv_prepare,
+                     decompress, fold_input_permutation, launch_count, set_option, spmm_execute, spmm_groups,
                      unpermute_rows, upload, validate_pattern)
 
 __all__ = ["BadGeometry", "BadParams", "ConvGeometry", "Error", "NonConformantMask", "ShapeMismatch",
-           "ShflBWMatrix", "TileConfig", "compress_shflbw", "conv2d", "conv_output_size", "decompress",
+           "ShflBWMatrix", "TileConfig", "compress_shflbw", "conv2d", "conv_output_size", "conv_prepare",
+           "decompress",
            "fold_input_permutation", "launch_count", "set_option", "spmm_execute", "spmm_groups",
            "unpermute_rows", "upload", "validate_pattern"]

@@ -53,6 +53,7 @@ SIGNATURES = {
     "shflbw_cu_spmm_groups": (C.c_int, [C.POINTER(CuMatrix), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                         C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                         C.c_void_p]),
+    "shflbw_cu_conv_prepare": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "shflbw_cu_fold_input_permutation": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "shflbw_cu_unpermute_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
                                            C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),

@@ -148,6 +148,8 @@ int shflbw_cu_matrix_download(const shflbw_cu_matrix* m, uint32_t* row_indices, 
                               uint32_t* cols, float* values, shflbw_stream_t stream) {
     if (int st = check_matrix(m)) return st;
     if (m->reserved & SHFLBW_FOLDED) return fail(SHFLBW_BAD_PARAMS, "matrix has a folded input permutation");
+    if (m->reserved & SHFLBW_CONV_ORDER)
+        return fail(SHFLBW_BAD_PARAMS, "matrix is in conv order (shflbw_cu_conv_prepare); download the original");
     return download_impl(m, row_indices, group_ncols, cols, values, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -228,7 +230,11 @@ int shflbw_cu_conv2d(const shflbw_cu_matrix* w, const void* input, int32_t C, in
                                 0, s);
     }
     Operand b;
-    b.kind = 1;
+    // 128-byte activation rows when the weight is in conv order for this S
+    const int ppb = Nb > 0 ? 64 / Nb : 0;  // output positions per 64-element row
+    const bool wide = (w->reserved & SHFLBW_CONV_ORDER) && SHFLBW_CONV_ORDER_S(w->reserved) == S && stride == 1 &&
+                      (Nb == 16 || Nb == 32) && Q % ppb == 0 && (static_cast<int64_t>(C) * H < (1LL << 31));
+    b.kind = wide ? 2 : 1;
     b.ptr = input;
     b.K = w->cols;
     b.N = static_cast<int>(flat);
@@ -248,6 +254,13 @@ int shflbw_cu_conv2d(const shflbw_cu_matrix* w, const void* input, int32_t C, in
     c.ldc = flat;
     c.compact = 0;
     return run_spmm(w, 0, w->groups, b, c, s);
+}
+
+int shflbw_cu_conv_prepare(const shflbw_cu_matrix* w, int32_t S, shflbw_cu_matrix* out, shflbw_stream_t stream) {
+    if (int st = check_matrix(w)) return st;
+    if (!out) return fail(SHFLBW_BAD_PARAMS, "conv_prepare: out is null");
+    if (S < 1 || w->cols % S != 0) return fail(SHFLBW_BAD_GEOMETRY, "conv_prepare: S must divide the weight columns");
+    return conv_prepare_impl(w, S, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int shflbw_cu_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n,

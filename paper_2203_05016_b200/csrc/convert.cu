@@ -31,6 +31,7 @@
 // smallest row as fail_row.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -452,14 +453,79 @@ __global__ void k_decompress(const int32_t* __restrict__ row_indices, const int3
                              const int32_t* __restrict__ group_ncols, const int32_t* __restrict__ col_idx,
                              const void* __restrict__ values, int V, int K, float* __restrict__ dense) {
     const int g = blockIdx.y;
-    const int gp = group_ptr[g], ng = group_ncols[g];
+    const int gp = group_ptr[g], width = group_ptr[g + 1] - gp;  // pads (-1) may sit anywhere (conv order)
     const auto* src = static_cast<const typename Elem<DT>::T*>(values);
-    const int64_t total = static_cast<int64_t>(ng) * V;
+    const int64_t total = static_cast<int64_t>(width) * V;
+    (void)group_ncols;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int j = static_cast<int>(idx / V), v = static_cast<int>(idx % V);
+        const int c = col_idx[gp + j];
+        if (c < 0) continue;
         const int64_t row = row_indices[static_cast<int64_t>(g) * V + v];
-        dense[row * K + col_idx[gp + j]] = Elem<DT>::to_f(src[(static_cast<int64_t>(gp) + j) * V + v]);
+        dense[row * K + c] = Elem<DT>::to_f(src[(static_cast<int64_t>(gp) + j) * V + v]);
+    }
+}
+
+// conv_prepare: per group, count the columns of each filter column s = c % S
+// (c = (ch*R + r)*S + s) and size the group for s-runs padded to quads
+__global__ void k_conv_widths(const int32_t* __restrict__ group_ptr, const int32_t* __restrict__ col_idx, int S,
+                              int* __restrict__ widths) {
+    __shared__ int cnt[32];
+    const int g = blockIdx.x;
+    if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    for (int j = group_ptr[g] + threadIdx.x; j < group_ptr[g + 1]; j += blockDim.x) {
+        const int c = col_idx[j];
+        if (c >= 0) atomicAdd(&cnt[c % S], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int w = 0;
+        for (int x = 0; x < S; ++x) w += (cnt[x] + 3) / 4 * 4;
+        widths[g] = (w + SHFLBW_K_TILE - 1) / SHFLBW_K_TILE * SHFLBW_K_TILE;
+    }
+}
+
+// one block per group: thread 0 assigns every column its slot (s-runs in
+// ascending s, ascending c within a run -- a stable partition), then the
+// block copies the V values of each column
+template <int DT>
+__global__ void k_conv_scatter(const int32_t* __restrict__ gp_in, const int32_t* __restrict__ col_in,
+                               const void* __restrict__ val_in, const int32_t* __restrict__ gp_out, int S, int V,
+                               int32_t* __restrict__ col_out, void* __restrict__ val_out, int32_t* __restrict__ slot) {
+    __shared__ int start[33];
+    const int g = blockIdx.x;
+    const int b0 = gp_in[g], b1 = gp_in[g + 1], o0 = gp_out[g];
+    if (threadIdx.x == 0) {
+        int cnt[32];
+        for (int x = 0; x < S; ++x) cnt[x] = 0;
+        for (int j = b0; j < b1; ++j)
+            if (col_in[j] >= 0) ++cnt[col_in[j] % S];
+        start[0] = 0;
+        for (int x = 0; x < S; ++x) start[x + 1] = start[x] + (cnt[x] + 3) / 4 * 4;
+        for (int x = 0; x < S; ++x) cnt[x] = 0;
+        for (int j = b0; j < b1; ++j) {
+            const int c = col_in[j];
+            if (c < 0) {
+                slot[j] = -1;
+                continue;
+            }
+            const int x = c % S;
+            const int p = o0 + start[x] + cnt[x]++;
+            slot[j] = p;
+            col_out[p] = c;
+        }
+    }
+    __syncthreads();
+    using T = typename Elem<DT>::T;
+    const T* src = static_cast<const T*>(val_in);
+    T* dst = static_cast<T*>(val_out);
+    const int64_t total = static_cast<int64_t>(b1 - b0) * V;
+    for (int64_t idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int j = b0 + static_cast<int>(idx / V), v = static_cast<int>(idx % V);
+        const int p = slot[j];
+        if (p >= 0) dst[static_cast<int64_t>(p) * V + v] = src[static_cast<int64_t>(j) * V + v];
     }
 }
 
@@ -866,10 +932,56 @@ int download_impl(const shflbw_cu_matrix* m, uint32_t* row_indices, uint32_t* gr
     return SHFLBW_OK;
 }
 
+int conv_prepare_impl(const shflbw_cu_matrix* w, int S, shflbw_cu_matrix* out, cudaStream_t s) {
+    if (S < 1 || S > 32) return fail(SHFLBW_UNSUPPORTED, "conv_prepare: filter width S must be 1..32");
+    const int M = w->rows, K = w->cols, V = w->v, G = w->groups;
+    if (int st = alloc_meta(out, M, K, V, w->dtype)) return st;
+    auto cleanup = [&](int st) {
+        if (st) free_matrix(out);
+        return st;
+    };
+    DevBuf widths, slot;
+    SBW_CUDA(widths.alloc(sizeof(int) * (G + 1), s));
+    SBW_CUDA(slot.alloc(sizeof(int32_t) * std::max<int64_t>(w->total_cols, 1), s));
+    SBW_CUDA(cudaMemcpyAsync(out->row_indices, w->row_indices, sizeof(int32_t) * M, cudaMemcpyDeviceToDevice, s));
+    SBW_CUDA(cudaMemcpyAsync(out->group_ncols, w->group_ncols, sizeof(int32_t) * G, cudaMemcpyDeviceToDevice, s));
+    int st;
+    if (G > 0) {
+        k_conv_widths<<<G, 256, 0, s>>>(w->group_ptr, w->col_idx, S, widths.as<int>());
+        SBW_LAUNCHED("k_conv_widths");
+    }
+    if ((st = scan_exclusive(widths.as<int>(), out->group_ptr, G, out->group_ptr + G, s))) return cleanup(st);
+    if (G > 0) {
+        k_max<<<1, 256, 0, s>>>(widths.as<int>(), G, widths.as<int>() + G);
+        SBW_LAUNCHED("k_max");
+    } else {
+        SBW_CUDA(cudaMemsetAsync(widths.as<int>(), 0, sizeof(int), s));
+    }
+    int total = 0, widest = 0;
+    SBW_CUDA(cudaMemcpyAsync(&total, out->group_ptr + G, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaMemcpyAsync(&widest, widths.as<int>() + G, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaStreamSynchronize(s));
+    out->max_group_cols = widest;
+    if ((st = alloc_data(out, total))) return cleanup(st);
+    if (total > 0) {
+        SBW_CUDA(cudaMemsetAsync(out->col_idx, 0xff, sizeof(int32_t) * static_cast<size_t>(total), s));
+        SBW_CUDA(cudaMemsetAsync(out->values, 0, static_cast<size_t>(total) * V * dtype_bytes(w->dtype), s));
+        by_dtype(w->dtype, [&]<int DT>() {
+            k_conv_scatter<DT><<<G, 256, 0, s>>>(w->group_ptr, w->col_idx, w->values, out->group_ptr, S, V,
+                                                 out->col_idx, out->values, slot.as<int32_t>());
+        });
+        SBW_LAUNCHED("k_conv_scatter");
+    }
+    out->reserved = (w->reserved & ~(SHFLBW_CONV_ORDER | (0xff << 8))) | SHFLBW_CONV_ORDER | (S << 8);
+    SBW_CUDA(cudaStreamSynchronize(s));
+    return SHFLBW_OK;
+}
+
 int decompress_impl(const shflbw_cu_matrix* m, float* dense, cudaStream_t s) {
     SBW_CUDA(cudaMemsetAsync(dense, 0, sizeof(float) * static_cast<size_t>(m->rows) * m->cols, s));
     if (m->groups == 0) return SHFLBW_OK;
-    dim3 grid(grid_for(static_cast<int64_t>(m->cols + 1) * m->v, 1024), m->groups);
+    const int64_t widest = m->max_group_cols > 0 ? m->max_group_cols : static_cast<int64_t>(m->cols) + SHFLBW_K_TILE;
+    dim3 grid(grid_for(std::max<int64_t>(widest, m->cols + 1) * m->v, 1024), m->groups);
     by_dtype(m->dtype, [&]<int DT>() {
         k_decompress<DT><<<grid, 256, 0, s>>>(m->row_indices, m->group_ptr, m->group_ncols, m->col_idx, m->values,
                                               m->v, m->cols, dense);

@@ -20,6 +20,7 @@ int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t
 int download_impl(const shflbw_cu_matrix* m, uint32_t* row_indices, uint32_t* group_ncols,
                   uint32_t* cols, float* values, cudaStream_t s);
 int decompress_impl(const shflbw_cu_matrix* m, float* dense, cudaStream_t s);
+int conv_prepare_impl(const shflbw_cu_matrix* w, int S, shflbw_cu_matrix* out, cudaStream_t s);
 int convert_impl(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s);
 int scan_exclusive(const int* in, int* out, int n, int* total_dev, cudaStream_t s);
 void free_matrix(shflbw_cu_matrix* m);
@@ -28,6 +29,10 @@ void free_matrix(shflbw_cu_matrix* m);
 //   kind 0 (SpMM): row c of B, element n at B[c * ldb + n]
 //   kind 1 (conv): implicit im2col of a [C][H][W][Nb] tensor; sparse column
 //                  c = (ch, r, s), flat output column n = (p*Q + q)*Nb + nb
+//   kind 2 (conv, 128-byte rows): as kind 1 for a matrix in conv order
+//                  (shflbw_cu_conv_prepare), stride 1, Nb in {16, 32} and
+//                  64/Nb | Q: each activation row fetched is 64/Nb adjacent
+//                  output positions x Nb from the [C*H][W*Nb] view
 struct Operand {
     int kind = 0;
     const void* ptr = nullptr;

@@ -38,7 +38,11 @@ __global__ void __launch_bounds__(kThreads) k_spmm_simt(
     const int g = g_begin + blockIdx.y;
     const int n = blockIdx.x * kThreads + threadIdx.x;
     const bool live = n < b.N;
-    const int gp = group_ptr[g], ng = group_ncols[g];
+    // the padded width: pad columns (-1) are skipped wherever they sit (at the
+    // end in the reference order, inside the group in conv order), so the sum
+    // keeps the layout's column order exactly
+    const int gp = group_ptr[g], ng = group_ptr[g + 1] - gp;
+    (void)group_ncols;
     const T* vals = static_cast<const T*>(values) + static_cast<int64_t>(gp) * V;
     const T* B = static_cast<const T*>(b.ptr);
 
@@ -67,7 +71,9 @@ __global__ void __launch_bounds__(kThreads) k_spmm_simt(
             }
             for (int jj = threadIdx.x; jj < nj; jj += kThreads) {
                 const int col = col_idx[gp + j0 + jj];
-                if (KIND == 0) {
+                if (col < 0) {
+                    base_s[jj] = -1;
+                } else if (KIND == 0) {
                     base_s[jj] = static_cast<int64_t>(col) * b.ldb;
                 } else {
                     const int rs = b.R * b.S;
@@ -80,6 +86,7 @@ __global__ void __launch_bounds__(kThreads) k_spmm_simt(
             __syncthreads();
             if (live) {
                 for (int jj = 0; jj < nj; ++jj) {
+                    if (base_s[jj] < 0) continue;  // pad column
                     float x;
                     if (KIND == 0) {
                         x = Elem<DT>::to_f(B[base_s[jj] + n]);

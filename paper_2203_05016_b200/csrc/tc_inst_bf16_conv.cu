@@ -1,0 +1,9 @@
+// tc_inst_bf16_conv.cu -- implicit-GEMM conv kernels of tc_kernels.cuh for bf16 operands
+// (one translation unit per dtype and operand kind, so nvcc builds them in parallel).
+#include "tc_kernels.cuh"
+
+namespace sbw {
+namespace tc {
+template SBW_TC_DISPATCH(SHFLBW_BF16, 1);
+}  // namespace tc
+}  // namespace sbw

@@ -1,0 +1,974 @@
+// tc_kernels.cuh -- K2: Shfl-BW SpMM / implicit-GEMM conv on the 5th-generation
+// tensor cores (kernels and launch templates; instantiated per input dtype and
+// operand kind in tc_inst_*.cu so they compile in parallel, host planning in
+// spmm_sm100.cu).
+//
+// Replaces spmm_execute (/root/reference/proj/src/spmm.cpp:76-146): the
+// reference's per-group "in-buffer stitching" (stitch_into, src/spmm.cpp:24-34),
+// tile_mma (src/spmm.cpp:60-74) and reordered write-back
+// (src/spmm.cpp:115-123) become one warp-specialised sm_100a kernel:
+//
+//   * work unit: (group g, 128 output columns n0..n0+127, V-slice).  The MMA
+//     runs transposed, D[n][v] = sum_j B[col_j][n] * W_g[v][j], so the
+//     activation tile is the M=128 operand and the group's V rows are the
+//     N operand (N = VS in {16, 32, 64, 128}): every V the paper uses maps
+//     to one legal tcgen05.mma shape, and the fp32 accumulator lives in TMEM
+//     (128 lanes x VS columns).
+//   * producer warp: for each 64-column K block, 32 TMA tile::gather4
+//     instructions (one per lane) fetch the 64 activation rows named by the
+//     group's column indices straight into the 128B-swizzled MN-major operand
+//     layout; pad columns carry index -1, which TMA zero-fills.  One 2D TMA
+//     tile load fetches the group's 64 x VS value block (V contiguous, the
+//     reference's column-major group layout, include/shflbw/formats.hpp:14-18).
+//     A full/empty mbarrier ring of `stages` slots keeps the loads ahead of
+//     the MMAs (the explicit empty barrier is what the literal Alg. 1 lacks,
+//     tests/test_pipeline.cpp:50-79).
+//   * MMA warp: one elected thread issues 4 x tcgen05.mma (K=16) per block and
+//     releases the slot with tcgen05.commit.
+//   * epilogue (all 4 warps): tcgen05.ld 32 columns at a time; thread t owns
+//     output column n0+t, so for every group row v the warp writes 32
+//     consecutive elements of output row row_indices[g*V+v] -- the permuted
+//     write-back fused into the epilogue with fully coalesced stores.
+//   * V split across a cluster of CS CTAs (CS*VS = V): each CTA owns VS of the
+//     group's rows; the activation gathers are split between the CTAs and
+//     multicast to all of them, so a group's activation tile is read from L2
+//     once per cluster while CS SMs share the MMA work.  Used when the grid
+//     would otherwise leave SMs idle (the north-star shape has 32 groups x 1
+//     column tile).
+//
+// Accumulation order: tensor-core fp32 accumulation over K=16 slices in
+// ascending k; products of 16-bit inputs are exact, so the result differs
+// from the reference's sequential fp32 sum only by accumulation rounding
+// (rel. Frobenius error ~1e-7, tolerance 1e-5 -- the reference's own bar,
+// tools/shflbw.cpp:33).
+#pragma once
+
+#include <cuda.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace sbw {
+namespace tc {
+
+
+constexpr int kBlockN = 128;  // output columns per CTA (MMA M)
+constexpr int kBlockK = 64;   // sparse columns per pipeline stage
+constexpr int kABytes = kBlockK * kBlockN * 2;  // 16 KB, two 64-column slabs
+
+struct TcParams {
+    const int32_t* row_indices;
+    const int32_t* group_ptr;
+    const int32_t* col_idx;
+    void* C;
+    int64_t ldc;
+    int V;
+    int g_begin;
+    int N;
+    int c_dtype;
+    int compact;
+    int stages;
+    int cps;         // activation slabs filled by cp.async (0..2); the rest by TMA gather4
+    const void* B;   // activations (cp.async path)
+    int64_t ldb;
+    unsigned long long* trace;  // optional per-CTA event timestamps (development)
+    int bulk_out;               // 1: C rows 16-byte aligned -> smem-staged vector stores
+    int bw;                     // MN block width of the activation tile (64 | 32 | 16 elements)
+    // implicit-GEMM conv geometry (KIND 1)
+    int Nb, H, W, RS, S, stride, pad, Q, PQ;
+    int ksplit;      // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
+    int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
+    int per_sm;      // persistent: resident CTAs per SM
+};
+
+// Development timeline (scripts/trace.py): compiled in only with -DSBW_TRACE.
+__device__ __forceinline__ void trace_event(unsigned long long* tr, int e) {
+#ifdef SBW_TRACE
+    if (tr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+        tr[cta * 32 + e] = t;
+    }
+#else
+    (void)tr;
+    (void)e;
+#endif
+}
+
+template <int VS>
+struct WeightLayout {
+    // bytes per k-row of the weight tile and UMMA layout constants
+    static constexpr int kRowBytes = VS * 2 < 128 ? VS * 2 : 128;
+    static constexpr int kSlabs = VS * 2 > 128 ? VS * 2 / 128 : 1;
+    static constexpr int kSlabBytes = kBlockK * kRowBytes;
+    static constexpr int kBytes = kSlabBytes * kSlabs;
+    static constexpr uint32_t kLayout = kRowBytes == 128 ? 2u : (kRowBytes == 64 ? 4u : 6u);
+    static constexpr uint32_t kSBO = 8 * kRowBytes;
+};
+
+constexpr int kMetaBlocks = 16;  // K blocks of column indices staged in smem at a time
+
+__device__ __forceinline__ void grid_dependency_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+template <class OT> __device__ __forceinline__ OT to_out(float x);
+template <> __device__ __forceinline__ float to_out<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ __half to_out<__half>(float x) { return __float2half_rn(x); }
+
+// Coalesced 16-byte stores of a staged [ROWS][128] tile of OT through the row
+// map: one output row = 128*sizeof(OT) bytes, 16 or 32 lanes per row.
+template <class OT, int ROWS>
+__device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigned char* ctile, const int32_t* rows,
+                                                int q, int lane, int n0) {
+    constexpr int esz = sizeof(OT);
+    constexpr int kLanesPerRow = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
+    constexpr int kRowsPerInst = 32 / kLanesPerRow;
+    const int chunk = lane % kLanesPerRow;
+    const int nn = n0 + chunk * (16 / esz);
+    if (nn < p.N) {
+#pragma unroll 4
+        for (int v = q * kRowsPerInst + lane / kLanesPerRow; v < ROWS; v += 4 * kRowsPerInst) {
+            const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
+            *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(rows[v]) * p.ldc + nn) * esz) = x;
+        }
+    }
+}
+
+// Epilogue for one output type: TMEM -> (staged tile -> 16-byte stores) or
+// direct stores, through the row map.  Kept as one straight-line routine per
+// type so the compiler never lowers the type switch per element.
+template <class OT, int VS>
+__device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row, int nkb, int m, int q, int lane,
+                                              int n0, const int32_t* rows_s, unsigned char* ctile) {
+    const int n = n0 + m;
+    const bool live = n < p.N;
+#pragma unroll
+    for (int c = 0; c < (VS + 31) / 32; ++c) {
+        constexpr int kW = VS < 32 ? VS : 32;
+        uint32_t r[32];
+        if (nkb > 0) {
+            if (kW == 32) tmem_ld32(t_row + c * 32, r);
+            else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tmem_ld_wait();
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (p.bulk_out) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                reinterpret_cast<OT*>(ctile)[(c * 32 + i) * kBlockN + m] = to_out<OT>(__uint_as_float(r[i]));
+        } else if (live) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[c * 32 + i]) * p.ldc + n] =
+                    to_out<OT>(__uint_as_float(r[i]));
+        }
+    }
+    if (p.bulk_out) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        store_tile_rows<OT, VS>(p, ctile, rows_s, q, lane, n0);
+    }
+}
+
+// K-split epilogue (KSF K ranks x VSF V ranks per cluster): K rank kr
+// finalises rows [kr*kRP, (kr+1)*kRP) of the VS slice.  Thread m (output
+// column n0+m) pushes the other K ranks' rows of its fp32 partial straight
+// from registers into their `recv` buffer with st.async (remote stores that
+// complete on the receiver's mbarrier), then sums the KSF partials of its own
+// rows in K-rank order (deterministic) and stores them through the staged
+// 16-byte path.  recv is [KSF][kRP][128] fp32: a warp's 32 threads touch 128
+// contiguous bytes per row, both for the remote stores and the local reads.
+template <class OT, int VS, int KSF, int VSF>
+__device__ __forceinline__ void ksplit_epilogue(const TcParams& p, uint32_t t_row, int nkb, int m, int q, int lane,
+                                                int n0, int kr, int vr, const int32_t* rows_s, float* recv,
+                                                uint64_t* recv_bar, unsigned char* ctile) {
+    constexpr int kRP = VS / KSF;
+    float vals[VS];
+#pragma unroll
+    for (int c = 0; c < (VS + 31) / 32; ++c) {
+        constexpr int kW = VS < 32 ? VS : 32;
+        uint32_t r[32];
+        if (nkb > 0) {
+            if (kW == 32) tmem_ld32(t_row + c * 32, r);
+            else tmem_ld16(t_row + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tmem_ld_wait();
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kW; ++i) vals[c * 32 + i] = __uint_as_float(r[i]);
+    }
+    // recv holds the KSF-1 peers' partials: peer c's rows land in slot
+    // (c < receiver ? c : c - 1)
+#pragma unroll
+    for (int c = 0; c < KSF; ++c) {
+        if (c == kr) continue;
+        const uint32_t peer = static_cast<uint32_t>(c * VSF + vr);
+        const int my_slot = kr < c ? kr : kr - 1;
+        const uint32_t slot = smem_u32(recv) + static_cast<uint32_t>((my_slot * kRP * kBlockN + m) * 4);
+        const uint32_t dst = mapa_shared(slot, peer), bar = mapa_shared(smem_u32(recv_bar), peer);
+#pragma unroll
+        for (int i = 0; i < kRP; ++i)
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                             dst + i * kBlockN * 4),
+                         "r"(__float_as_uint(vals[c * kRP + i])), "r"(bar)
+                         : "memory");
+    }
+    if (m == 0) trace_event(p.trace, 24);
+    mbar_wait(recv_bar, 0);
+    if (m == 0) trace_event(p.trace, 25);
+#pragma unroll
+    for (int i = 0; i < kRP; ++i) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int c = 0; c < KSF; ++c)  // K-rank order
+            acc += c == kr ? vals[c * kRP + i] : recv[((c < kr ? c : c - 1) * kRP + i) * kBlockN + m];
+        if (p.bulk_out) {
+            reinterpret_cast<OT*>(ctile)[i * kBlockN + m] = to_out<OT>(acc);
+        } else if (n0 + m < p.N) {
+            static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[kr * kRP + i]) * p.ldc + n0 + m] = to_out<OT>(acc);
+        }
+    }
+    if (p.bulk_out) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        store_tile_rows<OT, kRP>(p, ctile, rows_s + kr * kRP, q, lane, n0);
+    }
+}
+
+// KIND 2 (conv, weight in conv order): one gather4 = 4 K rows (ch, r, s) that
+// share the filter column s, each fetching the 64-element row segment of the
+// [C*H][W*Nb] input view that holds this MN block's 64/Nb adjacent output
+// positions (stride 1): row ch*H + p + r - pad, x = (q0 + s - pad)*Nb.  Rows
+// outside the image are -1 (zero-filled); columns left/right of it are out of
+// the view's bounds and zero-filled by TMA.  Returns the x coordinate.
+__device__ __forceinline__ int conv_wide_rows(const TcParams& p, int4& ci, int h0, int x0, bool pos_ok) {
+    int c0 = ci.x >= 0 ? ci.x : (ci.y >= 0 ? ci.y : (ci.z >= 0 ? ci.z : ci.w));
+    if (c0 < 0 || !pos_ok) {
+        ci = make_int4(-1, -1, -1, -1);
+        return 0;
+    }
+    auto row = [&](int c) -> int {
+        if (c < 0) return -1;
+        const int ch = c / p.RS, r = (c - ch * p.RS) / p.S;
+        const int h = h0 + r;
+        return (h < 0 || h >= p.H) ? -1 : ch * p.H + h;
+    };
+    const int sx = c0 % p.S;
+    ci.x = row(ci.x);
+    ci.y = row(ci.y);
+    ci.z = row(ci.z);
+    ci.w = row(ci.w);
+    return (x0 + sx) * p.Nb;
+}
+
+// warp roles (192 threads):
+//   warp 0  : stage bookkeeping -- waits for a free slot, arms the full
+//             barrier with the stage's byte count, loads the weight tile
+//   warp 1  : TMEM allocator + single-thread MMA issuer
+//   warps 2-5: gather issuers (8 gather4 each per K block, so the
+//             per-instruction ELECT/R2UR issue loop runs on all four SM
+//             sub-partitions in parallel), then the epilogue (warp w owns
+//             TMEM lanes 32*(w%4)..+31)
+constexpr int kGatherWarps = 4;
+constexpr int kThreadsTc = 64 + 32 * kGatherWarps;
+
+template <int DT, int VS, int CS, int KIND, int KSPLIT>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    k_spmm_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
+              TcParams p) {
+    using WL = WeightLayout<VS>;
+    constexpr int kStageBytes = kABytes + WL::kBytes;
+    constexpr uint32_t kTmemCols = VS < 32 ? 32 : VS;
+    constexpr uint32_t kIdesc = umma_idesc_f16(DT == SHFLBW_BF16 ? 1 : 0, kBlockN, VS);
+    using T = typename Elem<DT>::T;
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int stages = p.stages;
+    // cluster = KSF (K split) x VSF (V split) CTAs: KSPLIT 0 -> V split by
+    // CS, 1 -> K split by CS, 2 -> 2 x 2 (CS = 4).  Rank = kr * VSF + vr.
+    constexpr int KSF = KSPLIT == 1 ? CS : (KSPLIT == 2 ? 2 : 1);
+    constexpr int VSF = CS / KSF;
+    static_assert(KSF * VSF == CS, "cluster shape");
+    // K split: partial rows pushed here by the K peers, [KSF][128][VS/KSF] fp32
+    float* recv = reinterpret_cast<float*>(smem + stages * kStageBytes);
+    constexpr bool kKSplit = KSF > 1;
+    constexpr bool mcast = VSF > 1;
+    const int recv_bytes = kKSplit ? (KSF - 1) * (VS / KSF) * kBlockN * 4 : 0;
+    int32_t* meta_s = reinterpret_cast<int32_t*>(smem + stages * kStageBytes + recv_bytes);  // [kMetaBlocks][64]
+    int32_t* rows_s = meta_s + kMetaBlocks * kBlockK;                           // VS
+    uint64_t* full = reinterpret_cast<uint64_t*>(rows_s + (VS < 2 ? 2 : VS));
+    uint64_t* empty = full + stages;
+    uint64_t* accum = empty + stages;
+    uint64_t* recv_bar = accum + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
+    const int n_tile = blockIdx.x / CS;
+    const int n0 = n_tile * kBlockN;
+    const int g = p.g_begin + blockIdx.y;
+    const int gp = p.group_ptr[g];
+    const int nkb_all = (p.group_ptr[g + 1] - gp) / kBlockK;
+    // K split: this CTA's K blocks [kbase, kbase + nkb); V split: its V rows
+    const int kr = static_cast<int>(rank) / VSF, vr = static_cast<int>(rank) % VSF;
+    const int kbase = kKSplit ? nkb_all * kr / KSF : 0;
+    const int nkb = kKSplit ? nkb_all * (kr + 1) / KSF - kbase : nkb_all;
+    const int vbase = vr * VS;
+    // multicast group: the VSF CTAs that share this CTA's K blocks
+    const uint16_t cmask = static_cast<uint16_t>(((1u << VSF) - 1u) << (kr * VSF));
+    const int cps = p.cps;
+    const int et = threadIdx.x - 64;  // gather/epilogue thread 0..127 (warps 2..5)
+    if (threadIdx.x == 0) trace_event(p.trace, 0);
+
+    // gather warps stage a window of column indices (all 64 per K block)
+    auto stage_meta = [&](int kb0) {
+        const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
+        const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + (kbase + kb0) * kBlockK);
+        for (int i = et; i < nb * (kBlockK / 4); i += 128) reinterpret_cast<int4*>(meta_s)[i] = src[i];
+    };
+
+    // ---- prologue (reads only the static sparse matrix: overlaps the
+    //      previous kernel under PDL) ---------------------------------------
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1 + (cps > 0 ? 32 * kGatherWarps : 0));
+            mbar_init(&empty[s], mcast ? VSF : 1);
+        }
+        mbar_init(accum, 1);
+        mbar_init(recv_bar, 1);
+        if (kKSplit)  // the KSF-1 K peers' partial rows for this CTA
+            mbar_arrive_expect_tx(recv_bar, (KSF - 1) * (VS / KSF) * kBlockN * 4);
+        fence_mbar_init();
+        tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmW);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    if (CS > 1) cluster_sync();
+    else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_d = *tmem_slot;
+    if (threadIdx.x == 0) {
+        grid_launch_dependents();
+        trace_event(p.trace, 1);
+    }
+
+    if (warp == 0) {
+        // ---------------- stage bookkeeping + weights ----------------
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % stages;
+                if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[s], (2 - cps) * (kABytes / 2) + WL::kBytes);
+#pragma unroll
+                for (int sl = 0; sl < WL::kSlabs; ++sl)
+                    tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
+                                vbase + sl * 64, gp + (kbase + kb) * kBlockK);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        // activation operand: MN-major, MN blocks of p.bw elements, swizzle = block row bytes
+        const uint32_t a_row = static_cast<uint32_t>(p.bw) * 2;
+        const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % stages;
+                mbar_wait(&full[s], (kb / stages) & 1);
+                tc_fence_after();
+                if (kb == 0) trace_event(p.trace, 3);
+                if (kb < 8) trace_event(p.trace, 8 + kb);
+                const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
+                const uint32_t w_addr = a_addr + kABytes;
+#pragma unroll
+                for (int ks = 0; ks < kBlockK / 16; ++ks) {
+                    const uint64_t adesc = umma_smem_desc(a_addr + ks * 16 * a_row, kBlockK * a_row, 8 * a_row,
+                                                          a_layout);
+                    const uint64_t bdesc = umma_smem_desc(w_addr + ks * 16 * WL::kRowBytes,
+                                                          WL::kSlabBytes, WL::kSBO, WL::kLayout);
+                    umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
+                }
+                if constexpr (!mcast) umma_commit(&empty[s]);
+                else umma_commit_mc(&empty[s], cmask);
+            }
+            trace_event(p.trace, 4);
+            if (nkb > 0) umma_commit(accum);
+            else mbar_arrive(accum);
+        }
+        __syncwarp();
+    } else {
+        // ---------------- activation producers ----------------
+        const int gw = warp - 2;
+        // TMA part: slabs [0, 2-cps): row group rg of slab sl, 16 row groups
+        // per slab, spread over the 4 warps' first lanes
+        const int tma_slabs = 2 - cps;
+        const int nblk = KIND == 0 ? tma_slabs : kBlockN / p.bw;  // MN blocks filled by TMA
+        const int blk_bytes = kBlockK * p.bw * 2;
+        const int per_warp = 16 * nblk / kGatherWarps;              // gather4s per warp per K block
+        const int gi = gw * per_warp + lane;                        // this lane's gather
+        // a warp owns 4 row groups (16 rows) in every MN block, so both halves
+        // of an activation row are requested together
+        const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
+        const bool t_issue = lane < per_warp && (!mcast || (gi % VSF) == vr);
+        // conv: this gather's output positions (fixed for the CTA)
+        int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
+        bool g_pos_ok = true;
+        if (KIND == 1 || KIND == 2) {
+            const int base_n = n0 + g_b * p.bw;
+            const int pos = base_n / p.Nb;
+            g_x = base_n - pos * p.Nb;
+            g_pos_ok = pos < p.PQ;
+            g_p0 = (pos / p.Q) * p.stride - p.pad;
+            g_q0 = (pos % p.Q) * p.stride - p.pad;
+        }
+        auto conv_row = [&](int c) -> int {
+            if (c < 0 || !g_pos_ok) return -1;
+            const int ch = c / p.RS, rs = c - ch * p.RS;
+            const int r = rs / p.S, sx = rs - r * p.S;
+            const int h = g_p0 + r, w = g_q0 + sx;
+            if (h < 0 || h >= p.H || w < 0 || w >= p.W) return -1;
+            return (ch * p.H + h) * p.W + w;
+        };
+        // cp.async part (SpMM only): slabs [2-cps, 2): cps*512 16-byte chunks per K block
+        const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
+        const T* Bp = static_cast<const T*>(p.B);
+        if (nkb > 0) stage_meta(0);  // static metadata: before the dependency wait
+        grid_dependency_wait();  // B may be the previous kernel's output
+        if (et == 0) trace_event(p.trace, 2);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % stages;
+            const int win = kb % kMetaBlocks;
+            if (win == 0 && kb > 0) {
+                asm volatile("bar.sync 2, 128;" ::: "memory");  // all done with the old window
+                stage_meta(kb);
+            }
+            if (win == 0) asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+            if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
+            unsigned char* a_st = smem + s * kStageBytes;
+            const int32_t* mk = meta_s + win * kBlockK;
+            if (t_issue) {
+                int4 ci = reinterpret_cast<const int4*>(mk)[g_rg];
+                int x = g_x;
+                if (KIND == 1) {
+                    ci.x = conv_row(ci.x);
+                    ci.y = conv_row(ci.y);
+                    ci.z = conv_row(ci.z);
+                    ci.w = conv_row(ci.w);
+                } else if (KIND == 2) {
+                    x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
+                }
+                void* dst = a_st + g_b * blk_bytes + g_rg * (4 * p.bw * 2);
+                if constexpr (!mcast)
+                    tma_gather4(dst, &tmB, &full[s], x, ci.x, ci.y, ci.z, ci.w);
+                else
+                    tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci.x, ci.y, ci.z, ci.w);
+            }
+            if (cps > 0) {
+                const uint32_t a_u32 = smem_u32(a_st);
+                for (int id = et; id < cps * 512; id += 128) {
+                    const int r = id >> cpr_log2, c = id & ((1 << cpr_log2) - 1);
+                    const int sl = tma_slabs + (c >> 3), cc = c & 7;
+                    const int col = mk[r];
+                    const int n = n0 + sl * 64 + cc * 8;
+                    const bool ok = col >= 0 && n < p.N;
+                    const T* src = ok ? Bp + static_cast<int64_t>(col) * p.ldb + n : Bp;
+                    cp_async16(a_u32 + sl * (kABytes / 2) + r * 128 + ((cc ^ (r & 7)) << 4), src, ok);
+                }
+                cp_async_arrive_noinc(&full[s]);
+            }
+            __syncwarp();
+        }
+        // output row map for the epilogue, loaded while the MMAs run
+        for (int v = et; v < VS; v += 128) {
+            const int64_t gr = static_cast<int64_t>(g) * p.V + vbase + v;
+            rows_s[v] = p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
+                                  : p.row_indices[gr];
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+
+        // ---------------- epilogue: TMEM -> permuted rows of C ----------------
+        mbar_wait(accum, 0);
+        tc_fence_after();
+        if (et == 0) trace_event(p.trace, 5);
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int m = q * 32 + lane;
+        const uint32_t t_row = tmem_d + (static_cast<uint32_t>(q * 32) << 16);
+        // all MMAs are complete (accum), so the stage buffers are free: they
+        // hold the [VS][128] output tile for the bulk row stores
+        unsigned char* ctile = smem;
+        if constexpr (kKSplit) {
+            if (p.c_dtype == SHFLBW_F32)
+                ksplit_epilogue<float, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar, ctile);
+            else if (p.c_dtype == SHFLBW_BF16)
+                ksplit_epilogue<__nv_bfloat16, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv,
+                                                             recv_bar, ctile);
+            else
+                ksplit_epilogue<__half, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar,
+                                                      ctile);
+        } else {
+            if (p.c_dtype == SHFLBW_F32) epilogue_rows<float, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+            else if (p.c_dtype == SHFLBW_BF16)
+                epilogue_rows<__nv_bfloat16, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+            else epilogue_rows<__half, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+        }
+    }
+    if (et == 0) trace_event(p.trace, 6);
+    tc_fence_before();
+    if (CS > 1) cluster_sync_relaxed();  // only smem lifetime matters here
+    else __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem_d, kTmemCols);
+    if (threadIdx.x == 0) trace_event(p.trace, 7);
+}
+
+// ===========================================================================
+// Persistent variant: one CTA (cluster) per SM slot loops over (group,
+// column tile) units; the full/empty ring runs on across units and two TMEM
+// accumulators (ping-pong) let the epilogue of unit i overlap the loads and
+// MMAs of unit i+1.  Roles (320 threads): warp 0 weights + stage arming,
+// warp 1 TMEM + MMA, warps 2-5 activation gathers, warps 6-9 epilogue.
+// Used when the grid would need more than one wave of CTAs.
+// ===========================================================================
+constexpr int kThreadsPersist = 320;
+
+template <class OT, int VS>
+__device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc, int nkb, int m, int q, int lane,
+                                              int n0, const int32_t* rows_s, unsigned char* ctile,
+                                              uint64_t* acc_empty) {
+    const int n = n0 + m;
+    const bool live = n < p.N;
+#pragma unroll
+    for (int c = 0; c < (VS + 31) / 32; ++c) {
+        constexpr int kW = VS < 32 ? VS : 32;
+        uint32_t r[32];
+        if (nkb > 0) {
+            if (kW == 32) tmem_ld32(t_acc + c * 32, r);
+            else tmem_ld16(t_acc + c * 32, *reinterpret_cast<uint32_t(*)[16]>(r));
+            tmem_ld_wait();
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (p.bulk_out) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                reinterpret_cast<OT*>(ctile)[(c * 32 + i) * kBlockN + m] = to_out<OT>(__uint_as_float(r[i]));
+        } else if (live) {
+#pragma unroll
+            for (int i = 0; i < kW; ++i)
+                static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[c * 32 + i]) * p.ldc + n] =
+                    to_out<OT>(__uint_as_float(r[i]));
+        }
+    }
+    // accumulator drained: the MMA warp may start the next unit in it
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_empty);
+    if (p.bulk_out) {
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+        store_tile_rows<OT, VS>(p, ctile, rows_s, q, lane, n0);
+    }
+}
+
+template <int DT, int VS, int CS, int KIND>
+__global__ void __launch_bounds__(kThreadsPersist, 2)
+    k_spmm_persist(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW, TcParams p,
+                   int units, int n_tiles) {
+    using WL = WeightLayout<VS>;
+    constexpr int kStageBytes = kABytes + WL::kBytes;
+    constexpr uint32_t kAccCols = VS < 32 ? 32 : VS;
+    constexpr uint32_t kTmemCols = 2 * kAccCols;
+    constexpr uint32_t kIdesc = umma_idesc_f16(DT == SHFLBW_BF16 ? 1 : 0, kBlockN, VS);
+    constexpr bool mcast = CS > 1;
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int stages = p.stages;
+    const int ngroups = (units + n_tiles - 1) / n_tiles;
+    const int out_esz = p.c_dtype == SHFLBW_F32 ? 4 : 2;
+    unsigned char* ctile = smem + stages * kStageBytes;  // [VS][128] out (staged stores only)
+    int32_t* meta_s = reinterpret_cast<int32_t*>(ctile + (p.bulk_out ? VS * kBlockN * out_esz : 0));  // [2][kMetaBlocks][64]
+    int32_t* rows_s = meta_s + 2 * kMetaBlocks * kBlockK;                              // VS
+    int32_t* gptr_s = rows_s + (VS < 4 ? 4 : VS);                                      // ngroups + 1
+    uint64_t* full = reinterpret_cast<uint64_t*>(gptr_s + ((ngroups + 2) & ~1));
+    uint64_t* empty = full + stages;
+    uint64_t* acc_full = empty + stages;  // [2]
+    uint64_t* acc_empty = acc_full + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
+    const int cid = blockIdx.x / CS, nclusters = gridDim.x / CS;
+    const int vbase = static_cast<int>(rank) * VS;
+    const uint16_t cmask = static_cast<uint16_t>((1u << CS) - 1u);
+
+    if (threadIdx.x == 0) trace_event(p.trace, 0);
+    // this launch's group offsets (static: before the dependency wait), so no
+    // role stalls on a global load at a unit boundary
+    for (int x = threadIdx.x; x <= ngroups; x += blockDim.x) gptr_s[x] = p.group_ptr[p.g_begin + x];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], mcast ? CS : 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        fence_mbar_init();
+        tma_prefetch_desc(&tmB);
+        tma_prefetch_desc(&tmW);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    if (CS > 1) cluster_sync();
+    else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) {
+        grid_launch_dependents();
+        trace_event(p.trace, 1);
+    }
+    auto unit_nkb = [&](int u) { const int gl = u / n_tiles; return (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK; };
+
+    if (warp == 0) {
+        // ---------------- stage arming + weights ----------------
+        if (lane == 0) {
+            int kbg = 0;
+            for (int u = cid; u < units; u += nclusters) {
+                const int gl = u / n_tiles;
+                const int gp = gptr_s[gl];
+                const int nkb = (gptr_s[gl + 1] - gp) / kBlockK;
+                for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                    const int s = kbg % stages;
+                    if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], kStageBytes);
+#pragma unroll
+                    for (int sl = 0; sl < WL::kSlabs; ++sl)
+                        tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
+                                    vbase + sl * 64, gp + kb * kBlockK);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        const uint32_t a_row = KIND == 0 ? 128u : static_cast<uint32_t>(p.bw) * 2;
+        const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
+        if (lane == 0) {
+            int kbg = 0, i = 0;
+            for (int u = cid; u < units; u += nclusters, ++i) {
+                const int nkb = unit_nkb(u);
+                const int b = i & 1;
+                mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
+                tc_fence_after();
+                if (i < 8) trace_event(p.trace, 8 + i);  // MMA: accumulator free for unit i
+                const uint32_t tmem_d = tmem_base + b * kAccCols;
+                for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                    const int s = kbg % stages;
+                    mbar_wait(&full[s], (kbg / stages) & 1);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
+                    const uint32_t w_addr = a_addr + kABytes;
+#pragma unroll
+                    for (int ks = 0; ks < kBlockK / 16; ++ks) {
+                        const uint64_t adesc = umma_smem_desc(a_addr + ks * 16 * a_row, kBlockK * a_row, 8 * a_row,
+                                                              a_layout);
+                        const uint64_t bdesc = umma_smem_desc(w_addr + ks * 16 * WL::kRowBytes, WL::kSlabBytes,
+                                                              WL::kSBO, WL::kLayout);
+                        umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
+                    }
+                    if constexpr (!mcast) umma_commit(&empty[s]);
+                    else umma_commit_mc(&empty[s], cmask);
+                }
+                if (nkb > 0) umma_commit(&acc_full[b]);
+                else mbar_arrive(&acc_full[b]);
+            }
+        }
+        __syncwarp();
+    } else if (warp < 6) {
+        // ---------------- activation gathers ----------------
+        const int gw = warp - 2, et = threadIdx.x - 64;  // et 0..127
+        const int bw = KIND == 0 ? 64 : p.bw;
+        const int nblk = kBlockN / bw;
+        const int blk_bytes = kBlockK * bw * 2;
+        const int per_warp = 16 * nblk / kGatherWarps;
+        const int gi = gw * per_warp + lane;
+        const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
+        const bool t_issue = lane < per_warp && (!mcast || (gi % CS) == static_cast<int>(rank));
+        // column-index windows: meta_s[buf] holds kMetaBlocks K blocks of a
+        // unit; the first window of unit i+1 is prefetched (cp.async) into the
+        // other buffer while unit i issues its gathers
+        auto load_window = [&](int u, int kb0, int buf, bool async) {
+            const int gl = u / n_tiles;
+            const int nkb = (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK;
+            const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
+            const int32_t* src = p.col_idx + gptr_s[gl] + kb0 * kBlockK;
+            int32_t* dst = meta_s + buf * kMetaBlocks * kBlockK;
+            for (int x = et; x < nb * (kBlockK / 4); x += 128) {
+                if (async) cp_async16(smem_u32(dst + 4 * x), src + 4 * x, true);
+                else reinterpret_cast<int4*>(dst)[x] = reinterpret_cast<const int4*>(src)[x];
+            }
+        };
+        if (cid < units) load_window(cid, 0, 0, false);
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        grid_dependency_wait();  // B may be the previous kernel's output
+        if (et == 0) trace_event(p.trace, 2);
+        int kbg = 0, i = 0;
+        for (int u = cid; u < units; u += nclusters, ++i) {
+            const int buf = i & 1;
+            if (et == 0 && i < 8) trace_event(p.trace, 16 + i);  // gathers: unit i starts issuing
+            const int un = u + nclusters;
+            if (un < units) {  // the other buffer was released by the bar.sync ending unit i-1
+                load_window(un, 0, buf ^ 1, true);
+                cp_async_commit();
+            }
+            const int n0 = (u % n_tiles) * kBlockN;
+            const int nkb = unit_nkb(u);
+            const int32_t* mbuf = meta_s + buf * kMetaBlocks * kBlockK;
+            int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
+            bool g_pos_ok = true;
+            if (KIND == 1 || KIND == 2) {
+                const int base_n = n0 + g_b * p.bw;
+                const int pos = base_n / p.Nb;
+                g_x = base_n - pos * p.Nb;
+                g_pos_ok = pos < p.PQ;
+                g_p0 = (pos / p.Q) * p.stride - p.pad;
+                g_q0 = (pos % p.Q) * p.stride - p.pad;
+            }
+            for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                const int s = kbg % stages;
+                const int win = kb % kMetaBlocks;
+                if (win == 0 && kb > 0) {  // deep group: later windows of this unit, synchronously
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    load_window(u, kb, buf, false);
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                }
+                if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
+                if (t_issue) {
+                    int4 ci = reinterpret_cast<const int4*>(mbuf + win * kBlockK)[g_rg];
+                    int x = g_x;
+                    if (KIND == 2) x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
+                    if (KIND == 1) {
+                        auto conv_row = [&](int c) -> int {
+                            if (c < 0 || !g_pos_ok) return -1;
+                            const int ch = c / p.RS, rs = c - ch * p.RS;
+                            const int r = rs / p.S, sx = rs - r * p.S;
+                            const int h = g_p0 + r, w = g_q0 + sx;
+                            if (h < 0 || h >= p.H || w < 0 || w >= p.W) return -1;
+                            return (ch * p.H + h) * p.W + w;
+                        };
+                        ci.x = conv_row(ci.x);
+                        ci.y = conv_row(ci.y);
+                        ci.z = conv_row(ci.z);
+                        ci.w = conv_row(ci.w);
+                    }
+                    void* dst = smem + s * kStageBytes + g_b * blk_bytes + g_rg * (4 * bw * 2);
+                    if constexpr (!mcast)
+                        tma_gather4(dst, &tmB, &full[s], x, ci.x, ci.y, ci.z, ci.w);
+                    else
+                        tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci.x, ci.y, ci.z, ci.w);
+                }
+                __syncwarp();
+            }
+            cp_async_wait<0>();
+            asm volatile("bar.sync 2, 128;" ::: "memory");  // next unit's window visible; this buffer free
+        }
+    } else {
+        // ---------------- epilogue ----------------
+        const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - 192;
+        auto row_of = [&](int u, int v) -> int32_t {
+            const int g = p.g_begin + u / n_tiles;
+            return p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
+                             : p.row_indices[static_cast<int64_t>(g) * p.V + vbase + v];
+        };
+        int32_t next_row = (cid < units && et < VS) ? row_of(cid, et) : 0;  // static: before the wait
+        grid_dependency_wait();  // C may still be read by the previous kernel
+        int i = 0;
+        for (int u = cid; u < units; u += nclusters, ++i) {
+            const int n0 = (u % n_tiles) * kBlockN;
+            const int nkb = unit_nkb(u);
+            const int b = i & 1;
+            asm volatile("bar.sync 3, 128;" ::: "memory");  // previous unit done with rows_s / ctile
+            if (et < VS) rows_s[et] = next_row;
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            if (u + nclusters < units && et < VS) next_row = row_of(u + nclusters, et);  // in flight meanwhile
+            mbar_wait(&acc_full[b], (i >> 1) & 1);
+            tc_fence_after();
+            if (et == 0 && i < 8) trace_event(p.trace, 24 + i);  // epilogue: unit i accumulated
+            const uint32_t t_acc = tmem_base + b * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+            if (p.c_dtype == SHFLBW_F32)
+                persist_store<float, VS>(p, t_acc, nkb, m, q, lane, n0, rows_s, ctile, &acc_empty[b]);
+            else if (p.c_dtype == SHFLBW_BF16)
+                persist_store<__nv_bfloat16, VS>(p, t_acc, nkb, m, q, lane, n0, rows_s, ctile, &acc_empty[b]);
+            else
+                persist_store<__half, VS>(p, t_acc, nkb, m, q, lane, n0, rows_s, ctile, &acc_empty[b]);
+        }
+    }
+    tc_fence_before();
+    if (CS > 1) cluster_sync_relaxed();
+    else __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem_base, kTmemCols);
+    if (threadIdx.x == 0) trace_event(p.trace, 7);
+}
+
+// ---------------- host side ----------------
+
+int num_sms();
+
+template <int DT, int VS, int CS, int KIND, int KSPLIT>
+int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+              cudaStream_t s) {
+    constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
+    constexpr int KSF = KSPLIT == 1 ? CS : (KSPLIT == 2 ? 2 : 1);
+    const size_t recv = (CS > 1 && KSPLIT) ? static_cast<size_t>(KSF - 1) * (VS / KSF) * kBlockN * 4 : 0;
+    const size_t smem = static_cast<size_t>(prm.stages) * kStage + recv + 1024 + kMetaBlocks * kBlockK * 4 +
+                        (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 3) * 8 + 16;
+    auto kern = k_spmm_tc<DT, VS, CS, KIND, KSPLIT>;
+    static std::atomic<size_t> configured{0};  // per instantiation: raise the smem cap once
+    if (smem > configured.load(std::memory_order_relaxed)) {
+        SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        configured.store(smem, std::memory_order_relaxed);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_tiles * CS, groups, 1);
+    cfg.blockDim = dim3(kThreadsTc, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = option("pdl") ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, prm));
+    count_launch();
+    return SHFLBW_OK;
+}
+
+
+template <int DT, int VS, int CS, int KIND>
+int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+                   cudaStream_t s) {
+    constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
+    const size_t out_esz = prm.c_dtype == SHFLBW_F32 ? 4 : 2;
+    const size_t smem = static_cast<size_t>(prm.stages) * kStage +
+                        (prm.bulk_out ? static_cast<size_t>(VS) * kBlockN * out_esz : 0) + 1024 +
+                        2 * kMetaBlocks * kBlockK * 4 + (VS < 4 ? 4 : VS) * 4 + ((groups + 2) & ~1) * 4 +
+                        (2 * prm.stages + 5) * 8 + 16;
+    auto kern = k_spmm_persist<DT, VS, CS, KIND>;
+    static std::atomic<size_t> configured{0};
+    if (smem > configured.load(std::memory_order_relaxed)) {
+        SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        configured.store(smem, std::memory_order_relaxed);
+    }
+    const int units = n_tiles * groups;
+    const int per_sm = prm.per_sm;
+    // per_sm CTAs must be co-resident: launch bounds (320, 2) keep registers
+    // <= 102 and the host sizes stages so per_sm CTAs fit in shared memory
+    const int clusters = std::min(units, per_sm * num_sms() / CS);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(clusters * CS, 1, 1);
+    cfg.blockDim = dim3(kThreadsPersist, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = option("pdl") ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, prm, units, n_tiles));
+    count_launch();
+    return SHFLBW_OK;
+}
+
+// SpMM variants: V split (CS CTAs, multicast), K split, 2 x 2, persistent
+template <int DT, int VS>
+int dispatch_spmm(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles,
+                  int groups, cudaStream_t s) {
+    if (prm.persistent) {
+        switch (cs) {
+            case 1: return launch_persist<DT, VS, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 2: return launch_persist<DT, VS, 2, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 4: return launch_persist<DT, VS, 4, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        }
+        return SHFLBW_UNSUPPORTED;
+    }
+    switch (cs * 2 + prm.ksplit) {
+        case 2: case 3: return launch_tc<DT, VS, 1, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 4: return launch_tc<DT, VS, 2, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 5: return launch_tc<DT, VS, 2, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 8: return launch_tc<DT, VS, 4, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 9: return launch_tc<DT, VS, 4, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 10: return launch_tc<DT, VS, 4, 0, 2>(tmB, tmW, prm, n_tiles, groups, s);
+    }
+    return SHFLBW_UNSUPPORTED;
+}
+
+// conv variants (KIND 1: one output position per activation row, KIND 2:
+// conv-ordered weight, 128-byte rows): one CTA per unit, K split over 2 or 4
+// CTAs, persistent
+template <int DT, int VS, int KIND>
+int dispatch_conv(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles,
+                  int groups, cudaStream_t s) {
+    if (prm.persistent) return launch_persist<DT, VS, 1, KIND>(tmB, tmW, prm, n_tiles, groups, s);
+    switch (cs * 2 + prm.ksplit) {
+        case 2: case 3: return launch_tc<DT, VS, 1, KIND, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 5: return launch_tc<DT, VS, 2, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 9: return launch_tc<DT, VS, 4, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
+    }
+    return SHFLBW_UNSUPPORTED;
+}
+
+// KG 0: SpMM (kind 0), KG 1: conv (kinds 1, 2) -- explicitly instantiated in
+// tc_inst_{bf16,f16}_{spmm,conv}.cu
+template <int DT, int KG>
+int dispatch(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm,
+             int n_tiles, int groups, cudaStream_t s) {
+    auto one = [&]<int VS>() -> int {
+        if constexpr (KG == 0) return dispatch_spmm<DT, VS>(cs, tmB, tmW, prm, n_tiles, groups, s);
+        else if (kind == 2) return dispatch_conv<DT, VS, 2>(cs, tmB, tmW, prm, n_tiles, groups, s);
+        else return dispatch_conv<DT, VS, 1>(cs, tmB, tmW, prm, n_tiles, groups, s);
+    };
+    switch (vs) {
+        case 16: return one.template operator()<16>();
+        case 32: return one.template operator()<32>();
+        case 64: return one.template operator()<64>();
+        case 128: return one.template operator()<128>();
+    }
+    return SHFLBW_UNSUPPORTED;
+}
+
+#define SBW_TC_DISPATCH(DT, KG)                                                                          \
+    int dispatch<DT, KG>(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW,      \
+                         const TcParams& prm, int n_tiles, int groups, cudaStream_t s)
+extern template SBW_TC_DISPATCH(SHFLBW_BF16, 0);
+extern template SBW_TC_DISPATCH(SHFLBW_BF16, 1);
+extern template SBW_TC_DISPATCH(SHFLBW_F16, 0);
+extern template SBW_TC_DISPATCH(SHFLBW_F16, 1);
+
+}  // namespace tc
+}  // namespace sbw

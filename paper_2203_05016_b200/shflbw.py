@@ -277,6 +277,19 @@ def spmm_execute(a: ShflBWMatrix, b: torch.Tensor, cfg: TileConfig | None = None
     return out
 
 
+def conv_prepare(w: ShflBWMatrix, geo: "ConvGeometry | int") -> ShflBWMatrix:
+    """A copy of conv weight `w` in conv order for filter width S = geo.s
+    (shflbw_cu_conv_prepare): per group, columns ordered by filter column s
+    with each s-run padded to a multiple of 4.  conv2d then fetches 128-byte
+    activation rows (64/N adjacent output positions) for stride-1 convs with
+    batch N in {16, 32}; results stay within the 1e-5 tolerance (only the
+    fp32 summation order differs).  One-time cost, like a filter reorder."""
+    S = geo if isinstance(geo, int) else geo.s
+    cm = L.CuMatrix()
+    _check(_lib().shflbw_cu_conv_prepare(w.ptr, S, C.byref(cm), _stream()))
+    return ShflBWMatrix(cm)
+
+
 def fold_input_permutation(a: ShflBWMatrix, producer) -> ShflBWMatrix:
     """Remap a's column indices so it consumes the group-ordered output of
     `producer` (a ShflBWMatrix run with permuted_output=True, or a device

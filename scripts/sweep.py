@@ -98,7 +98,7 @@ def conv_row(name, C, H, Kf, R, pad, Nb, V, alpha, steps, dev):
     mats, xs, outs, Wc, xc = [], [], [], [], []
     for s in range(n):
         W = bench.uniform_bf16(torch, (Kf, crs), 100 + s, dev)
-        mats.append(sb.compress_shflbw(W, mask, V))
+        mats.append(sb.conv_prepare(sb.compress_shflbw(W, mask, V), geo))  # one-time conv weight order
         Wc.append((W * mask).reshape(Kf, C, R, R).contiguous())
         x = bench.uniform_bf16(torch, (C, H, H, Nb), 300 + s, dev)
         xs.append(x)

@@ -599,3 +599,117 @@ def test_fold_input_permutation_errors(sb, oracle):
     x = torch.zeros((16, 4, 4, 32), dtype=torch.bfloat16, device="cuda")  # 16*4*4... C*R*S = 256 = 16*4*4
     with pytest.raises(sb.BadParams):
         sb.conv2d(a, x, sb.ConvGeometry(4, 4, 1, 0))
+
+
+# ------------------------------------------- conv order (128-byte activation rows)
+
+def _conv_setup(oracle, C, H, Wd, Kf, R, S, V, Nb, seed=5):
+    crs = C * R * S
+    mask = oracle.random_shflbw_mask(Kf, crs, V, max(1, crs // 4), oracle.rng(seed))
+    Wt = oracle.round16(oracle.random_dense(Kf, crs, seed + 1))
+    x = oracle.round16(oracle.fill_uniform(oracle.rng(seed + 2), C * H * Wd * Nb).reshape(C, H, Wd, Nb))
+    return mask, Wt, x
+
+
+def test_conv_prepare_layout(sb, oracle):
+    """Per group: the same (column, values) pairs, s-runs in ascending s and
+    ascending c, every aligned quad of K positions shares one filter column
+    s, groups padded to K-tile multiples; decompress is unchanged."""
+    C, R, S, Kf, V = 24, 3, 3, 128, 32
+    mask, Wt, _ = _conv_setup(oracle, C, 4, 4, Kf, R, S, V, 16)
+    w = sb.compress_shflbw(dev(Wt), dev(mask), V)
+    wp = sb.conv_prepare(w, sb.ConvGeometry(R, S, 1, 1))
+    gp, ci, vv = w.raw()
+    gq, cq, vq = wp.raw()
+    assert np.all(np.diff(gq) % 64 == 0)
+    for g in range(Kf // V):
+        a0, a1, b0, b1 = gp[g], gp[g + 1], gq[g], gq[g + 1]
+        cols = ci[a0:a1][ci[a0:a1] >= 0]
+        got = cq[b0:b1]
+        quads = got.reshape(-1, 4)
+        for qd in quads:
+            v = qd[qd >= 0]
+            assert len(set((v % S).tolist())) <= 1
+        valid = got[got >= 0]
+        want = np.concatenate([np.sort(cols[cols % S == s]) for s in range(S)])
+        assert np.array_equal(valid, want)
+        src = {int(c): vv[(a0 + j) * V:(a0 + j + 1) * V] for j, c in enumerate(ci[a0:a1]) if c >= 0}
+        for j, c in enumerate(got):
+            blk = vq[(b0 + j) * V:(b0 + j + 1) * V]
+            assert np.array_equal(blk, src[int(c)] if c >= 0 else np.zeros(V, blk.dtype))
+    d0 = sb.decompress(w).cpu().numpy()
+    d1 = sb.decompress(wp).cpu().numpy()
+    assert np.array_equal(d0, d1)
+    with pytest.raises(sb.BadParams):
+        wp.to_host()
+
+
+@pytest.mark.parametrize("C,H,Wd,Kf,R,pad,V,Nb", [
+    (16, 8, 8, 64, 3, 1, 64, 32),     # 128-byte rows: 2 positions x 32
+    (8, 6, 12, 64, 3, 1, 32, 16),     # 4 positions x 16, H != W
+    (8, 7, 7, 64, 3, 1, 64, 32),      # Q odd: falls back to one position per row
+    (12, 9, 9, 128, 3, 0, 64, 32),    # no padding
+    (4, 10, 10, 64, 5, 2, 16, 32),    # 5x5 filter (S = 5)
+    (64, 14, 14, 128, 3, 1, 64, 32),  # ResNet-like
+])
+def test_conv_prepared_matches_oracle(sb, oracle, C, H, Wd, Kf, R, pad, V, Nb):
+    mask, Wt, x = _conv_setup(oracle, C, H, Wd, Kf, R, R, V, Nb)
+    w = sb.compress_shflbw(dev(Wt), dev(mask), V)
+    wp = sb.conv_prepare(w, sb.ConvGeometry(R, R, 1, pad))
+    xd = dev(x, torch.bfloat16)
+    geo = sb.ConvGeometry(R, R, 1, pad)
+    want = oracle.conv2d(oracle.compress(Wt, mask, V), x, R, R, 1, pad)
+    got = sb.conv2d(wp, xd, geo).cpu().numpy()
+    assert oracle.rel_frobenius(got, want) <= TOL
+    base = sb.conv2d(w, xd, geo).cpu().numpy()
+    assert oracle.rel_frobenius(got, base) <= TOL
+    # persistent kernel: same bits as one CTA per unit
+    outs = {}
+    for mode in (-1, 2):
+        sb.set_option("persistent", mode)
+        outs[mode] = sb.conv2d(wp, xd, geo).cpu().numpy()
+    sb.set_option("persistent", 0)
+    assert np.array_equal(outs[2], outs[-1])
+    # CUDA-core path over the conv-ordered layout (pads inside groups)
+    sb.set_option("force_simt", 1)
+    simt = sb.conv2d(wp, xd, geo).cpu().numpy()
+    sb.set_option("force_simt", 0)
+    assert oracle.rel_frobenius(simt, want) <= TOL
+
+
+def test_spmm_with_conv_ordered_matrix(sb, oracle):
+    """A conv-ordered matrix is still a valid SpMM operand (pads inside
+    groups), on both kernels."""
+    mask, Wt, _ = _conv_setup(oracle, 32, 4, 4, 128, 3, 3, 64, 16)
+    B = oracle.round16(oracle.random_dense(32 * 9, 256, 77))
+    w = sb.compress_shflbw(dev(Wt), dev(mask), 64)
+    wp = sb.conv_prepare(w, 3)
+    want = oracle.spmm(oracle.compress(Wt, mask, 64), B)
+    Bd = dev(B, torch.bfloat16)
+    assert oracle.rel_frobenius(sb.spmm_execute(wp, Bd).cpu().numpy(), want) <= TOL
+    sb.set_option("force_simt", 1)
+    got = sb.spmm_execute(wp, Bd).cpu().numpy()
+    sb.set_option("force_simt", 0)
+    assert oracle.rel_frobenius(got, want) <= TOL
+
+
+@pytest.mark.parametrize("prepared", [False, True])
+def test_conv_ksplit(sb, oracle, prepared):
+    """Conv with its K blocks split over a 2- or 4-CTA cluster (DSMEM
+    reduction in K-rank order): deterministic and within tolerance, for both
+    activation-row layouts."""
+    C, H, Kf, R, pad, V, Nb = 64, 10, 128, 3, 1, 64, 32
+    mask, Wt, x = _conv_setup(oracle, C, H, H, Kf, R, R, V, Nb, seed=11)
+    w = sb.compress_shflbw(dev(Wt), dev(mask), V)
+    if prepared:
+        w = sb.conv_prepare(w, R)
+    xd = dev(x, torch.bfloat16)
+    geo = sb.ConvGeometry(R, R, 1, pad)
+    want = oracle.conv2d(oracle.compress(Wt, mask, V), x, R, R, 1, pad)
+    for split in (1, 2, 4):
+        sb.set_option("split", split)
+        a1 = sb.conv2d(w, xd, geo).cpu().numpy()
+        a2 = sb.conv2d(w, xd, geo).cpu().numpy()
+        assert np.array_equal(a1, a2)
+        assert oracle.rel_frobenius(a1, want) <= TOL, split
+    sb.set_option("split", 0)
