@@ -34,7 +34,10 @@ enum shflbw_status {
     SHFLBW_BAD_PARAMS = 3,         /* shflbw::BadParams         */
     SHFLBW_BAD_GEOMETRY = 4,       /* shflbw::BadGeometry       */
     SHFLBW_CUDA_ERROR = 5,         /* shflbw::Error (runtime)   */
-    SHFLBW_UNSUPPORTED = 6         /* shflbw::Error (no kernel for this case) */
+    SHFLBW_UNSUPPORTED = 6,        /* shflbw::Error (no kernel for this case) */
+    SHFLBW_BAD_MAGIC = 7,          /* shflbw::BadMagic          (SMX1 container) */
+    SHFLBW_UNSUPPORTED_VERSION = 8,/* shflbw::UnsupportedVersion (SMX1 container) */
+    SHFLBW_CORRUPT_PAYLOAD = 9     /* shflbw::CorruptPayload    (SMX1 container) */
 };
 
 enum shflbw_dtype { SHFLBW_F32 = 0, SHFLBW_BF16 = 1, SHFLBW_F16 = 2 };
@@ -207,6 +210,25 @@ int shflbw_cu_conv_prepare(const shflbw_cu_matrix* w, int32_t S, shflbw_cu_matri
  * over the folded input order, W[:, producer_rows]).  Synchronises `stream`. */
 int shflbw_cu_fold_input_permutation(shflbw_cu_matrix* a, const int32_t* producer_rows,
                                      shflbw_stream_t stream);
+
+/* ---- SMX1 container <-> device layout (the reference's
+ *      on-disk format, include/shflbw/container.hpp:14-22) ------------------ */
+
+/* bytes [host] = a whole SMX1 file.  Kind 3 (Shfl-BW): validated with the
+ * reference's rules (decode_container + as_shflbw, src/container.cpp:147-215,
+ * :90-134) and uploaded into *out with values rounded to value_dtype (F32
+ * keeps them exact).  BAD_MAGIC / UNSUPPORTED_VERSION / CORRUPT_PAYLOAD as the
+ * reference; another valid kind (0, 1, 2, 4) -> BAD_PARAMS without walking its
+ * payload.  Synchronises `stream`. */
+int shflbw_cu_smx1_decode(const void* bytes, uint64_t nbytes, int32_t value_dtype,
+                          shflbw_cu_matrix* out, shflbw_stream_t stream);
+/* *m -> SMX1 kind-3 bytes (encode_container, src/container.cpp:141-145):
+ * *nbytes = the file size; bytes [host] == NULL is a size query.  Values are
+ * written as f32 (exact widening of bf16/f16), so a matrix decoded with F32
+ * values re-encodes byte-identically.  Folded / conv-ordered matrices:
+ * BAD_PARAMS.  Synchronises `stream`. */
+int shflbw_cu_smx1_encode(const shflbw_cu_matrix* m, void* bytes, uint64_t capacity,
+                          uint64_t* nbytes, shflbw_stream_t stream);
 
 /* C[row_indices[r]][:] = C_perm[r][:] for r < M (2- or 4-byte elements);
  * rows with row_indices[r] < 0 (padding of an all-gathered buffer) are skipped. */

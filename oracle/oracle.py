@@ -24,7 +24,7 @@ ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libshflbw_ref.so")
 
 STATUS_NAMES = {0: "ok", 1: "ShapeMismatch", 2: "NonConformantMask", 3: "BadParams",
-                4: "BadGeometry", 9: "Error"}
+                4: "BadGeometry", 7: "BadMagic", 8: "UnsupportedVersion", 9: "CorruptPayload", 99: "Error"}
 
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
@@ -425,6 +425,123 @@ class Reference(_Backend):
     def free_prebuilt(self, ha, hb) -> None:
         self.lib.ref_matrix_free(ha)
         self.lib.ref_dense_free(hb)
+
+    # SMX1 container (src/container.cpp)
+    def smx1_encode(self, a: Packed) -> bytes:
+        size = C.c_size_t(0)
+        f = self.lib.ref_smx1_encode_shflbw
+        args = [a.M, a.K, a.V, _nz(a.row_indices).ctypes.data, _nz(a.group_ncols).ctypes.data,
+                _nz(a.cols).ctypes.data, _nz(a.values).ctypes.data]
+        f.argtypes = [C.c_uint32] * 3 + [C.c_void_p] * 5 + [C.c_size_t, C.POINTER(C.c_size_t)]
+        self._check(f(*args, None, 0, C.byref(size)))
+        out = np.zeros(size.value, np.uint8)
+        self._check(f(*args, out.ctypes.data, size.value, C.byref(size)))
+        return out.tobytes()
+
+    def smx1_encode_dense(self, d: np.ndarray) -> bytes:
+        d = np.ascontiguousarray(d, np.float32)
+        size = C.c_size_t(0)
+        f = self.lib.ref_smx1_encode_dense
+        f.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]
+        self._check(f(d.shape[0], d.shape[1], _nz(d).ctypes.data, None, 0, C.byref(size)))
+        out = np.zeros(size.value, np.uint8)
+        self._check(f(d.shape[0], d.shape[1], _nz(d).ctypes.data, out.ctypes.data, size.value, C.byref(size)))
+        return out.tobytes()
+
+    def smx1_decode(self, b: bytes) -> tuple[int, "Packed | None"]:
+        f = self.lib.ref_smx1_decode_shflbw
+        f.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p] + [C.c_void_p] * 4
+        buf = np.frombuffer(b, np.uint8).copy() if len(b) else np.zeros(1, np.uint8)
+        hdr = np.zeros(5, np.uint32)
+        st = f(buf.ctypes.data, len(b), hdr.ctypes.data, None, None, None, None)
+        if st:
+            return st, None
+        M, K, V, G, T = (int(x) for x in hdr)
+        ri, gn = np.zeros(max(M, 1), np.uint32), np.zeros(max(G, 1), np.uint32)
+        cols, vals = np.zeros(max(T, 1), np.uint32), np.zeros(max(T * V, 1), np.float32)
+        st = f(buf.ctypes.data, len(b), hdr.ctypes.data, ri.ctypes.data, gn.ctypes.data, cols.ctypes.data,
+               vals.ctypes.data)
+        return st, Packed(M, K, V, ri[:M], gn[:G], cols[:T], vals[:T * V])
+
+
+# --------------------------------------------------------------------------
+# SMX1 container, kind 3 (Shfl-BW) -- restatement of the reference's byte
+# format (include/shflbw/container.hpp:14-22, src/container.cpp): header
+# "SMX1", u32 version = 1, kind, M, K, V, G (src/container.cpp:71-80); kind 3
+# payload = M u32 row_indices, then per group u32 n_g, n_g u32 columns,
+# V*n_g f32 values (src/container.cpp:82-88, :141-145); all little-endian.
+
+SMX1_MAGIC = b"SMX1"
+
+
+def smx1_encode(p: Packed) -> bytes:
+    """encode_container(ShflBWMatrix) (src/container.cpp:141-145)."""
+    G = p.G
+    parts = [SMX1_MAGIC, np.array([1, 3, p.M, p.K, p.V, G], "<u4").tobytes(),
+             np.asarray(p.row_indices, "<u4").tobytes()]
+    off = 0
+    for g in range(G):
+        n = int(p.group_ncols[g])
+        parts.append(np.array([n], "<u4").tobytes())
+        parts.append(np.asarray(p.cols[off:off + n], "<u4").tobytes())
+        parts.append(np.asarray(p.values[off * p.V:(off + n) * p.V], "<f4").tobytes())
+        off += n
+    return b"".join(parts)
+
+
+def smx1_decode(b: bytes) -> tuple[int, "Packed | None"]:
+    """decode_container + as_shflbw (src/container.cpp:147-215, :90-124,
+    :126-134): (status, matrix).  Status codes as include/shflbw_cu.h:
+    3 BadParams (another kind), 7 BadMagic, 8 UnsupportedVersion,
+    9 CorruptPayload.  Only kind 3 payloads are walked; other valid kinds
+    decode in the reference and then fail as_shflbw with BadParams."""
+    if len(b) < 4 or b[:4] != SMX1_MAGIC:
+        return 7, None
+    pos = 4
+
+    def u32s(n):
+        nonlocal pos
+        if n > (len(b) - pos) // 4:
+            raise ValueError
+        v = np.frombuffer(b, "<u4", n, pos).astype(np.uint32)
+        pos += 4 * n
+        return v
+    try:
+        version = int(u32s(1)[0])
+        if version != 1:
+            return 8, None
+        kind, M, K, V, G = (int(x) for x in u32s(5))
+        if kind in (0, 1, 2, 4):
+            return 3, None
+        if kind != 3:
+            return 9, None
+        ri = u32s(M)
+        seen = np.zeros(M, bool)
+        if np.any(ri >= M):
+            return 9, None
+        seen[ri] = True
+        if not seen.all():
+            return 9, None
+        if V == 0 or V * G != M:
+            return 9, None
+        gn, cols, vals = [], [], []
+        for _ in range(G):
+            n = int(u32s(1)[0])
+            if n > K:
+                return 9, None
+            c = u32s(n)
+            if n and (np.any(c >= K) or np.any(np.diff(c.astype(np.int64)) <= 0)):
+                return 9, None
+            gn.append(n)
+            cols.append(c)
+            vals.append(u32s(n * V).view(np.float32))
+        if pos != len(b):
+            return 9, None
+    except ValueError:
+        return 9, None
+    return 0, Packed(M, K, V, ri.copy(), np.array(gn, np.uint32),
+                     np.concatenate(cols).astype(np.uint32) if cols else np.zeros(0, np.uint32),
+                     np.concatenate(vals).astype(np.float32) if vals else np.zeros(0, np.float32))
 
 
 def _nz(a: np.ndarray) -> np.ndarray:

@@ -2,20 +2,22 @@
 //
 // TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together
 // with the reference's own sources where they lie
-// (/root/reference/proj/src/{matrix,formats,spmm,rng}.cpp) into
+// (/root/reference/proj/src/{matrix,formats,spmm,rng,container}.cpp) into
 // oracle/_ref/libshflbw_ref.so.  It is used (a) to generate and re-check the
 // golden fixtures under tests/golden/, (b) to pin the C restatement in
 // oracle/shflbw_oracle.c, and (c) as bench.py's `--impl reference` arm (the
 // reference's own CPU spmm_execute / conv2d, all host threads).
 //
-// Flat array conventions follow oracle/shflbw_oracle.h.  Return codes:
-// 0 ok, 1 ShapeMismatch, 2 NonConformantMask, 3 BadParams, 4 BadGeometry,
-// 9 other shflbw::Error.
+// Flat array conventions follow oracle/shflbw_oracle.h.  Return codes (the
+// library's, include/shflbw_cu.h): 0 ok, 1 ShapeMismatch, 2 NonConformantMask,
+// 3 BadParams, 4 BadGeometry, 7 BadMagic, 8 UnsupportedVersion,
+// 9 CorruptPayload, 99 other shflbw::Error.
 #include <cstdint>
 #include <cstring>
 #include <random>
 #include <vector>
 
+#include "shflbw/container.hpp"
 #include "shflbw/formats.hpp"
 #include "shflbw/rng.hpp"
 #include "shflbw/spmm.hpp"
@@ -44,9 +46,18 @@ int guarded(F&& f) {
     } catch (const BadGeometry& e) {
         g_last_error = e.what();
         return 4;
-    } catch (const Error& e) {
+    } catch (const BadMagic& e) {
+        g_last_error = e.what();
+        return 7;
+    } catch (const UnsupportedVersion& e) {
+        g_last_error = e.what();
+        return 8;
+    } catch (const CorruptPayload& e) {
         g_last_error = e.what();
         return 9;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return 99;
     }
 }
 
@@ -225,6 +236,55 @@ int ref_stitch_to_blockwise(uint32_t K, uint32_t V, uint32_t G, const uint32_t* 
                 tile_group[n++] = g;
             }
         *ntiles = n;
+    });
+}
+
+// SMX1 container (src/container.cpp): encode a kind-3 (Shfl-BW) matrix;
+// *size = byte count, bytes copied when out != NULL and cap suffices.
+int ref_smx1_encode_shflbw(uint32_t M, uint32_t K, uint32_t V, const uint32_t* row_indices,
+                           const uint32_t* group_ncols, const uint32_t* cols, const float* values, uint8_t* out,
+                           size_t cap, size_t* size) {
+    return guarded([&] {
+        const auto bytes = encode_container(AnyMatrix(build(M, K, V, row_indices, group_ncols, cols, values)));
+        *size = bytes.size();
+        if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+    });
+}
+
+// decode_container + as_shflbw: hdr = {M, K, V, G, total columns}; the arrays
+// are filled when non-NULL (sized from a first call with NULLs).
+int ref_smx1_decode_shflbw(const uint8_t* bytes, size_t n, uint32_t* hdr, uint32_t* row_indices,
+                           uint32_t* group_ncols, uint32_t* cols, float* values) {
+    return guarded([&] {
+        const auto any = decode_container(std::vector<uint8_t>(bytes, bytes + n));
+        const ShflBWMatrix& a = as_shflbw(any);
+        const uint32_t V = a.core.vector_size, G = static_cast<uint32_t>(a.core.groups.size());
+        size_t total = 0;
+        for (const auto& g : a.core.groups) total += g.cols.size();
+        hdr[0] = a.core.rows;
+        hdr[1] = a.core.cols;
+        hdr[2] = V;
+        hdr[3] = G;
+        hdr[4] = static_cast<uint32_t>(total);
+        if (!row_indices) return;
+        std::memcpy(row_indices, a.row_indices.data(), sizeof(uint32_t) * a.row_indices.size());
+        size_t off = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            const auto& grp = a.core.groups[g];
+            group_ncols[g] = static_cast<uint32_t>(grp.cols.size());
+            std::memcpy(cols + off, grp.cols.data(), sizeof(uint32_t) * grp.cols.size());
+            std::memcpy(values + off * V, grp.values.data(), sizeof(float) * grp.values.size());
+            off += grp.cols.size();
+        }
+    });
+}
+
+// a valid kind-0 (dense) container, for the kind-mismatch case
+int ref_smx1_encode_dense(uint32_t rows, uint32_t cols, const float* v, uint8_t* out, size_t cap, size_t* size) {
+    return guarded([&] {
+        const auto bytes = encode_container(AnyMatrix(DenseMatrix(rows, cols, std::vector<float>(v, v + size_t(rows) * cols))));
+        *size = bytes.size();
+        if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
     });
 }
 

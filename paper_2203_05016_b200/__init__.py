@@ -6,12 +6,14 @@ and the reference-compatible C++ API of ``include/shflbw/``.  This Python
 package is a thin host mirror of the reference interface over that ABI
 (``shflbw``) plus the multi-GPU row-group sharding (``sharded``).
 """
-from .shflbw import (BadGeometry, BadParams, ConvGeometry, Error, NonConformantMask, ShapeMismatch,
+from .shflbw import (BadGeometry, BadMagic, BadParams, ConvGeometry, CorruptPayload, Error, NonConformantMask,
+                     ShapeMismatch, UnsupportedVersion, smx1_dump, smx1_dumps, smx1_load, smx1_loads,
                      ShflBWMatrix, TileConfig, compress_shflbw, conv2d, conv_output_size, conv_prepare,
                      decompress, fold_input_permutation, launch_count, set_option, spmm_execute, spmm_groups,
                      unpermute_rows, upload, validate_pattern)
 
-__all__ = ["BadGeometry", "BadParams", "ConvGeometry", "Error", "NonConformantMask", "ShapeMismatch",
+__all__ = ["BadGeometry", "BadMagic", "BadParams", "ConvGeometry", "CorruptPayload", "Error", "NonConformantMask",
+           "ShapeMismatch", "UnsupportedVersion", "smx1_dump", "smx1_dumps", "smx1_load", "smx1_loads",
            "ShflBWMatrix", "TileConfig", "compress_shflbw", "conv2d", "conv_output_size", "conv_prepare",
            "decompress",
            "fold_input_permutation", "launch_count", "set_option", "spmm_execute", "spmm_groups",

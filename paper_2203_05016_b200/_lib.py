@@ -12,7 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libshflbw_b200.so")
 
-OK, SHAPE_MISMATCH, NONCONFORMANT_MASK, BAD_PARAMS, BAD_GEOMETRY, CUDA_ERROR, UNSUPPORTED = range(7)
+(OK, SHAPE_MISMATCH, NONCONFORMANT_MASK, BAD_PARAMS, BAD_GEOMETRY, CUDA_ERROR, UNSUPPORTED, BAD_MAGIC,
+ UNSUPPORTED_VERSION, CORRUPT_PAYLOAD) = range(10)
 F32, BF16, F16 = 0, 1, 2
 PAD_COLUMN = -1
 K_TILE = 64
@@ -53,6 +54,8 @@ SIGNATURES = {
     "shflbw_cu_spmm_groups": (C.c_int, [C.POINTER(CuMatrix), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                         C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                         C.c_void_p]),
+    "shflbw_cu_smx1_decode": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p]),
+    "shflbw_cu_smx1_encode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
     "shflbw_cu_conv_prepare": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "shflbw_cu_fold_input_permutation": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "shflbw_cu_unpermute_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,

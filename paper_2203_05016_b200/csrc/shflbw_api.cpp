@@ -38,6 +38,9 @@ shflbw_stream_t sstream() { return reinterpret_cast<shflbw_stream_t>(cudaStreamP
         case SHFLBW_NONCONFORMANT_MASK: throw NonConformantMask(msg);
         case SHFLBW_BAD_PARAMS: throw BadParams(msg);
         case SHFLBW_BAD_GEOMETRY: throw BadGeometry(msg);
+        case SHFLBW_BAD_MAGIC: throw BadMagic(msg);
+        case SHFLBW_UNSUPPORTED_VERSION: throw UnsupportedVersion(msg);
+        case SHFLBW_CORRUPT_PAYLOAD: throw CorruptPayload(msg);
         default: throw Error(msg);
     }
 }

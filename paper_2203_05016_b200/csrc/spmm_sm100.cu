@@ -155,7 +155,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     //      DSMEM;
     //   0  auto (default): an explicit "split" means V split; otherwise, when
     //      4 CTAs per unit fit on the GPU, by the widest group's K blocks
-    //      (measured): >= 24 -> K split by 4, >= 8 (V >= 64) ->
+    //      (measured): >= 24 -> K split by 4, >= 8 (V == 64) ->
     //      2 x 2, else V split.
     const int min_kb = 2;  // K blocks per CTA worth splitting for
     const int kb_all = (a->cols + kBlockK - 1) / kBlockK;
@@ -170,7 +170,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
             if (kb_grp >= 24) {
                 mode = 1;
                 cs = 4;
-            } else if (kb_grp >= 8 && V >= 64) {
+            } else if (kb_grp >= 8 && V == 64) {
                 mode = 2;
             }
         }

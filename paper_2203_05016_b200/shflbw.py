@@ -46,8 +46,21 @@ class BadGeometry(Error):
     pass
 
 
+class BadMagic(Error):
+    """Container errors (include/shflbw/errors.hpp:29-40)."""
+
+
+class UnsupportedVersion(Error):
+    pass
+
+
+class CorruptPayload(Error):
+    pass
+
+
 _ERRORS = {L.SHAPE_MISMATCH: ShapeMismatch, L.NONCONFORMANT_MASK: NonConformantMask,
-           L.BAD_PARAMS: BadParams, L.BAD_GEOMETRY: BadGeometry}
+           L.BAD_PARAMS: BadParams, L.BAD_GEOMETRY: BadGeometry, L.BAD_MAGIC: BadMagic,
+           L.UNSUPPORTED_VERSION: UnsupportedVersion, L.CORRUPT_PAYLOAD: CorruptPayload}
 
 
 def _lib():
@@ -275,6 +288,39 @@ def spmm_execute(a: ShflBWMatrix, b: torch.Tensor, cfg: TileConfig | None = None
     if st:
         _check(st)
     return out
+
+
+def smx1_loads(data: bytes, dtype: torch.dtype = torch.bfloat16) -> ShflBWMatrix:
+    """An SMX1 kind-3 container (the reference's file format,
+    include/shflbw/container.hpp:14-22) straight into the device layout;
+    the reference's validation rules and error classes (BadMagic,
+    UnsupportedVersion, CorruptPayload; BadParams for another kind)."""
+    buf = (C.c_uint8 * max(len(data), 1)).from_buffer_copy(bytes(data) or b"\0")
+    cm = L.CuMatrix()
+    _check(_lib().shflbw_cu_smx1_decode(buf, len(data), _dt(dtype), C.byref(cm), _stream()))
+    return ShflBWMatrix(cm)
+
+
+def smx1_load(path, dtype: torch.dtype = torch.bfloat16) -> ShflBWMatrix:
+    """read_container(path) + as_shflbw, into the device layout."""
+    with open(path, "rb") as f:
+        return smx1_loads(f.read(), dtype)
+
+
+def smx1_dumps(a: ShflBWMatrix) -> bytes:
+    """encode_container(ShflBWMatrix) of a device matrix (values widened to
+    f32, so an F32 matrix round-trips byte-identically)."""
+    n = C.c_uint64(0)
+    _check(_lib().shflbw_cu_smx1_encode(a.ptr, None, 0, C.byref(n), _stream()))
+    buf = (C.c_uint8 * max(n.value, 1))()
+    _check(_lib().shflbw_cu_smx1_encode(a.ptr, buf, n.value, C.byref(n), _stream()))
+    return bytes(buf[: n.value])
+
+
+def smx1_dump(a: ShflBWMatrix, path) -> None:
+    """write_container(ShflBWMatrix, path)."""
+    with open(path, "wb") as f:
+        f.write(smx1_dumps(a))
 
 
 def conv_prepare(w: ShflBWMatrix, geo: "ConvGeometry | int") -> ShflBWMatrix:

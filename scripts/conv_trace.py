@@ -22,6 +22,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="conv56")
 ap.add_argument("--opts", default="")
 ap.add_argument("--chain", type=int, default=4)
+ap.add_argument("--prepared", action="store_true")
+ap.add_argument("--persist", action="store_true")
 args = ap.parse_args()
 
 C, H, Kf, R, pad, Nb, V, alpha = CONV[args.workload]
@@ -30,6 +32,8 @@ crs = C * R * R
 mask = torch.from_numpy(bench.synth_mask(Kf, crs, V, int(round(alpha * crs)), 1234)).to(dev)
 nset = max(1, args.chain)
 ws = [sb.compress_shflbw(bench.uniform_bf16(torch, (Kf, crs), 100 + i, dev), mask, V) for i in range(nset)]
+if args.prepared:
+    ws = [sb.conv_prepare(w, R) for w in ws]
 xs = [bench.uniform_bf16(torch, (C, H, H, Nb), 300 + i, dev) for i in range(nset)]
 P = H + 2 * pad - R + 1
 outs = [torch.empty((Kf, P, P, Nb), dtype=torch.bfloat16, device=dev) for _ in range(nset)]
@@ -65,3 +69,14 @@ for e, nm in enumerate(names):
 d = rel[:, 7] - rel[:, 0]
 print(f"  CTA lifetime p50 {np.median(d):.2f} us, max {d.max():.2f}; first_full-dep {np.median(rel[:, 3] - rel[:, 2]):.2f}; "
       f"full[k+1]-full[k] p50 {np.median(rel[:, 9] - rel[:, 8]):.2f}; accum->exit p50 {np.median(rel[:, 7] - rel[:, 5]):.2f}")
+
+if args.persist:
+    dep = rel[:, 2]
+    print("  per unit i (median over CTAs, us after the CTA's dependency wait): gathers start / MMA start / "
+          "accumulated")
+    for i in range(8):
+        ok = t[:, 24 + i] > 0
+        if ok.sum() == 0:
+            break
+        cols = [rel[:, 16 + i] - dep, rel[:, 8 + i] - dep, rel[:, 24 + i] - dep]
+        print(f"  unit {i}: " + "  ".join(f"{np.median(c[ok]):7.2f}" for c in cols) + f"   ({ok.sum()} CTAs)")

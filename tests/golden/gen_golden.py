@@ -257,6 +257,47 @@ def full_size(ref: Reference) -> list[dict]:
     return out
 
 
+def smx1_cases(ref: Reference) -> list[dict]:
+    """SMX1 kind-3 containers written by the reference's encode_container
+    (src/container.cpp:141-145) and the statuses its decode_container +
+    as_shflbw give for valid and corrupted files (src/container.cpp:147-215)."""
+    out = []
+    for name, m, k, v, cpg, mseed, dseed in [("small", 64, 96, 8, 24, 3, 4), ("v1", 12, 10, 1, 3, 5, 6),
+                                           ("empty_groups", 32, 40, 16, 0, 7, 8), ("v64", 128, 96, 64, 20, 9, 10),
+                                           ("tiny", 16, 12, 4, 3, 12, 13)]:
+        mask = ref.random_shflbw_mask(m, k, v, cpg, ref.rng(mseed))
+        p = ref.compress(ref.random_dense(m, k, dseed), mask, v)
+        b = ref.smx1_encode(p)
+        out.append({"name": name, "M": m, "K": k, "V": v, "cpg": cpg, "mask_seed": mseed, "dense_seed": dseed,
+                    "hex": b.hex(), "status": ref.smx1_decode(b)[0]})
+    base = bytes.fromhex(out[-1]["hex"])  # the tiny matrix
+    M, V, K = 16, 4, 12
+    ri_off = 28
+    g0 = ri_off + 4 * M  # first group record
+    def patch(b, off, val):
+        return b[:off] + int(val).to_bytes(4, "little") + b[off + 4:]
+    bad = {
+        "bad_magic": b"SMX2" + base[4:],
+        "short_magic": base[:3],
+        "version_2": patch(base, 4, 2),
+        "truncated_header": base[:20],
+        "truncated_payload": base[:-3],
+        "trailing_byte": base + b"\0",
+        "unknown_kind": patch(base, 8, 7),
+        "dense_kind": ref.smx1_encode_dense(ref.random_dense(3, 5, 11)),
+        "row_indices_duplicate": patch(base, ri_off + 4, int.from_bytes(base[ri_off:ri_off + 4], "little")),
+        "row_index_out_of_range": patch(base, ri_off, M),
+        "vg_mismatch": patch(base, 24, M // V + 1),
+        "v_zero": patch(base, 20, 0),
+        "ncols_exceeds_k": patch(base, g0, K + 1),
+        "col_out_of_range": patch(base, g0 + 4, K),
+        "cols_not_increasing": patch(base, g0 + 8, int.from_bytes(base[g0 + 4:g0 + 8], "little")),
+    }
+    for name, b in bad.items():
+        out.append({"name": name, "hex": b.hex(), "status": ref.smx1_decode(b)[0]})
+    return out
+
+
 def main() -> None:
     ref = Reference()
     files = {
@@ -265,7 +306,10 @@ def main() -> None:
         "spmm_random.json": spmm_random(ref),
         "conv_cases.json": conv_cases(ref),
         "full_size.json": full_size(ref),
+        "smx1_cases.json": smx1_cases(ref),
     }
+    only = sys.argv[1:]
+    files = {k: v for k, v in files.items() if not only or k in only}
     for name, obj in files.items():
         with open(os.path.join(HERE, name), "w") as f:
             json.dump({"generator": "tests/golden/gen_golden.py (reference: oracle/_ref)",

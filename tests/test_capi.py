@@ -79,3 +79,21 @@ def test_compute_fails_loudly_without_gpu(lib):
     # argument checks come first and keep the reference's error classes
     assert lib.shflbw_cu_compress(None, 0, None, 4, 4, 3, 1, C.byref(m), C.byref(fr), None) == L.BAD_PARAMS
     assert lib.shflbw_cu_spmm(None, None, 0, 0, 0, None, 0, 0, None) == L.BAD_PARAMS
+
+
+def test_smx1_decode_rejects_like_the_reference_without_gpu(lib):
+    """Every corrupted SMX1 container of tests/golden/smx1_cases.json gets the
+    reference's status from the library's host-side validation (before any
+    device work); a valid file then needs the GPU."""
+    import json
+    from paper_2203_05016_b200 import _lib as L
+    cases = json.load(open(os.path.join(ROOT, "tests", "golden", "smx1_cases.json")))["cases"]
+    for c in cases:
+        data = bytes.fromhex(c["hex"])
+        buf = (C.c_uint8 * max(len(data), 1)).from_buffer_copy(data or b"\0")
+        m = L.CuMatrix()
+        st = lib.shflbw_cu_smx1_decode(buf, len(data), L.BF16, C.byref(m), None)
+        if c["status"] == 0:
+            assert st in (L.OK, L.CUDA_ERROR), c["name"]
+        else:
+            assert st == c["status"], (c["name"], st, c["status"])

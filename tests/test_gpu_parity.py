@@ -713,3 +713,54 @@ def test_conv_ksplit(sb, oracle, prepared):
         assert np.array_equal(a1, a2)
         assert oracle.rel_frobenius(a1, want) <= TOL, split
     sb.set_option("split", 0)
+
+
+# ---------------------------------------------- SMX1 container <-> device (§8 f1)
+
+@pytest.mark.parametrize("case", [c for c in load_golden("smx1_cases.json") if "M" in c], ids=lambda c: c["name"])
+def test_smx1_load_store(sb, oracle, case):
+    """Reference-written SMX1 files load straight into the device layout
+    (== the oracle's packing of the same matrix), re-encode byte-identically
+    with F32 values and to the bf16-rounded file with bf16 values, and
+    compute exactly what compress_shflbw's matrix computes."""
+    from oracle import smx1_encode
+    data = bytes.fromhex(case["hex"])
+    mask = oracle.random_shflbw_mask(case["M"], case["K"], case["V"], case["cpg"], oracle.rng(case["mask_seed"]))
+    dense = oracle.random_dense(case["M"], case["K"], case["dense_seed"])
+    p = oracle.compress(dense, mask, case["V"])
+    a32 = sb.smx1_loads(data, torch.float32)
+    assert sb.smx1_dumps(a32) == data
+    ri, gn, cols, vals = a32.to_host()
+    assert np.array_equal(ri, p.row_indices) and np.array_equal(gn, p.group_ncols)
+    assert np.array_equal(cols, p.cols) and np.array_equal(vals.view(np.uint32), p.values.view(np.uint32))
+    a16 = sb.smx1_loads(data)  # bf16 values
+    gp, ci, vv = a16.raw()
+    egp, eci, evv = oracle.pack_device(p, 64, "bf16")
+    assert np.array_equal(gp, egp) and np.array_equal(ci, eci) and np.array_equal(vv, evv)
+    p16 = type(p)(p.M, p.K, p.V, p.row_indices, p.group_ncols, p.cols, oracle.round16(p.values))
+    assert sb.smx1_dumps(a16) == smx1_encode(p16)
+    # same device matrix as the converter's: identical SpMM bits
+    if case["V"] in (16, 32, 64, 128):
+        B = oracle.round16(oracle.random_dense(case["K"], 256, 3))
+        ac = sb.compress_shflbw(dev(oracle.round16(dense)), dev(mask), case["V"])
+        assert np.array_equal(sb.spmm_execute(a16, dev(B, torch.bfloat16)).cpu().numpy(),
+                              sb.spmm_execute(ac, dev(B, torch.bfloat16)).cpu().numpy())
+
+
+def test_smx1_errors_and_files(sb, oracle, tmp_path):
+    errs = {7: sb.BadMagic, 8: sb.UnsupportedVersion, 9: sb.CorruptPayload, 3: sb.BadParams}
+    for c in load_golden("smx1_cases.json"):
+        if c["status"]:
+            with pytest.raises(errs[c["status"]]):
+                sb.smx1_loads(bytes.fromhex(c["hex"]))
+    mask = oracle.random_shflbw_mask(128, 64, 32, 20, oracle.rng(1))
+    W = oracle.random_dense(128, 64, 2)
+    a = sb.compress_shflbw(dev(W), dev(mask), 32, dtype=torch.float32)
+    path = tmp_path / "w.smx1"
+    sb.smx1_dump(a, path)
+    from oracle import smx1_encode
+    assert path.read_bytes() == smx1_encode(oracle.compress(W, mask, 32))
+    b = sb.smx1_load(path, torch.float32)
+    assert sb.smx1_dumps(b) == path.read_bytes()
+    with pytest.raises(sb.BadParams):  # conv-ordered layouts are not the reference's format
+        sb.smx1_dumps(sb.conv_prepare(a, 4))

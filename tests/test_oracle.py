@@ -248,3 +248,48 @@ def test_bf16_rounding_rne(oracle):
     # 1 + 2^-8 is a tie -> even (1.0); 1 + 3*2^-8 is a tie -> 1 + 2^-6
     y = oracle.round16(x)
     assert y[0] == 1.0 and y[1] == 1.0 and y[2] == np.float32(1.015625) and y[3] == -2.5
+
+
+# ---------------------------------------------------------------- SMX1 container
+
+def _smx1_source(oracle, c):
+    mask = oracle.random_shflbw_mask(c["M"], c["K"], c["V"], c["cpg"], oracle.rng(c["mask_seed"]))
+    return oracle.compress(oracle.random_dense(c["M"], c["K"], c["dense_seed"]), mask, c["V"])
+
+
+def test_smx1_restatement_matches_reference_bytes(oracle):
+    """oracle.smx1_encode / smx1_decode (the kind-3 byte format restated)
+    against containers written by the reference's encode_container and the
+    statuses its decode_container + as_shflbw return."""
+    from oracle import smx1_decode, smx1_encode
+    for c in load_golden("smx1_cases.json"):
+        data = bytes.fromhex(c["hex"])
+        st, p = smx1_decode(data)
+        assert st == c["status"], c["name"]
+        if "M" in c:
+            src = _smx1_source(oracle, c)
+            assert smx1_encode(src) == data, c["name"]
+            assert np.array_equal(p.row_indices, src.row_indices) and np.array_equal(p.cols, src.cols)
+            assert np.array_equal(p.values.view(np.uint32), src.values.view(np.uint32))
+
+
+def test_smx1_restatement_vs_reference_fuzz(oracle, reference):
+    """Random valid and single-word-corrupted containers: identical status
+    and contents from the restatement and the compiled reference."""
+    from oracle import smx1_decode
+    rs = np.random.RandomState(5)
+    for t in range(60):
+        V = int(rs.choice([1, 2, 4, 8]))
+        M, K = V * int(rs.randint(1, 6)), int(rs.randint(1, 40))
+        mask = reference.random_shflbw_mask(M, K, V, int(rs.randint(0, K + 1)), reference.rng(t))
+        data = bytearray(reference.smx1_encode(reference.compress(reference.random_dense(M, K, t), mask, V)))
+        if t % 2:
+            w = int(rs.randint(0, len(data) // 4))
+            data[4 * w:4 * w + 4] = int(rs.randint(0, 2 ** 32)).to_bytes(4, "little")
+        data = bytes(data)
+        s1, p1 = smx1_decode(data)
+        s2, p2 = reference.smx1_decode(data)
+        assert s1 == s2, t
+        if s1 == 0:
+            assert np.array_equal(p1.cols, p2.cols) and np.array_equal(p1.row_indices, p2.row_indices)
+            assert np.array_equal(p1.values.view(np.uint32), p2.values.view(np.uint32))
