@@ -211,6 +211,47 @@ int shflbw_cu_conv_prepare(const shflbw_cu_matrix* w, int32_t S, shflbw_cu_matri
 int shflbw_cu_fold_input_permutation(shflbw_cu_matrix* a, const int32_t* producer_rows,
                                      shflbw_stream_t stream);
 
+/* ---- pruning: the converter's upstream producer (
+ *      include/shflbw/pruning.hpp:27-94, src/pruning.cpp) ------------------
+ * Importance scores are M x K f32 [dev], finite and >= 0 (else BAD_PARAMS,
+ * the ImportanceMatrix ctor, src/pruning.cpp:35-44).  Masks are M x K bytes
+ * [dev] (0/1).  Every result is identical to the reference's: the integer
+ * and index work is exact and every double sum runs in the reference's
+ * order with separately rounded operations. */
+typedef struct shflbw_prune_config {
+    double alpha;              /* target non-zero ratio, (0, 1]             */
+    double beta_factor;        /* beta = min(1, beta_factor * alpha)        */
+    uint32_t v;                /* group size, divides M                     */
+    uint32_t kmeans_max_iters; /* >= 1                                      */
+    uint64_t seed;
+    uint32_t restarts;         /* >= 1                                      */
+    uint32_t reserved;
+} shflbw_prune_config;
+
+/* scores[i] = |w[i]| (importance_scores, src/pruning.cpp:61-66). */
+int shflbw_cu_importance_scores(const float* w, int64_t n, float* scores, shflbw_stream_t stream);
+/* *out = sum of scores where mask (kept_score, src/pruning.cpp:68-75), in the
+ * reference's linear order.  Synchronises `stream`. */
+int shflbw_cu_kept_score(const float* scores, const uint8_t* mask, int32_t M, int32_t K, double* out,
+                         shflbw_stream_t stream);
+/* Top llround(keep_ratio*M*K) entries, ties to the lower linear index
+ * (prune_unstructured, src/pruning.cpp:77-92). */
+int shflbw_cu_prune_unstructured(const float* scores, int32_t M, int32_t K, double keep_ratio,
+                                 uint8_t* mask, shflbw_stream_t stream);
+/* Per group of V consecutive rows, the llround(alpha*K) columns with the
+ * largest score sums (prune_vectorwise, src/pruning.cpp:94-121). */
+int shflbw_cu_prune_vectorwise(const float* scores, int32_t M, int32_t K, uint32_t V, double alpha,
+                               uint8_t* mask, shflbw_stream_t stream);
+/* Balanced K-Means row grouping of `mask` with `restarts` seeds, scored by
+ * the vector-wise prune of the permuted scores (kmeans_row_grouping,
+ * src/pruning.cpp:183-337): order[i] = original row at grouped position i. */
+int shflbw_cu_kmeans_row_grouping(const uint8_t* mask, const float* scores, int32_t M, int32_t K,
+                                  const shflbw_prune_config* cfg, uint32_t* order, shflbw_stream_t stream);
+/* prune_shflbw (src/pruning.cpp:339-362): mask [dev] M x K, permutation
+ * [dev] M, *kept_score.  Synchronises `stream`. */
+int shflbw_cu_prune_shflbw(const float* scores, int32_t M, int32_t K, const shflbw_prune_config* cfg,
+                           uint8_t* mask, uint32_t* permutation, double* kept_score, shflbw_stream_t stream);
+
 /* ---- SMX1 container <-> device layout (the reference's
  *      on-disk format, include/shflbw/container.hpp:14-22) ------------------ */
 

@@ -426,6 +426,58 @@ class Reference(_Backend):
         self.lib.ref_matrix_free(ha)
         self.lib.ref_dense_free(hb)
 
+    # pruning (src/pruning.cpp)
+    def kept_score(self, scores: np.ndarray, mask: np.ndarray) -> float:
+        s = np.ascontiguousarray(scores, np.float32)
+        m = np.ascontiguousarray(mask, np.uint8)
+        out = C.c_double(0.0)
+        f = self.lib.ref_kept_score
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]
+        self._check(f(_nz(s).ctypes.data, _nz(m).ctypes.data, s.shape[0], s.shape[1], C.byref(out)))
+        return out.value
+
+    def prune_unstructured(self, scores: np.ndarray, ratio: float) -> np.ndarray:
+        s = np.ascontiguousarray(scores, np.float32)
+        out = np.zeros(max(s.size, 1), np.uint8)
+        f = self.lib.ref_prune_unstructured
+        f.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_void_p]
+        self._check(f(_nz(s).ctypes.data, s.shape[0], s.shape[1], ratio, out.ctypes.data))
+        return out[: s.size].reshape(s.shape)
+
+    def prune_vectorwise(self, scores: np.ndarray, v: int, alpha: float) -> np.ndarray:
+        s = np.ascontiguousarray(scores, np.float32)
+        out = np.zeros(max(s.size, 1), np.uint8)
+        f = self.lib.ref_prune_vectorwise
+        f.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_void_p]
+        self._check(f(_nz(s).ctypes.data, s.shape[0], s.shape[1], v, alpha, out.ctypes.data))
+        return out[: s.size].reshape(s.shape)
+
+    def kmeans_row_grouping(self, mask: np.ndarray, scores: np.ndarray, cfg: dict) -> np.ndarray:
+        s = np.ascontiguousarray(scores, np.float32)
+        m = np.ascontiguousarray(mask, np.uint8)
+        out = np.zeros(max(s.shape[0], 1), np.uint32)
+        f = self.lib.ref_kmeans_row_grouping
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
+                      C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p]
+        self._check(f(_nz(m).ctypes.data, _nz(s).ctypes.data, s.shape[0], s.shape[1], cfg["alpha"],
+                      cfg["beta_factor"], cfg["v"], cfg["kmeans_max_iters"], cfg["seed"], cfg["restarts"],
+                      out.ctypes.data))
+        return out[: s.shape[0]]
+
+    def prune_shflbw(self, scores: np.ndarray, cfg: dict):
+        """-> (mask u8 [M, K], permutation u32 [M], kept_score)"""
+        s = np.ascontiguousarray(scores, np.float32)
+        mask = np.zeros(max(s.size, 1), np.uint8)
+        perm = np.zeros(max(s.shape[0], 1), np.uint32)
+        kept = C.c_double(0.0)
+        f = self.lib.ref_prune_shflbw
+        f.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_uint32, C.c_uint32,
+                      C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
+        self._check(f(_nz(s).ctypes.data, s.shape[0], s.shape[1], cfg["alpha"], cfg["beta_factor"], cfg["v"],
+                      cfg["kmeans_max_iters"], cfg["seed"], cfg["restarts"], mask.ctypes.data, perm.ctypes.data,
+                      C.byref(kept)))
+        return mask[: s.size].reshape(s.shape), perm[: s.shape[0]], kept.value
+
     # SMX1 container (src/container.cpp)
     def smx1_encode(self, a: Packed) -> bytes:
         size = C.c_size_t(0)

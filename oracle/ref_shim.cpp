@@ -2,7 +2,7 @@
 //
 // TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together
 // with the reference's own sources where they lie
-// (/root/reference/proj/src/{matrix,formats,spmm,rng,container}.cpp) into
+// (/root/reference/proj/src/{matrix,formats,spmm,rng,container,pruning}.cpp) into
 // oracle/_ref/libshflbw_ref.so.  It is used (a) to generate and re-check the
 // golden fixtures under tests/golden/, (b) to pin the C restatement in
 // oracle/shflbw_oracle.c, and (c) as bench.py's `--impl reference` arm (the
@@ -19,6 +19,7 @@
 
 #include "shflbw/container.hpp"
 #include "shflbw/formats.hpp"
+#include "shflbw/pruning.hpp"
 #include "shflbw/rng.hpp"
 #include "shflbw/spmm.hpp"
 #include "test_helpers.hpp"
@@ -285,6 +286,60 @@ int ref_smx1_encode_dense(uint32_t rows, uint32_t cols, const float* v, uint8_t*
         const auto bytes = encode_container(AnyMatrix(DenseMatrix(rows, cols, std::vector<float>(v, v + size_t(rows) * cols))));
         *size = bytes.size();
         if (out && cap >= bytes.size()) std::memcpy(out, bytes.data(), bytes.size());
+    });
+}
+
+// ---- pruning (src/pruning.cpp) ----
+namespace {
+ImportanceMatrix scores_of(const float* s, uint32_t M, uint32_t K) {
+    return ImportanceMatrix(M, K, std::vector<float>(s, s + size_t(M) * K));
+}
+SparsityMask mask_of(const uint8_t* m, uint32_t M, uint32_t K) {
+    return SparsityMask(M, K, std::vector<uint8_t>(m, m + size_t(M) * K));
+}
+PruneConfig cfg_of(double alpha, double beta_factor, uint32_t v, uint32_t iters, uint64_t seed, uint32_t restarts) {
+    PruneConfig c;
+    c.alpha = alpha;
+    c.beta_factor = beta_factor;
+    c.v = v;
+    c.kmeans_max_iters = iters;
+    c.seed = seed;
+    c.restarts = restarts;
+    return c;
+}
+}  // namespace
+
+int ref_kept_score(const float* s, const uint8_t* m, uint32_t M, uint32_t K, double* out) {
+    return guarded([&] { *out = kept_score(scores_of(s, M, K), mask_of(m, M, K)); });
+}
+int ref_prune_unstructured(const float* s, uint32_t M, uint32_t K, double ratio, uint8_t* out) {
+    return guarded([&] {
+        const auto m = prune_unstructured(scores_of(s, M, K), ratio);
+        std::memcpy(out, m.bits.data(), m.bits.size());
+    });
+}
+int ref_prune_vectorwise(const float* s, uint32_t M, uint32_t K, uint32_t v, double alpha, uint8_t* out) {
+    return guarded([&] {
+        const auto m = prune_vectorwise(scores_of(s, M, K), v, alpha);
+        std::memcpy(out, m.bits.data(), m.bits.size());
+    });
+}
+int ref_kmeans_row_grouping(const uint8_t* m, const float* s, uint32_t M, uint32_t K, double alpha,
+                            double beta_factor, uint32_t v, uint32_t iters, uint64_t seed, uint32_t restarts,
+                            uint32_t* order) {
+    return guarded([&] {
+        const auto o = kmeans_row_grouping(mask_of(m, M, K), v, cfg_of(alpha, beta_factor, v, iters, seed, restarts),
+                                           scores_of(s, M, K));
+        std::memcpy(order, o.data(), sizeof(uint32_t) * o.size());
+    });
+}
+int ref_prune_shflbw(const float* s, uint32_t M, uint32_t K, double alpha, double beta_factor, uint32_t v,
+                     uint32_t iters, uint64_t seed, uint32_t restarts, uint8_t* mask, uint32_t* perm, double* kept) {
+    return guarded([&] {
+        const auto r = prune_shflbw(scores_of(s, M, K), cfg_of(alpha, beta_factor, v, iters, seed, restarts));
+        std::memcpy(mask, r.mask.bits.data(), r.mask.bits.size());
+        std::memcpy(perm, r.permutation.data(), sizeof(uint32_t) * r.permutation.size());
+        *kept = r.kept_score;
     });
 }
 

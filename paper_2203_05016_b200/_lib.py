@@ -19,6 +19,13 @@ PAD_COLUMN = -1
 K_TILE = 64
 
 
+class PruneConfigC(C.Structure):
+    """struct shflbw_prune_config"""
+    _fields_ = [("alpha", C.c_double), ("beta_factor", C.c_double), ("v", C.c_uint32),
+                ("kmeans_max_iters", C.c_uint32), ("seed", C.c_uint64), ("restarts", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
 class CuMatrix(C.Structure):
     """struct shflbw_cu_matrix (include/shflbw_cu.h)."""
     _fields_ = [
@@ -54,6 +61,17 @@ SIGNATURES = {
     "shflbw_cu_spmm_groups": (C.c_int, [C.POINTER(CuMatrix), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                         C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                         C.c_void_p]),
+    "shflbw_cu_importance_scores": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "shflbw_cu_kept_score": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                       C.c_void_p]),
+    "shflbw_cu_prune_unstructured": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_void_p,
+                                               C.c_void_p]),
+    "shflbw_cu_prune_vectorwise": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_uint32, C.c_double,
+                                             C.c_void_p, C.c_void_p]),
+    "shflbw_cu_kmeans_row_grouping": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                                C.c_void_p, C.c_void_p]),
+    "shflbw_cu_prune_shflbw": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_double), C.c_void_p]),
     "shflbw_cu_smx1_decode": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p]),
     "shflbw_cu_smx1_encode": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_void_p]),
     "shflbw_cu_conv_prepare": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),

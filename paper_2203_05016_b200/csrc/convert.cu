@@ -588,8 +588,8 @@ int scan_exclusive(const int* in, int* out, int n, int* total_dev, cudaStream_t 
     return SHFLBW_OK;
 }
 
-namespace {
-
+// stable LSD radix sort of (u64 key, u32 value) pairs, ascending by key;
+// keys_tmp / vals_tmp are scratch of n elements (also used by prune.cu)
 int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int n,
                      cudaStream_t s) {
     const int nb = (n + kRadixTile - 1) / kRadixTile;
@@ -612,6 +612,8 @@ int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_
     // 8 passes: result is back in keys / vals
     return SHFLBW_OK;
 }
+
+namespace {
 
 // Steps 1-4 shared by validate and compress.
 struct ClassPlan {

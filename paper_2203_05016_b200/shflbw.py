@@ -290,6 +290,98 @@ def spmm_execute(a: ShflBWMatrix, b: torch.Tensor, cfg: TileConfig | None = None
     return out
 
 
+# ---------------------------------------------------------------- pruning (§8 f3)
+
+@dataclass
+class PruneConfig:
+    """include/shflbw/pruning.hpp:27-37"""
+    alpha: float = 0.5
+    beta_factor: float = 2.0
+    v: int = 1
+    kmeans_max_iters: int = 50
+    seed: int = 0
+    restarts: int = 4
+
+    def beta(self) -> float:
+        return min(1.0, self.beta_factor * self.alpha)
+
+    def _c(self) -> "L.PruneConfigC":
+        return L.PruneConfigC(self.alpha, self.beta_factor, self.v, self.kmeans_max_iters, self.seed,
+                              self.restarts, 0)
+
+
+@dataclass
+class PruneResult:
+    """mask [M, K] uint8, permutation [M] int32 (grouped position -> original
+    row), kept_score (include/shflbw/pruning.hpp:39-45)."""
+    mask: torch.Tensor
+    permutation: torch.Tensor
+    kept_score: float
+
+
+def _scores(scores: torch.Tensor) -> torch.Tensor:
+    if not (isinstance(scores, torch.Tensor) and scores.is_cuda and scores.dim() == 2):
+        raise BadParams("scores must be a 2-D CUDA tensor")
+    return scores.to(torch.float32).contiguous()
+
+
+def importance_scores(weights: torch.Tensor) -> torch.Tensor:
+    """|weights| (src/pruning.cpp:61-66)."""
+    w = weights.to(torch.float32).contiguous()
+    out = torch.empty_like(w)
+    _check(_lib().shflbw_cu_importance_scores(w.data_ptr(), w.numel(), out.data_ptr(), _stream()))
+    return out
+
+
+def kept_score(scores: torch.Tensor, mask: torch.Tensor) -> float:
+    """sum of scores under the mask, in the reference's order (src/pruning.cpp:68-75)."""
+    s, m = _scores(scores), _dev_u8(mask)
+    if tuple(s.shape) != tuple(m.shape):
+        raise ShapeMismatch("kept_score: shapes differ")
+    out = C.c_double(0.0)
+    _check(_lib().shflbw_cu_kept_score(s.data_ptr(), m.data_ptr(), s.shape[0], s.shape[1], C.byref(out), _stream()))
+    return out.value
+
+
+def prune_unstructured(scores: torch.Tensor, keep_ratio: float) -> torch.Tensor:
+    s = _scores(scores)
+    out = torch.empty(s.shape, dtype=torch.uint8, device=s.device)
+    _check(_lib().shflbw_cu_prune_unstructured(s.data_ptr(), s.shape[0], s.shape[1], keep_ratio, out.data_ptr(),
+                                               _stream()))
+    return out
+
+
+def prune_vectorwise(scores: torch.Tensor, v: int, alpha: float) -> torch.Tensor:
+    s = _scores(scores)
+    out = torch.empty(s.shape, dtype=torch.uint8, device=s.device)
+    _check(_lib().shflbw_cu_prune_vectorwise(s.data_ptr(), s.shape[0], s.shape[1], v, alpha, out.data_ptr(),
+                                             _stream()))
+    return out
+
+
+def kmeans_row_grouping(mask: torch.Tensor, scores: torch.Tensor, cfg: PruneConfig) -> torch.Tensor:
+    s, m = _scores(scores), _dev_u8(mask)
+    if tuple(s.shape) != tuple(m.shape):
+        raise ShapeMismatch("kmeans_row_grouping: mask and scores differ")
+    out = torch.empty(s.shape[0], dtype=torch.int32, device=s.device)
+    c = cfg._c()
+    _check(_lib().shflbw_cu_kmeans_row_grouping(m.data_ptr(), s.data_ptr(), s.shape[0], s.shape[1], C.byref(c),
+                                                out.data_ptr(), _stream()))
+    return out
+
+
+def prune_shflbw(scores: torch.Tensor, cfg: PruneConfig) -> PruneResult:
+    """The Shfl-BW pruner (src/pruning.cpp:339-362) on the GPU."""
+    s = _scores(scores)
+    mask = torch.empty(s.shape, dtype=torch.uint8, device=s.device)
+    perm = torch.empty(s.shape[0], dtype=torch.int32, device=s.device)
+    kept = C.c_double(0.0)
+    c = cfg._c()
+    _check(_lib().shflbw_cu_prune_shflbw(s.data_ptr(), s.shape[0], s.shape[1], C.byref(c), mask.data_ptr(),
+                                         perm.data_ptr(), C.byref(kept), _stream()))
+    return PruneResult(mask, perm, kept.value)
+
+
 def smx1_loads(data: bytes, dtype: torch.dtype = torch.bfloat16) -> ShflBWMatrix:
     """An SMX1 kind-3 container (the reference's file format,
     include/shflbw/container.hpp:14-22) straight into the device layout;

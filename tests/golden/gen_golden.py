@@ -298,6 +298,51 @@ def smx1_cases(ref: Reference) -> list[dict]:
     return out
 
 
+PRUNE_CASES = [  # name, M, K, V, alpha, beta_factor, iters, seed, restarts, score seed, quantise
+    ("small", 8, 12, 2, 0.5, 2.0, 50, 0, 4, 1, False),
+    ("ties", 16, 16, 4, 0.25, 2.0, 50, 3, 4, 2, True),
+    ("v1_topk", 6, 10, 1, 0.3, 2.0, 50, 0, 2, 3, False),
+    ("single_group", 8, 20, 8, 0.25, 2.0, 50, 1, 2, 4, False),
+    ("alpha_one", 8, 8, 4, 1.0, 2.0, 50, 0, 2, 5, False),
+    ("mid", 64, 96, 8, 0.25, 2.0, 50, 7, 4, 6, False),
+    ("mid_ties", 60, 40, 6, 0.3, 1.5, 20, 11, 3, 7, True),
+    ("wide", 128, 256, 16, 0.25, 2.0, 50, 2, 4, 8, False),
+    ("v64", 256, 512, 64, 0.25, 2.0, 50, 5, 2, 9, False),
+]
+
+
+def prune_scores(ref_or_orc, M, K, sseed, quantise):
+    """importance scores for the pruning fixtures: |random_dense| (the
+    reference's generator), optionally quantised to quarters so that ties
+    exercise every tie-break rule."""
+    s = np.abs(ref_or_orc.random_dense(M, K, sseed)).astype(np.float32)
+    if quantise:
+        s = (np.floor(s * 4.0) / 4.0).astype(np.float32)
+    return s
+
+
+def prune_cases(ref: Reference) -> list[dict]:
+    """prune_shflbw and its parts (src/pruning.cpp) on the reference."""
+    out = []
+    for (name, M, K, V, alpha, bf, iters, seed, restarts, sseed, quant) in PRUNE_CASES:
+        s = prune_scores(ref, M, K, sseed, quant)
+        cfg = {"alpha": alpha, "beta_factor": bf, "v": V, "kmeans_max_iters": iters, "seed": seed,
+               "restarts": restarts}
+        mask, perm, kept = ref.prune_shflbw(s, cfg)
+        beta = min(1.0, bf * alpha)
+        um = ref.prune_unstructured(s, beta)
+        vm = ref.prune_vectorwise(s, V, alpha)
+        order = ref.kmeans_row_grouping(um, s, cfg)
+        out.append({"name": name, "M": M, "K": K, "cfg": cfg, "score_seed": sseed, "quantise": quant,
+                    "scores_digest": digest(s),
+                    "mask_digest": digest(mask), "mask_popcount": int(mask.sum()),
+                    "permutation": perm.tolist(), "kept_score_hex": float(kept).hex(),
+                    "unstructured_digest": digest(um), "vectorwise_digest": digest(vm),
+                    "kmeans_order": order.tolist(),
+                    "kept_vectorwise_hex": float(ref.kept_score(s, vm)).hex()})
+    return out
+
+
 def main() -> None:
     ref = Reference()
     files = {
@@ -307,6 +352,7 @@ def main() -> None:
         "conv_cases.json": conv_cases(ref),
         "full_size.json": full_size(ref),
         "smx1_cases.json": smx1_cases(ref),
+        "prune_cases.json": prune_cases(ref),
     }
     only = sys.argv[1:]
     files = {k: v for k, v in files.items() if not only or k in only}

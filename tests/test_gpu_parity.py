@@ -764,3 +764,77 @@ def test_smx1_errors_and_files(sb, oracle, tmp_path):
     assert sb.smx1_dumps(b) == path.read_bytes()
     with pytest.raises(sb.BadParams):  # conv-ordered layouts are not the reference's format
         sb.smx1_dumps(sb.conv_prepare(a, 4))
+
+
+# ------------------------------------------------ pruning on the GPU (§8 f3)
+
+def _prune_scores(oracle, c):
+    s = np.abs(oracle.random_dense(c["M"], c["K"], c["score_seed"])).astype(np.float32)
+    if c["quantise"]:
+        s = (np.floor(s * 4.0) / 4.0).astype(np.float32)
+    return s
+
+
+def _sha(t):
+    return hashlib.sha256(np.ascontiguousarray(t.cpu().numpy()).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("case", load_golden("prune_cases.json"), ids=lambda c: c["name"])
+def test_prune_shflbw_matches_reference(sb, oracle, case):
+    """prune_shflbw and every stage of it equal the reference's results
+    (tests/golden/prune_cases.json, written by the compiled reference): masks
+    byte for byte, the permutation, and the kept score to the last bit."""
+    s = dev(_prune_scores(oracle, case))
+    cfg = sb.PruneConfig(**case["cfg"])
+    r = sb.prune_shflbw(s, cfg)
+    assert _sha(r.mask) == case["mask_digest"]
+    assert r.permutation.cpu().tolist() == case["permutation"]
+    assert float(r.kept_score).hex() == case["kept_score_hex"]
+    um = sb.prune_unstructured(s, cfg.beta())
+    assert _sha(um) == case["unstructured_digest"]
+    vm = sb.prune_vectorwise(s, cfg.v, cfg.alpha)
+    assert _sha(vm) == case["vectorwise_digest"]
+    assert float(sb.kept_score(s, vm)).hex() == case["kept_vectorwise_hex"]
+    assert sb.kmeans_row_grouping(um, s, cfg).cpu().tolist() == case["kmeans_order"]
+    # the pruned mask is a valid Shfl-BW pattern for the converter
+    assert sb.validate_pattern(r.mask, "shfl_bw", cfg.v)[0]
+
+
+def test_prune_fuzz_vs_reference(sb, reference):
+    """Random shapes, densities and tie-heavy scores against the compiled
+    reference (oracle/_ref travels to the GPU box)."""
+    rs = np.random.RandomState(77)
+    for t in range(12):
+        V = int(rs.choice([1, 2, 4, 8, 16]))
+        M = V * int(rs.randint(1, 9))
+        K = int(rs.randint(1, 80))
+        s = np.abs(rs.randn(M, K)).astype(np.float32)
+        if t % 3 == 0:
+            s = (np.floor(s * 2) / 2).astype(np.float32)  # many ties, zeros
+        cfg = {"alpha": float(rs.choice([0.1, 0.25, 0.5, 0.75, 1.0])), "beta_factor": float(rs.choice([1.0, 2.0, 3.0])),
+               "v": V, "kmeans_max_iters": int(rs.choice([1, 5, 50])), "seed": int(rs.randint(0, 100)),
+               "restarts": int(rs.randint(1, 4))}
+        mask, perm, kept = reference.prune_shflbw(s, cfg)
+        r = sb.prune_shflbw(dev(s), sb.PruneConfig(**cfg))
+        assert np.array_equal(r.mask.cpu().numpy(), mask), (t, cfg)
+        assert np.array_equal(r.permutation.cpu().numpy().astype(np.uint32), perm), (t, cfg)
+        assert float(r.kept_score).hex() == float(kept).hex(), (t, cfg)
+
+
+def test_prune_errors(sb):
+    s = torch.ones((8, 8), device="cuda")
+    with pytest.raises(sb.BadParams):
+        sb.prune_shflbw(s, sb.PruneConfig(alpha=0.0, v=2))
+    with pytest.raises(sb.BadParams):
+        sb.prune_shflbw(s, sb.PruneConfig(alpha=0.5, v=3))
+    with pytest.raises(sb.BadParams):
+        sb.prune_shflbw(s, sb.PruneConfig(alpha=0.5, v=2, restarts=0))
+    bad = s.clone()
+    bad[1, 1] = -1.0
+    with pytest.raises(sb.BadParams):
+        sb.prune_shflbw(bad, sb.PruneConfig(alpha=0.5, v=2))
+    bad[1, 1] = float("nan")
+    with pytest.raises(sb.BadParams):
+        sb.kept_score(bad, torch.ones((8, 8), dtype=torch.uint8, device="cuda"))
+    w = torch.tensor([[-3.0, 2.0]], device="cuda")
+    assert sb.importance_scores(w).cpu().tolist() == [[3.0, 2.0]]

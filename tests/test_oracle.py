@@ -293,3 +293,27 @@ def test_smx1_restatement_vs_reference_fuzz(oracle, reference):
         if s1 == 0:
             assert np.array_equal(p1.cols, p2.cols) and np.array_equal(p1.row_indices, p2.row_indices)
             assert np.array_equal(p1.values.view(np.uint32), p2.values.view(np.uint32))
+
+
+# ---------------------------------------------------------------- pruning fixtures
+
+def _prune_scores(gen, c):
+    s = np.abs(gen.random_dense(c["M"], c["K"], c["score_seed"])).astype(np.float32)
+    if c["quantise"]:
+        s = (np.floor(s * 4.0) / 4.0).astype(np.float32)
+    return s
+
+
+def test_prune_fixture_scores_regenerate(oracle):
+    """The pruning fixtures' importance scores come from the restated
+    generator (|random_dense|), so GPU tests rebuild them without the reference."""
+    for c in load_golden("prune_cases.json"):
+        assert hashlib.sha256(_prune_scores(oracle, c).tobytes()).hexdigest() == c["scores_digest"], c["name"]
+
+
+def test_prune_fixtures_against_reference(reference):
+    for c in load_golden("prune_cases.json"):
+        s = _prune_scores(reference, c)
+        mask, perm, kept = reference.prune_shflbw(s, c["cfg"])
+        assert hashlib.sha256(mask.tobytes()).hexdigest() == c["mask_digest"]
+        assert perm.tolist() == c["permutation"] and float(kept).hex() == c["kept_score_hex"]
