@@ -126,19 +126,49 @@ template <> __device__ __forceinline__ __half to_out<__half>(float x) { return _
 
 // Coalesced 16-byte stores of a staged [ROWS][128] tile of OT through the row
 // map: one output row = 128*sizeof(OT) bytes, 16 or 32 lanes per row.
-template <class OT, int ROWS>
+template <class OT, int ROWS, bool BATCH = true>
 __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigned char* ctile, const int32_t* rows,
                                                 int q, int lane, int n0) {
     constexpr int esz = sizeof(OT);
     constexpr int kLanesPerRow = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
     constexpr int kRowsPerInst = 32 / kLanesPerRow;
+    constexpr int kIters = (ROWS + 4 * kRowsPerInst - 1) / (4 * kRowsPerInst);
     const int chunk = lane % kLanesPerRow;
     const int nn = n0 + chunk * (16 / esz);
-    if (nn < p.N) {
+    const int v0 = q * kRowsPerInst + lane / kLanesPerRow;
+    if (!BATCH) {  // interleaved: fewer live registers (the persistent kernel's epilogue warps)
+        if (nn < p.N) {
 #pragma unroll 4
-        for (int v = q * kRowsPerInst + lane / kLanesPerRow; v < ROWS; v += 4 * kRowsPerInst) {
-            const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
-            *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(rows[v]) * p.ldc + nn) * esz) = x;
+            for (int v = v0; v < ROWS; v += 4 * kRowsPerInst) {
+                const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
+                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(rows[v]) * p.ldc + nn) * esz) =
+                    x;
+            }
+        }
+        return;
+    }
+    if (nn < p.N) {
+        // all shared-memory reads first (explicit ld.shared, so no store below
+        // can alias them), then the global stores
+        int4 x[kIters];
+        int32_t row[kIters];
+        const uint32_t base = smem_u32(ctile) + static_cast<uint32_t>(chunk * 16);
+#pragma unroll
+        for (int k = 0; k < kIters; ++k) {
+            const int v = v0 + k * 4 * kRowsPerInst;
+            if (v < ROWS) {
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x[k].x), "=r"(x[k].y), "=r"(x[k].z), "=r"(x[k].w)
+                             : "r"(base + static_cast<uint32_t>(v * kBlockN * esz)));
+                row[k] = rows[v];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kIters; ++k) {
+            const int v = v0 + k * 4 * kRowsPerInst;
+            if (v < ROWS)
+                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(row[k]) * p.ldc + nn) * esz) =
+                    x[k];
         }
     }
 }
@@ -228,22 +258,47 @@ __device__ __forceinline__ void ksplit_epilogue(const TcParams& p, uint32_t t_ro
     if (m == 0) trace_event(p.trace, 24);
     mbar_wait(recv_bar, 0);
     if (m == 0) trace_event(p.trace, 25);
+    // the peers' partials into registers first: explicit ld.shared, issued
+    // back to back (a generic load per row, serialised behind each store,
+    // cost ~0.7 us here)
+    float peer[KSF - 1][kRP];
+    const uint32_t recv_u32 = smem_u32(recv) + static_cast<uint32_t>(m * 4);
+#pragma unroll
+    for (int sl = 0; sl < KSF - 1; ++sl)
+#pragma unroll
+        for (int i = 0; i < kRP; ++i)
+            asm volatile("ld.shared.f32 %0, [%1];"
+                         : "=f"(peer[sl][i])
+                         : "r"(recv_u32 + static_cast<uint32_t>((sl * kRP + i) * kBlockN * 4)));
+    float res[kRP];
 #pragma unroll
     for (int i = 0; i < kRP; ++i) {
         float acc = 0.0f;
 #pragma unroll
-        for (int c = 0; c < KSF; ++c)  // K-rank order
-            acc += c == kr ? vals[c * kRP + i] : recv[((c < kr ? c : c - 1) * kRP + i) * kBlockN + m];
-        if (p.bulk_out) {
-            reinterpret_cast<OT*>(ctile)[i * kBlockN + m] = to_out<OT>(acc);
-        } else if (n0 + m < p.N) {
-            static_cast<OT*>(p.C)[static_cast<int64_t>(rows_s[kr * kRP + i]) * p.ldc + n0 + m] = to_out<OT>(acc);
+        for (int c = 0; c < KSF; ++c) {  // K-rank order; peer c sits in slot c (c < kr) or c - 1
+            float part = vals[c * kRP + i];
+            if (c < KSF - 1) part = (c < kr) ? peer[c < KSF - 1 ? c : 0][i] : part;
+            if (c > 0) part = (c > kr) ? peer[c > 0 ? c - 1 : 0][i] : part;
+            acc += part;
         }
+        res[i] = acc;
     }
+    if (m == 0) trace_event(p.trace, 26);
     if (p.bulk_out) {
+#pragma unroll
+        for (int i = 0; i < kRP; ++i) reinterpret_cast<OT*>(ctile)[i * kBlockN + m] = to_out<OT>(res[i]);
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (m == 0) trace_event(p.trace, 27);
         store_tile_rows<OT, kRP>(p, ctile, rows_s + kr * kRP, q, lane, n0);
+    } else if (n0 + m < p.N) {
+        int32_t row[kRP];
+#pragma unroll
+        for (int i = 0; i < kRP; ++i) row[i] = rows_s[kr * kRP + i];
+#pragma unroll
+        for (int i = 0; i < kRP; ++i)
+            static_cast<OT*>(p.C)[static_cast<int64_t>(row[i]) * p.ldc + n0 + m] = to_out<OT>(res[i]);
     }
+    if (m == 0) trace_event(p.trace, 28);
 }
 
 // KIND 2 (conv, weight in conv order): one gather4 = 4 K rows (ch, r, s) that
@@ -580,7 +635,7 @@ __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc,
     if (lane == 0) mbar_arrive(acc_empty);
     if (p.bulk_out) {
         asm volatile("bar.sync 3, 128;" ::: "memory");
-        store_tile_rows<OT, VS>(p, ctile, rows_s, q, lane, n0);
+        store_tile_rows<OT, VS, false>(p, ctile, rows_s, q, lane, n0);
     }
 }
 
