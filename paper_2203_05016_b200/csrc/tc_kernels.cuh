@@ -502,22 +502,27 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
         const T* Bp = static_cast<const T*>(p.B);
         if (nkb > 0) stage_meta(0);  // static metadata: before the dependency wait
+        asm volatile("bar.sync 2, 128;" ::: "memory");  // first window visible (overlaps the previous grid)
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
+        const uint32_t meta_u32 = smem_u32(meta_s);
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % stages;
             const int win = kb % kMetaBlocks;
             if (win == 0 && kb > 0) {
                 asm volatile("bar.sync 2, 128;" ::: "memory");  // all done with the old window
                 stage_meta(kb);
+                asm volatile("bar.sync 2, 128;" ::: "memory");
             }
-            if (win == 0) asm volatile("bar.sync 2, 128;" ::: "memory");
             if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
             if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
             unsigned char* a_st = smem + s * kStageBytes;
             const int32_t* mk = meta_s + win * kBlockK;
             if (t_issue) {
-                int4 ci = reinterpret_cast<const int4*>(mk)[g_rg];
+                int4 ci;  // explicit ld.shared (a generic load would take the slower generic path)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
+                             : "r"(meta_u32 + static_cast<uint32_t>((win * kBlockK + g_rg * 4) * 4)));
                 int x = g_x;
                 if (KIND == 1) {
                     ci.x = conv_row(ci.x);
@@ -816,7 +821,10 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
                 }
                 if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
                 if (t_issue) {
-                    int4 ci = reinterpret_cast<const int4*>(mbuf + win * kBlockK)[g_rg];
+                    int4 ci;
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
+                                 : "r"(smem_u32(mbuf) + static_cast<uint32_t>((win * kBlockK + g_rg * 4) * 4)));
                     int x = g_x;
                     if (KIND == 2) x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
                     if (KIND == 1) {
