@@ -138,11 +138,20 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
     const int v0 = q * kRowsPerInst + lane / kLanesPerRow;
     if (!BATCH) {  // interleaved: fewer live registers (the persistent kernel's epilogue warps)
         if (nn < p.N) {
+            // explicit ld.shared, volatile so it stays after the bar.sync above
+            // but without a memory clobber, so the compiler may start the next
+            // row's reads before this row's global store
+            const uint32_t base = smem_u32(ctile) + static_cast<uint32_t>(chunk * 16);
+            const uint32_t rbase = smem_u32(rows);
 #pragma unroll 4
             for (int v = v0; v < ROWS; v += 4 * kRowsPerInst) {
-                const int4 x = *reinterpret_cast<const int4*>(ctile + (v * kBlockN) * esz + chunk * 16);
-                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(rows[v]) * p.ldc + nn) * esz) =
-                    x;
+                int4 x;
+                int32_t row;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                             : "r"(base + static_cast<uint32_t>(v * kBlockN * esz)));
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(row) : "r"(rbase + static_cast<uint32_t>(v * 4)));
+                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(row) * p.ldc + nn) * esz) = x;
             }
         }
         return;
