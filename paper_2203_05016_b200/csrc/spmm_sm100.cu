@@ -153,10 +153,11 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     //   2  2 x 2 (CS = 4): V split over a CTA pair (multicast) and K split
     //      over two pairs -- half the gathers per SM, VS/2 rows per CTA cross
     //      DSMEM;
-    //   0  auto (default): an explicit "split" means V split; otherwise, when
-    //      4 CTAs per unit fit on the GPU, by the widest group's K blocks
-    //      (measured): >= 24 -> K split by 4, >= 8 (V == 64) ->
-    //      2 x 2, else V split.
+    //   0  auto (default): an explicit "split" means V split; otherwise by
+    //      the widest group's K blocks and how many CTAs per unit fit on the
+    //      GPU (measured): >= 24 K blocks and 4 fit -> K split
+    //      by 4; >= 8 and 4 fit (V >= 64) -> 2 x 2; >= 8 and 2 fit -> K split
+    //      by 2; else V split.
     const int min_kb = 2;  // K blocks per CTA worth splitting for
     const int kb_all = (a->cols + kBlockK - 1) / kBlockK;
     const int kb_grp = a->max_group_cols > 0 ? a->max_group_cols / kBlockK : kb_all;  // widest group
@@ -166,12 +167,16 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     const int64_t units = static_cast<int64_t>(n_tiles) * groups;
     if (mode == 0) {
         mode = 3;
-        if (cs <= 0 && units * 4 <= num_sms() && b.kind == 0) {
-            if (kb_grp >= 24) {
+        if (cs <= 0 && b.kind == 0 && kb_grp >= 8) {
+            const bool fit4 = units * 4 <= num_sms(), fit2 = units * 2 <= num_sms();
+            if (fit4 && kb_grp >= 24) {
                 mode = 1;
                 cs = 4;
-            } else if (kb_grp >= 8 && V == 64) {
+            } else if (fit4 && V >= 64) {
                 mode = 2;
+            } else if (fit2) {
+                mode = 1;
+                cs = 2;
             }
         }
     }
