@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libshflbw_b200.so")
+LIB_PATH = os.environ.get("SBW_LIB") or os.path.join(HERE, "lib", "libshflbw_b200.so")  # SBW_LIB: A/B runs
 
 (OK, SHAPE_MISMATCH, NONCONFORMANT_MASK, BAD_PARAMS, BAD_GEOMETRY, CUDA_ERROR, UNSUPPORTED, BAD_MAGIC,
  UNSUPPORTED_VERSION, CORRUPT_PAYLOAD) = range(10)

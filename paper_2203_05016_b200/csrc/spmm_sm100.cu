@@ -136,6 +136,11 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         else return SHFLBW_UNSUPPORTED;
         if (static_cast<int64_t>(b.C) * b.H * b.W >= (1LL << 31)) return SHFLBW_UNSUPPORTED;
     }
+    // conv column encoding (tc_kernels.cuh conv_encode): fdiv's exact range,
+    // R, S <= 16 and the tap's base row < 2^23
+    if (b.kind != 0 && (b.K >= (1 << 22) || b.R > 16 || b.S > 16 ||
+                        static_cast<int64_t>(b.C) * b.H * (b.kind == 1 ? b.W : 1) >= (1LL << 23)))
+        return SHFLBW_UNSUPPORTED;
     const int groups = g_end - g_begin;
     if (groups <= 0) return SHFLBW_OK;
     if (groups > 65535) return SHFLBW_UNSUPPORTED;
@@ -227,6 +232,8 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.W = b.W;
     prm.RS = b.R * b.S;
     prm.S = b.S;
+    prm.inv_rs = 1.0f / static_cast<float>(prm.RS > 0 ? prm.RS : 1);
+    prm.inv_s = 1.0f / static_cast<float>(b.S > 0 ? b.S : 1);
     prm.stride = b.stride;
     prm.pad = b.pad;
     prm.Q = b.Q;

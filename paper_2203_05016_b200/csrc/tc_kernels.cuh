@@ -79,6 +79,7 @@ struct TcParams {
     int bw;                     // MN block width of the activation tile (64 | 32 | 16 elements)
     // implicit-GEMM conv geometry (KIND 1)
     int Nb, H, W, RS, S, stride, pad, Q, PQ;
+    float inv_rs, inv_s;  // 1/RS, 1/S for fdiv (column ids < 2^22, checked on the host)
     int ksplit;      // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
     int per_sm;      // persistent: resident CTAs per SM
@@ -310,30 +311,71 @@ __device__ __forceinline__ void ksplit_epilogue(const TcParams& p, uint32_t t_ro
     if (m == 0) trace_event(p.trace, 28);
 }
 
+// c / d for 0 <= c < 2^22 and a small divisor d, given inv = 1.0f / d: the
+// fractional part of (c + 0.5) / d is at least 0.5 / d from an integer and the
+// two float roundings move it by < 2^-23 (c + 0.5) / d, so the truncation is
+// exact.  Replaces the ~25-instruction integer division on the gather issue
+// path (9 of them per lane per K block for a 3x3 conv).
+__device__ __forceinline__ int fdiv(int c, float inv) {
+    return __float2int_rz((static_cast<float>(c) + 0.5f) * inv);
+}
+
+// Conv column encoding, applied once when a window of column indices is
+// staged in shared memory (not per gather): sparse column c = (ch, r, s) of
+// the C*R*S filter becomes (base << 8) | (r << 4) | s with base the input row
+// of tap (r, s) for output position (0, 0) before the padding shift --
+// KIND 2: ch*H + r in the [C*H][W*Nb] view, KIND 1: (ch*H + r)*W + s in the
+// [C*H*W][Nb] view.  R, S <= 16 and base < 2^23 (host-checked).  Pad columns
+// stay -1.
+template <int KIND>
+__device__ __forceinline__ int conv_encode(const TcParams& p, int c) {
+    if (c < 0) return -1;
+    const int ch = fdiv(c, p.inv_rs), rs = c - ch * p.RS;
+    const int r = fdiv(rs, p.inv_s), sx = rs - r * p.S;
+    const int base = KIND == 2 ? ch * p.H + r : (ch * p.H + r) * p.W + sx;
+    return (base << 8) | (r << 4) | sx;
+}
+
+template <int KIND>
+__device__ __forceinline__ int4 conv_encode4(const TcParams& p, int4 c) {
+    if constexpr (KIND == 0) return c;
+    return make_int4(conv_encode<KIND>(p, c.x), conv_encode<KIND>(p, c.y), conv_encode<KIND>(p, c.z),
+                     conv_encode<KIND>(p, c.w));
+}
+
+// KIND 1: input row of an encoded column for this gather's output position
+// (h0, w0 = its top-left tap, i.e. p*stride - pad, q*stride - pad); -1 outside
+// the image.
+__device__ __forceinline__ int conv_row_enc(const TcParams& p, int e, int h0, int w0, bool pos_ok) {
+    if (e < 0 || !pos_ok) return -1;
+    const int h = h0 + ((e >> 4) & 15), w = w0 + (e & 15);
+    if (h < 0 || h >= p.H || w < 0 || w >= p.W) return -1;
+    return (e >> 8) + h0 * p.W + w0;
+}
+
 // KIND 2 (conv, weight in conv order): one gather4 = 4 K rows (ch, r, s) that
 // share the filter column s, each fetching the 64-element row segment of the
 // [C*H][W*Nb] input view that holds this MN block's 64/Nb adjacent output
 // positions (stride 1): row ch*H + p + r - pad, x = (q0 + s - pad)*Nb.  Rows
 // outside the image are -1 (zero-filled); columns left/right of it are out of
-// the view's bounds and zero-filled by TMA.  Returns the x coordinate.
+// the view's bounds and zero-filled by TMA.  ci holds encoded columns; returns
+// the x coordinate.
 __device__ __forceinline__ int conv_wide_rows(const TcParams& p, int4& ci, int h0, int x0, bool pos_ok) {
-    int c0 = ci.x >= 0 ? ci.x : (ci.y >= 0 ? ci.y : (ci.z >= 0 ? ci.z : ci.w));
+    const int c0 = ci.x >= 0 ? ci.x : (ci.y >= 0 ? ci.y : (ci.z >= 0 ? ci.z : ci.w));
     if (c0 < 0 || !pos_ok) {
         ci = make_int4(-1, -1, -1, -1);
         return 0;
     }
-    auto row = [&](int c) -> int {
-        if (c < 0) return -1;
-        const int ch = c / p.RS, r = (c - ch * p.RS) / p.S;
-        const int h = h0 + r;
-        return (h < 0 || h >= p.H) ? -1 : ch * p.H + h;
+    auto row = [&](int e) -> int {
+        if (e < 0) return -1;
+        const int h = h0 + ((e >> 4) & 15);
+        return (h < 0 || h >= p.H) ? -1 : (e >> 8) + h0;
     };
-    const int sx = c0 % p.S;
     ci.x = row(ci.x);
     ci.y = row(ci.y);
     ci.z = row(ci.z);
     ci.w = row(ci.w);
-    return (x0 + sx) * p.Nb;
+    return (x0 + (c0 & 15)) * p.Nb;
 }
 
 // warp roles (192 threads):
@@ -401,7 +443,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     auto stage_meta = [&](int kb0) {
         const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
         const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + (kbase + kb0) * kBlockK);
-        for (int i = et; i < nb * (kBlockK / 4); i += 128) reinterpret_cast<int4*>(meta_s)[i] = src[i];
+        for (int i = et; i < nb * (kBlockK / 4); i += 128)
+            reinterpret_cast<int4*>(meta_s)[i] = conv_encode4<KIND>(p, src[i]);
     };
 
     // ---- prologue (reads only the static sparse matrix: overlaps the
@@ -499,14 +542,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             g_p0 = (pos / p.Q) * p.stride - p.pad;
             g_q0 = (pos % p.Q) * p.stride - p.pad;
         }
-        auto conv_row = [&](int c) -> int {
-            if (c < 0 || !g_pos_ok) return -1;
-            const int ch = c / p.RS, rs = c - ch * p.RS;
-            const int r = rs / p.S, sx = rs - r * p.S;
-            const int h = g_p0 + r, w = g_q0 + sx;
-            if (h < 0 || h >= p.H || w < 0 || w >= p.W) return -1;
-            return (ch * p.H + h) * p.W + w;
-        };
         // cp.async part (SpMM only): slabs [2-cps, 2): cps*512 16-byte chunks per K block
         const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
         const T* Bp = static_cast<const T*>(p.B);
@@ -534,10 +569,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                              : "r"(meta_u32 + static_cast<uint32_t>((win * kBlockK + g_rg * 4) * 4)));
                 int x = g_x;
                 if (KIND == 1) {
-                    ci.x = conv_row(ci.x);
-                    ci.y = conv_row(ci.y);
-                    ci.z = conv_row(ci.z);
-                    ci.w = conv_row(ci.w);
+                    ci.x = conv_row_enc(p, ci.x, g_p0, g_q0, g_pos_ok);
+                    ci.y = conv_row_enc(p, ci.y, g_p0, g_q0, g_pos_ok);
+                    ci.z = conv_row_enc(p, ci.z, g_p0, g_q0, g_pos_ok);
+                    ci.w = conv_row_enc(p, ci.w, g_p0, g_q0, g_pos_ok);
                 } else if (KIND == 2) {
                     x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
                 }
@@ -791,7 +826,17 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
             int32_t* dst = meta_s + buf * kMetaBlocks * kBlockK;
             for (int x = et; x < nb * (kBlockK / 4); x += 128) {
                 if (async) cp_async16(smem_u32(dst + 4 * x), src + 4 * x, true);
-                else reinterpret_cast<int4*>(dst)[x] = reinterpret_cast<const int4*>(src)[x];
+                else reinterpret_cast<int4*>(dst)[x] = conv_encode4<KIND>(p, reinterpret_cast<const int4*>(src)[x]);
+            }
+        };
+        // conv: encode a window that arrived raw through cp.async (in place)
+        auto encode_window = [&](int u, int buf) {
+            if constexpr (KIND != 0) {
+                const int gl = u / n_tiles;
+                const int nkb = (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK;
+                const int nb = nkb < kMetaBlocks ? nkb : kMetaBlocks;
+                int4* w = reinterpret_cast<int4*>(meta_s + buf * kMetaBlocks * kBlockK);
+                for (int x = et; x < nb * (kBlockK / 4); x += 128) w[x] = conv_encode4<KIND>(p, w[x]);
             }
         };
         if (cid < units) load_window(cid, 0, 0, false);
@@ -837,18 +882,10 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
                     int x = g_x;
                     if (KIND == 2) x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
                     if (KIND == 1) {
-                        auto conv_row = [&](int c) -> int {
-                            if (c < 0 || !g_pos_ok) return -1;
-                            const int ch = c / p.RS, rs = c - ch * p.RS;
-                            const int r = rs / p.S, sx = rs - r * p.S;
-                            const int h = g_p0 + r, w = g_q0 + sx;
-                            if (h < 0 || h >= p.H || w < 0 || w >= p.W) return -1;
-                            return (ch * p.H + h) * p.W + w;
-                        };
-                        ci.x = conv_row(ci.x);
-                        ci.y = conv_row(ci.y);
-                        ci.z = conv_row(ci.z);
-                        ci.w = conv_row(ci.w);
+                        ci.x = conv_row_enc(p, ci.x, g_p0, g_q0, g_pos_ok);
+                        ci.y = conv_row_enc(p, ci.y, g_p0, g_q0, g_pos_ok);
+                        ci.z = conv_row_enc(p, ci.z, g_p0, g_q0, g_pos_ok);
+                        ci.w = conv_row_enc(p, ci.w, g_p0, g_q0, g_pos_ok);
                     }
                     void* dst = smem + s * kStageBytes + g_b * blk_bytes + g_rg * (4 * bw * 2);
                     if constexpr (!mcast)
@@ -860,6 +897,10 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
             }
             cp_async_wait<0>();
             asm volatile("bar.sync 2, 128;" ::: "memory");  // next unit's window visible; this buffer free
+            if (KIND != 0 && un < units) {
+                encode_window(un, buf ^ 1);
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+            }
         }
     } else {
         // ---------------- epilogue ----------------

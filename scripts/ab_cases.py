@@ -1,0 +1,31 @@
+"""Short timing of a fixed case list (development, for scripts/ab.sh)."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+import torch  # noqa: E402
+
+import sweep  # noqa: E402
+
+dev = torch.device("cuda", 0)
+only = sys.argv[1].split(",") if len(sys.argv) > 1 else ["ns", "ffn2", "gnmt90", "conv56", "conv14"]
+cases = {
+    "ns": lambda: sweep.spmm_row("ns", 2048, 128, 2048, 64, 0.25, 2000, dev),
+    "ffn2": lambda: sweep.spmm_row("ffn2", 512, 4096, 2048, 64, 0.25, 1000, dev),
+    "ffn1_50": lambda: sweep.spmm_row("ffn1_50", 2048, 4096, 512, 64, 0.5, 1000, dev),
+    "ffn2_v32": lambda: sweep.spmm_row("ffn2_v32", 512, 4096, 2048, 32, 0.25, 1000, dev),
+    "gnmt90": lambda: sweep.spmm_row("gnmt90", 4096, 128, 1024, 64, 0.1, 2000, dev),
+    "lf": lambda: sweep.spmm_row("lf", 16384, 8192, 4096, 64, 0.25, 20, dev),
+    "conv56": lambda: sweep.conv_row("conv56", 64, 56, 64, 3, 1, 32, 64, 0.25, 300, dev),
+    "conv28": lambda: sweep.conv_row("conv28", 128, 28, 128, 3, 1, 32, 64, 0.25, 300, dev),
+    "conv14": lambda: sweep.conv_row("conv14", 256, 14, 256, 3, 1, 32, 64, 0.25, 300, dev),
+    "conv7": lambda: sweep.conv_row("conv7", 512, 7, 512, 3, 1, 32, 64, 0.25, 300, dev),
+}
+out = {}
+for k in only:
+    r = cases[k]()
+    out[k] = (round(r["us"], 2), round(r["dense_us"], 2))
+print(json.dumps(out))

@@ -97,3 +97,15 @@ def test_smx1_decode_rejects_like_the_reference_without_gpu(lib):
             assert st in (L.OK, L.CUDA_ERROR), c["name"]
         else:
             assert st == c["status"], (c["name"], st, c["status"])
+
+
+def test_conv_fdiv_reciprocal_exact():
+    """The conv producers divide column ids by R*S and S with a float
+    reciprocal (tc_kernels.cuh fdiv): trunc((c + 0.5f) * (1.0f / d)) == c / d
+    for every c < 2^22 (the host-checked range) and every filter size used."""
+    import numpy as np
+    c = np.arange(0, 1 << 22, dtype=np.int64)
+    cf = c.astype(np.float32) + np.float32(0.5)
+    for d in list(range(1, 50)) + [64, 81, 121, 256]:
+        q = np.trunc(cf * (np.float32(1.0) / np.float32(d))).astype(np.int64)
+        assert np.array_equal(q, c // d), d
