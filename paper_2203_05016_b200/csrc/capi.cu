@@ -12,7 +12,7 @@ namespace sbw {
 namespace {
 thread_local std::string g_error;
 thread_local int64_t g_launches = 0;
-std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0}, g_pdl{1}, g_cps{0}, g_trace{0}, g_nobulk{0}, g_split_mode{0}, g_persist{0};
+std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0}, g_pdl{1}, g_cps{0}, g_trace{0}, g_nobulk{0}, g_split_mode{0}, g_persist{0}, g_gw{0};
 }  // namespace
 
 void set_error(const std::string& msg) { g_error = msg; }
@@ -36,6 +36,7 @@ int64_t option(const char* key) {
     if (!std::strcmp(key, "no_bulk_out")) return g_nobulk.load();
     if (!std::strcmp(key, "split_mode")) return g_split_mode.load();
     if (!std::strcmp(key, "persistent")) return g_persist.load();
+    if (!std::strcmp(key, "gather_warps")) return g_gw.load();
     return 0;
 }
 
@@ -114,6 +115,7 @@ int shflbw_cu_set_option(const char* key, int64_t value) {
     else if (!std::strcmp(key, "no_bulk_out")) g_nobulk = value;
     else if (!std::strcmp(key, "split_mode")) g_split_mode = value;
     else if (!std::strcmp(key, "persistent")) g_persist = value;
+    else if (!std::strcmp(key, "gather_warps")) g_gw = value;
     else return fail(SHFLBW_BAD_PARAMS, std::string("unknown option ") + key);
     return SHFLBW_OK;
 }

@@ -292,6 +292,16 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     const int max_kb = (kb_grp + ksf - 1) / ksf;  // K blocks per CTA
     if (!prm.persistent && stages > max_kb) stages = max_kb < 2 ? 2 : max_kb;  // the ring spans units otherwise
     prm.stages = stages;
+    {
+        // gather warps per CTA ("gather_warps", 0 = auto): an SM's gather rate
+        // grows with the warps issuing (scripts/fillbench2.cu)
+        const int64_t gwo = option("gather_warps");
+        // auto: 8 for units of >= 5 K blocks without a K split (measured
+        // 2-7 % faster: large FFN, FFN2 N=4096, ResNet 3x3 @28/@14); the
+        // short-unit, north-star and K-split kernels are not issue-bound
+        prm.gw = gwo > 0 ? static_cast<int>(gwo) : ((!prm.ksplit && kb_grp >= 5) ? 8 : 4);
+        if (prm.gw != 4 && prm.gw != 8) return fail(SHFLBW_BAD_PARAMS, "gather_warps must be 4 or 8");
+    }
 
     CUtensorMap tmB, tmW;
     int st;

@@ -83,6 +83,7 @@ struct TcParams {
     int ksplit;      // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
     int per_sm;      // persistent: resident CTAs per SM
+    int gw;          // gather warps per CTA (4, 8)
 };
 
 // Development timeline (scripts/trace.py): compiled in only with -DSBW_TRACE.
@@ -112,6 +113,12 @@ struct WeightLayout {
 };
 
 constexpr int kMetaBlocks = 16;  // K blocks of column indices staged in smem at a time
+
+// named barrier over the first/only `threads` threads that use it
+template <int THREADS>
+__device__ __forceinline__ void named_bar(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(THREADS) : "memory");
+}
 
 __device__ __forceinline__ void grid_dependency_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -378,19 +385,18 @@ __device__ __forceinline__ int conv_wide_rows(const TcParams& p, int4& ci, int h
     return (x0 + (c0 & 15)) * p.Nb;
 }
 
-// warp roles (192 threads):
+// warp roles (64 + 32 GW threads):
 //   warp 0  : stage bookkeeping -- waits for a free slot, arms the full
 //             barrier with the stage's byte count, loads the weight tile
 //   warp 1  : TMEM allocator + single-thread MMA issuer
-//   warps 2-5: gather issuers (8 gather4 each per K block, so the
-//             per-instruction ELECT/R2UR issue loop runs on all four SM
-//             sub-partitions in parallel), then the epilogue (warp w owns
-//             TMEM lanes 32*(w%4)..+31)
-constexpr int kGatherWarps = 4;
-constexpr int kThreadsTc = 64 + 32 * kGatherWarps;
-
-template <int DT, int VS, int CS, int KIND, int KSPLIT>
-__global__ void __launch_bounds__(kThreadsTc, 1)
+//   warps 2..2+GW-1: gather issuers (32/GW gather4 each per K block), then
+//             warps 2-5 run the epilogue (warp w owns TMEM lanes
+//             32*(w%4)..+31).  A warp issues one gather4 per ~70-90 cycles
+//             (the ELECT/R2UR/UTMALDG loop), so an SM's gather rate grows
+//             with the issuing warps: 23 / 32 / 40 B/cycle for 4 / 8 / 16
+//             warps in one CTA, 54 for 2 CTAs x 8 (scripts/fillbench2.cu).
+template <int DT, int VS, int CS, int KIND, int KSPLIT, int GW>
+__global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     k_spmm_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
               TcParams p) {
     using WL = WeightLayout<VS>;
@@ -436,14 +442,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     // multicast group: the VSF CTAs that share this CTA's K blocks
     const uint16_t cmask = static_cast<uint16_t>(((1u << VSF) - 1u) << (kr * VSF));
     const int cps = p.cps;
-    const int et = threadIdx.x - 64;  // gather/epilogue thread 0..127 (warps 2..5)
+    constexpr int kGT = 32 * GW;      // gather threads
+    const int et = threadIdx.x - 64;  // gather thread 0..kGT-1 (epilogue: et < 128)
     if (threadIdx.x == 0) trace_event(p.trace, 0);
 
     // gather warps stage a window of column indices (all 64 per K block)
     auto stage_meta = [&](int kb0) {
         const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
         const int4* src = reinterpret_cast<const int4*>(p.col_idx + gp + (kbase + kb0) * kBlockK);
-        for (int i = et; i < nb * (kBlockK / 4); i += 128)
+        for (int i = et; i < nb * (kBlockK / 4); i += kGT)
             reinterpret_cast<int4*>(meta_s)[i] = conv_encode4<KIND>(p, src[i]);
     };
 
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     //      previous kernel under PDL) ---------------------------------------
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
-            mbar_init(&full[s], 1 + (cps > 0 ? 32 * kGatherWarps : 0));
+            mbar_init(&full[s], 1 + (cps > 0 ? kGT : 0));
             mbar_init(&empty[s], mcast ? VSF : 1);
         }
         mbar_init(accum, 1);
@@ -525,11 +532,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int tma_slabs = 2 - cps;
         const int nblk = KIND == 0 ? tma_slabs : kBlockN / p.bw;  // MN blocks filled by TMA
         const int blk_bytes = kBlockK * p.bw * 2;
-        const int per_warp = 16 * nblk / kGatherWarps;              // gather4s per warp per K block
+        constexpr int kRGW = 16 / GW;                               // row groups (4 rows) per warp
+        const int per_warp = kRGW * nblk;                           // gather4s per warp per K block
         const int gi = gw * per_warp + lane;                        // this lane's gather
-        // a warp owns 4 row groups (16 rows) in every MN block, so both halves
-        // of an activation row are requested together
-        const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
+        // a warp owns kRGW row groups in every MN block, so both halves of an
+        // activation row are requested together
+        const int g_rg = gw * kRGW + lane % kRGW, g_b = lane / kRGW;
         const bool t_issue = lane < per_warp && (!mcast || (gi % VSF) == vr);
         // conv: this gather's output positions (fixed for the CTA)
         int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
@@ -546,7 +554,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
         const T* Bp = static_cast<const T*>(p.B);
         if (nkb > 0) stage_meta(0);  // static metadata: before the dependency wait
-        asm volatile("bar.sync 2, 128;" ::: "memory");  // first window visible (overlaps the previous grid)
+        named_bar<kGT>(2);  // first window visible (overlaps the previous grid)
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
         const uint32_t meta_u32 = smem_u32(meta_s);
@@ -554,9 +562,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             const int s = kb % stages;
             const int win = kb % kMetaBlocks;
             if (win == 0 && kb > 0) {
-                asm volatile("bar.sync 2, 128;" ::: "memory");  // all done with the old window
+                named_bar<kGT>(2);  // all done with the old window
                 stage_meta(kb);
-                asm volatile("bar.sync 2, 128;" ::: "memory");
+                named_bar<kGT>(2);
             }
             if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
             if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
@@ -584,7 +592,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
             if (cps > 0) {
                 const uint32_t a_u32 = smem_u32(a_st);
-                for (int id = et; id < cps * 512; id += 128) {
+                for (int id = et; id < cps * 512; id += kGT) {
                     const int r = id >> cpr_log2, c = id & ((1 << cpr_log2) - 1);
                     const int sl = tma_slabs + (c >> 3), cc = c & 7;
                     const int col = mk[r];
@@ -597,38 +605,40 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
             __syncwarp();
         }
-        // output row map for the epilogue, loaded while the MMAs run
-        for (int v = et; v < VS; v += 128) {
-            const int64_t gr = static_cast<int64_t>(g) * p.V + vbase + v;
-            rows_s[v] = p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
-                                  : p.row_indices[gr];
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (gw < 4) {  // warps 2-5 run the epilogue; any further gather warps are done
+            // output row map for the epilogue, loaded while the MMAs run
+            for (int v = et; v < VS; v += 128) {
+                const int64_t gr = static_cast<int64_t>(g) * p.V + vbase + v;
+                rows_s[v] = p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
+                                      : p.row_indices[gr];
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
 
-        // ---------------- epilogue: TMEM -> permuted rows of C ----------------
-        mbar_wait(accum, 0);
-        tc_fence_after();
-        if (et == 0) trace_event(p.trace, 5);
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const int m = q * 32 + lane;
-        const uint32_t t_row = tmem_d + (static_cast<uint32_t>(q * 32) << 16);
-        // all MMAs are complete (accum), so the stage buffers are free: they
-        // hold the [VS][128] output tile for the bulk row stores
-        unsigned char* ctile = smem;
-        if constexpr (kKSplit) {
-            if (p.c_dtype == SHFLBW_F32)
-                ksplit_epilogue<float, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar, ctile);
-            else if (p.c_dtype == SHFLBW_BF16)
-                ksplit_epilogue<__nv_bfloat16, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv,
-                                                             recv_bar, ctile);
-            else
-                ksplit_epilogue<__half, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar,
-                                                      ctile);
-        } else {
-            if (p.c_dtype == SHFLBW_F32) epilogue_rows<float, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
-            else if (p.c_dtype == SHFLBW_BF16)
-                epilogue_rows<__nv_bfloat16, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
-            else epilogue_rows<__half, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+            // ---------------- epilogue: TMEM -> permuted rows of C ----------------
+            mbar_wait(accum, 0);
+            tc_fence_after();
+            if (et == 0) trace_event(p.trace, 5);
+            const int q = warp & 3;  // TMEM lane quarter this warp may access
+            const int m = q * 32 + lane;
+            const uint32_t t_row = tmem_d + (static_cast<uint32_t>(q * 32) << 16);
+            // all MMAs are complete (accum), so the stage buffers are free: they
+            // hold the [VS][128] output tile for the bulk row stores
+            unsigned char* ctile = smem;
+            if constexpr (kKSplit) {
+                if (p.c_dtype == SHFLBW_F32)
+                    ksplit_epilogue<float, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar, ctile);
+                else if (p.c_dtype == SHFLBW_BF16)
+                    ksplit_epilogue<__nv_bfloat16, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv,
+                                                                 recv_bar, ctile);
+                else
+                    ksplit_epilogue<__half, VS, KSF, VSF>(p, t_row, nkb, m, q, lane, n0, kr, vr, rows_s, recv, recv_bar,
+                                                          ctile);
+            } else {
+                if (p.c_dtype == SHFLBW_F32) epilogue_rows<float, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+                else if (p.c_dtype == SHFLBW_BF16)
+                    epilogue_rows<__nv_bfloat16, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+                else epilogue_rows<__half, VS>(p, t_row, nkb, m, q, lane, n0, rows_s, ctile);
+            }
         }
     }
     if (et == 0) trace_event(p.trace, 6);
@@ -643,11 +653,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 // Persistent variant: one CTA (cluster) per SM slot loops over (group,
 // column tile) units; the full/empty ring runs on across units and two TMEM
 // accumulators (ping-pong) let the epilogue of unit i overlap the loads and
-// MMAs of unit i+1.  Roles (320 threads): warp 0 weights + stage arming,
-// warp 1 TMEM + MMA, warps 2-5 activation gathers, warps 6-9 epilogue.
-// Used when the grid would need more than one wave of CTAs.
+// MMAs of unit i+1.  Roles (192 + 32 GW threads): warp 0 weights + stage
+// arming, warp 1 TMEM + MMA, warps 2..2+GW-1 activation gathers, the last 4
+// warps the epilogue.  Used when the grid would need more than one wave of
+// CTAs.
 // ===========================================================================
-constexpr int kThreadsPersist = 320;
 
 template <class OT, int VS>
 __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc, int nkb, int m, int q, int lane,
@@ -688,8 +698,8 @@ __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc,
     }
 }
 
-template <int DT, int VS, int CS, int KIND>
-__global__ void __launch_bounds__(kThreadsPersist, 2)
+template <int DT, int VS, int CS, int KIND, int GW>
+__global__ void __launch_bounds__(192 + 32 * GW, 2)
     k_spmm_persist(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW, TcParams p,
                    int units, int n_tiles) {
     using WL = WeightLayout<VS>;
@@ -805,15 +815,17 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
             }
         }
         __syncwarp();
-    } else if (warp < 6) {
+    } else if (warp < 2 + GW) {
         // ---------------- activation gathers ----------------
-        const int gw = warp - 2, et = threadIdx.x - 64;  // et 0..127
+        constexpr int kGT = 32 * GW;
+        const int gw = warp - 2, et = threadIdx.x - 64;  // et 0..kGT-1
         const int bw = KIND == 0 ? 64 : p.bw;
         const int nblk = kBlockN / bw;
         const int blk_bytes = kBlockK * bw * 2;
-        const int per_warp = 16 * nblk / kGatherWarps;
+        constexpr int kRGW = 16 / GW;  // row groups (4 rows) per warp in every MN block
+        const int per_warp = kRGW * nblk;
         const int gi = gw * per_warp + lane;
-        const int g_rg = gw * 4 + (lane & 3), g_b = lane >> 2;
+        const int g_rg = gw * kRGW + lane % kRGW, g_b = lane / kRGW;
         const bool t_issue = lane < per_warp && (!mcast || (gi % CS) == static_cast<int>(rank));
         // column-index windows: meta_s[buf] holds kMetaBlocks K blocks of a
         // unit; the first window of unit i+1 is prefetched (cp.async) into the
@@ -824,7 +836,7 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
             const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
             const int32_t* src = p.col_idx + gptr_s[gl] + kb0 * kBlockK;
             int32_t* dst = meta_s + buf * kMetaBlocks * kBlockK;
-            for (int x = et; x < nb * (kBlockK / 4); x += 128) {
+            for (int x = et; x < nb * (kBlockK / 4); x += kGT) {
                 if (async) cp_async16(smem_u32(dst + 4 * x), src + 4 * x, true);
                 else reinterpret_cast<int4*>(dst)[x] = conv_encode4<KIND>(p, reinterpret_cast<const int4*>(src)[x]);
             }
@@ -836,11 +848,11 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
                 const int nkb = (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK;
                 const int nb = nkb < kMetaBlocks ? nkb : kMetaBlocks;
                 int4* w = reinterpret_cast<int4*>(meta_s + buf * kMetaBlocks * kBlockK);
-                for (int x = et; x < nb * (kBlockK / 4); x += 128) w[x] = conv_encode4<KIND>(p, w[x]);
+                for (int x = et; x < nb * (kBlockK / 4); x += kGT) w[x] = conv_encode4<KIND>(p, w[x]);
             }
         };
         if (cid < units) load_window(cid, 0, 0, false);
-        asm volatile("bar.sync 2, 128;" ::: "memory");
+        named_bar<kGT>(2);
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
         int kbg = 0, i = 0;
@@ -869,9 +881,9 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
                 const int s = kbg % stages;
                 const int win = kb % kMetaBlocks;
                 if (win == 0 && kb > 0) {  // deep group: later windows of this unit, synchronously
-                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    named_bar<kGT>(2);
                     load_window(u, kb, buf, false);
-                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    named_bar<kGT>(2);
                 }
                 if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
                 if (t_issue) {
@@ -896,15 +908,15 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
                 __syncwarp();
             }
             cp_async_wait<0>();
-            asm volatile("bar.sync 2, 128;" ::: "memory");  // next unit's window visible; this buffer free
+            named_bar<kGT>(2);  // next unit's window visible; this buffer free
             if (KIND != 0 && un < units) {
                 encode_window(un, buf ^ 1);
-                asm volatile("bar.sync 2, 128;" ::: "memory");
+                named_bar<kGT>(2);
             }
         }
     } else {
         // ---------------- epilogue ----------------
-        const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - 192;
+        const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - (64 + 32 * GW);
         auto row_of = [&](int u, int v) -> int32_t {
             const int g = p.g_begin + u / n_tiles;
             return p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
@@ -944,7 +956,7 @@ __global__ void __launch_bounds__(kThreadsPersist, 2)
 
 int num_sms();
 
-template <int DT, int VS, int CS, int KIND, int KSPLIT>
+template <int DT, int VS, int CS, int KIND, int KSPLIT, int GW>
 int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
               cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
@@ -952,7 +964,7 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     const size_t recv = (CS > 1 && KSPLIT) ? static_cast<size_t>(KSF - 1) * (VS / KSF) * kBlockN * 4 : 0;
     const size_t smem = static_cast<size_t>(prm.stages) * kStage + recv + 1024 + kMetaBlocks * kBlockK * 4 +
                         (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 3) * 8 + 16;
-    auto kern = k_spmm_tc<DT, VS, CS, KIND, KSPLIT>;
+    auto kern = k_spmm_tc<DT, VS, CS, KIND, KSPLIT, GW>;
     static std::atomic<size_t> configured{0};  // per instantiation: raise the smem cap once
     if (smem > configured.load(std::memory_order_relaxed)) {
         SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -960,7 +972,7 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_tiles * CS, groups, 1);
-    cfg.blockDim = dim3(kThreadsTc, 1, 1);
+    cfg.blockDim = dim3(64 + 32 * GW, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -978,7 +990,7 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
 }
 
 
-template <int DT, int VS, int CS, int KIND>
+template <int DT, int VS, int CS, int KIND, int GW>
 int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
                    cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
@@ -987,7 +999,7 @@ int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParam
                         (prm.bulk_out ? static_cast<size_t>(VS) * kBlockN * out_esz : 0) + 1024 +
                         2 * kMetaBlocks * kBlockK * 4 + (VS < 4 ? 4 : VS) * 4 + ((groups + 2) & ~1) * 4 +
                         (2 * prm.stages + 5) * 8 + 16;
-    auto kern = k_spmm_persist<DT, VS, CS, KIND>;
+    auto kern = k_spmm_persist<DT, VS, CS, KIND, GW>;
     static std::atomic<size_t> configured{0};
     if (smem > configured.load(std::memory_order_relaxed)) {
         SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1001,7 +1013,7 @@ int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParam
     const int clusters = std::min(units, per_sm * num_sms() / CS);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(clusters * CS, 1, 1);
-    cfg.blockDim = dim3(kThreadsPersist, 1, 1);
+    cfg.blockDim = dim3(192 + 32 * GW, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -1018,25 +1030,43 @@ int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParam
     return SHFLBW_OK;
 }
 
+// gather warps per CTA (prm.gw): 4 or 8
+template <int DT, int VS, int CS, int KIND, int KSPLIT>
+int launch_tc_gw(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+                 cudaStream_t s) {
+    // (V = 128 K-split epilogues hold 128 fp32 partials per thread: they would
+    // spill at the 2-CTA register budget of 8 gather warps)
+    if constexpr (!(VS == 128 && KSPLIT != 0))
+        if (prm.gw == 8) return launch_tc<DT, VS, CS, KIND, KSPLIT, 8>(tmB, tmW, prm, n_tiles, groups, s);
+    return launch_tc<DT, VS, CS, KIND, KSPLIT, 4>(tmB, tmW, prm, n_tiles, groups, s);
+}
+
+template <int DT, int VS, int CS, int KIND>
+int launch_persist_gw(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+                      cudaStream_t s) {
+    if (prm.gw >= 8) return launch_persist<DT, VS, CS, KIND, 8>(tmB, tmW, prm, n_tiles, groups, s);
+    return launch_persist<DT, VS, CS, KIND, 4>(tmB, tmW, prm, n_tiles, groups, s);
+}
+
 // SpMM variants: V split (CS CTAs, multicast), K split, 2 x 2, persistent
 template <int DT, int VS>
 int dispatch_spmm(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles,
                   int groups, cudaStream_t s) {
     if (prm.persistent) {
         switch (cs) {
-            case 1: return launch_persist<DT, VS, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
-            case 2: return launch_persist<DT, VS, 2, 0>(tmB, tmW, prm, n_tiles, groups, s);
-            case 4: return launch_persist<DT, VS, 4, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 1: return launch_persist_gw<DT, VS, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 2: return launch_persist_gw<DT, VS, 2, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 4: return launch_persist_gw<DT, VS, 4, 0>(tmB, tmW, prm, n_tiles, groups, s);
         }
         return SHFLBW_UNSUPPORTED;
     }
     switch (cs * 2 + prm.ksplit) {
-        case 2: case 3: return launch_tc<DT, VS, 1, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 4: return launch_tc<DT, VS, 2, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 5: return launch_tc<DT, VS, 2, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
-        case 8: return launch_tc<DT, VS, 4, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 9: return launch_tc<DT, VS, 4, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
-        case 10: return launch_tc<DT, VS, 4, 0, 2>(tmB, tmW, prm, n_tiles, groups, s);
+        case 2: case 3: return launch_tc_gw<DT, VS, 1, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 4: return launch_tc_gw<DT, VS, 2, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 5: return launch_tc_gw<DT, VS, 2, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 8: return launch_tc_gw<DT, VS, 4, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 9: return launch_tc_gw<DT, VS, 4, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 10: return launch_tc_gw<DT, VS, 4, 0, 2>(tmB, tmW, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }
@@ -1047,11 +1077,11 @@ int dispatch_spmm(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const 
 template <int DT, int VS, int KIND>
 int dispatch_conv(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles,
                   int groups, cudaStream_t s) {
-    if (prm.persistent) return launch_persist<DT, VS, 1, KIND>(tmB, tmW, prm, n_tiles, groups, s);
+    if (prm.persistent) return launch_persist_gw<DT, VS, 1, KIND>(tmB, tmW, prm, n_tiles, groups, s);
     switch (cs * 2 + prm.ksplit) {
-        case 2: case 3: return launch_tc<DT, VS, 1, KIND, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 5: return launch_tc<DT, VS, 2, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
-        case 9: return launch_tc<DT, VS, 4, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 2: case 3: return launch_tc_gw<DT, VS, 1, KIND, 0>(tmB, tmW, prm, n_tiles, groups, s);
+        case 5: return launch_tc_gw<DT, VS, 2, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 9: return launch_tc_gw<DT, VS, 4, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }

@@ -8,13 +8,18 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "scripts"))
 import torch  # noqa: E402
 
+import paper_2203_05016_b200 as sb  # noqa: E402
 import sweep  # noqa: E402
 
 dev = torch.device("cuda", 0)
+for kv in [x for x in os.environ.get("SBW_OPTS", "").split(",") if x]:  # e.g. SBW_OPTS=gather_warps=8
+    k, v = kv.split("=")
+    sb.set_option(k, int(v))
 only = sys.argv[1].split(",") if len(sys.argv) > 1 else ["ns", "ffn2", "gnmt90", "conv56", "conv14"]
 cases = {
     "ns": lambda: sweep.spmm_row("ns", 2048, 128, 2048, 64, 0.25, 2000, dev),
     "ffn2": lambda: sweep.spmm_row("ffn2", 512, 4096, 2048, 64, 0.25, 1000, dev),
+    "ffn1": lambda: sweep.spmm_row("ffn1", 2048, 4096, 512, 64, 0.25, 1000, dev),
     "ffn1_50": lambda: sweep.spmm_row("ffn1_50", 2048, 4096, 512, 64, 0.5, 1000, dev),
     "ffn2_v32": lambda: sweep.spmm_row("ffn2_v32", 512, 4096, 2048, 32, 0.25, 1000, dev),
     "gnmt90": lambda: sweep.spmm_row("gnmt90", 4096, 128, 1024, 64, 0.1, 2000, dev),

@@ -12,6 +12,8 @@ are identical and every product is exact in fp32.  Bars:
 """
 import hashlib
 
+import os
+
 import numpy as np
 import pytest
 
@@ -29,7 +31,8 @@ def sb():
         pytest.skip("no CUDA device")
     import paper_2203_05016_b200 as sb
     for k, v in (("force_simt", 0), ("split", 0), ("stages", 0), ("split_mode", 0), ("cp_async_slabs", 0),
-                 ("persistent", 0), ("no_bulk_out", 0)):
+                 ("persistent", 0), ("no_bulk_out", 0),
+                 ("gather_warps", int(os.environ.get("SBW_GATHER_WARPS", "0")))):  # env: run the suite at 4 / 8
         sb.set_option(k, v)
     return sb
 
@@ -838,3 +841,54 @@ def test_prune_errors(sb):
         sb.kept_score(bad, torch.ones((8, 8), dtype=torch.uint8, device="cuda"))
     w = torch.tensor([[-3.0, 2.0]], device="cuda")
     assert sb.importance_scores(w).cpu().tolist() == [[3.0, 2.0]]
+
+
+@pytest.mark.parametrize("M,N,K,V,alpha,split,mode,persistent",
+                         [(2048, 128, 2048, 64, 0.25, 0, 0, 0), (2048, 128, 2048, 64, 0.25, 2, 1, 0),
+                          (2048, 128, 2048, 64, 0.25, 4, 3, 0), (1024, 384, 1024, 32, 0.3, 0, 0, -1),
+                          (512, 1000, 700, 128, 0.3, 0, 0, -1), (2048, 2048, 512, 64, 0.25, 0, 0, 2),
+                          (512, 520, 300, 16, 0.5, 0, 0, 1)])
+def test_gather_warps_bitwise(sb, oracle, M, N, K, V, alpha, split, mode, persistent):
+    """4 or 8 gather-issuing warps per CTA only change who issues which
+    gather4: identical bits in every kernel variant (V/K/2x2 splits,
+    persistent), fp32 and bf16 out."""
+    mask, W, B = synthetic(oracle, M, K, N, V, alpha)
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("split", split)
+    sb.set_option("split_mode", mode)
+    sb.set_option("persistent", persistent)
+    outs = {}
+    for gw in (4, 8):
+        sb.set_option("gather_warps", gw)
+        outs[gw] = (sb.spmm_execute(a, Bd).cpu().numpy(),
+                    sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
+    for k, v in (("split", 0), ("split_mode", 0), ("persistent", 0), ("gather_warps", 0)):
+        sb.set_option(k, v)
+    assert oracle.rel_frobenius(outs[4][0], oracle.spmm(p, B)) <= TOL
+    for gw in (8,):
+        assert np.array_equal(outs[gw][0], outs[4][0]) and np.array_equal(outs[gw][1], outs[4][1]), gw
+
+
+@pytest.mark.parametrize("prepared", [False, True])
+def test_gather_warps_conv_bitwise(sb, oracle, prepared):
+    C, H, Kf, R, pad, V, Nb = 64, 14, 128, 3, 1, 64, 32
+    mask, Wt, x = _conv_setup(oracle, C, H, H, Kf, R, R, V, Nb, seed=13)
+    w = sb.compress_shflbw(dev(Wt), dev(mask), V)
+    if prepared:
+        w = sb.conv_prepare(w, R)
+    xd = dev(x, torch.bfloat16)
+    geo = sb.ConvGeometry(R, R, 1, pad)
+    want = oracle.conv2d(oracle.compress(Wt, mask, V), x, R, R, 1, pad)
+    outs = {}
+    for persistent in (-1, 2):
+        sb.set_option("persistent", persistent)
+        for gw in (4, 8):
+            sb.set_option("gather_warps", gw)
+            outs[(persistent, gw)] = sb.conv2d(w, xd, geo).cpu().numpy()
+    sb.set_option("persistent", 0)
+    sb.set_option("gather_warps", 0)
+    ref = outs[(-1, 4)]
+    assert oracle.rel_frobenius(ref, want) <= TOL
+    for k, v in outs.items():
+        assert np.array_equal(v, ref), k
