@@ -234,6 +234,8 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.S = b.S;
     prm.inv_rs = 1.0f / static_cast<float>(prm.RS > 0 ? prm.RS : 1);
     prm.inv_s = 1.0f / static_cast<float>(b.S > 0 ? b.S : 1);
+    prm.inv_nb = 1.0 / static_cast<double>(b.Nb > 0 ? b.Nb : 1);
+    prm.inv_q = 1.0 / static_cast<double>(b.Q > 0 ? b.Q : 1);
     prm.stride = b.stride;
     prm.pad = b.pad;
     prm.Q = b.Q;

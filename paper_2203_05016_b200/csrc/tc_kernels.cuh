@@ -80,6 +80,7 @@ struct TcParams {
     // implicit-GEMM conv geometry (KIND 1)
     int Nb, H, W, RS, S, stride, pad, Q, PQ;
     float inv_rs, inv_s;  // 1/RS, 1/S for fdiv (column ids < 2^22, checked on the host)
+    double inv_nb, inv_q;  // 1/Nb, 1/Q for ddiv (persistent conv unit positions)
     int ksplit;      // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
     int per_sm;      // persistent: resident CTAs per SM
@@ -483,14 +484,16 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     if (warp == 0) {
         // ---------------- stage bookkeeping + weights ----------------
         if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;  // ring slot and round parity (no runtime division by `stages`)
             for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % stages;
-                if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+                if (kb >= stages) mbar_wait(&empty[s], ph ^ 1);
                 mbar_arrive_expect_tx(&full[s], (2 - cps) * (kABytes / 2) + WL::kBytes);
 #pragma unroll
                 for (int sl = 0; sl < WL::kSlabs; ++sl)
                     tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
                                 vbase + sl * 64, gp + (kbase + kb) * kBlockK);
+                if (++s == stages) s = 0, ph ^= 1;
             }
         }
         __syncwarp();
@@ -500,9 +503,10 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
         const uint32_t a_row = static_cast<uint32_t>(p.bw) * 2;
         const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
         if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
             for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % stages;
-                mbar_wait(&full[s], (kb / stages) & 1);
+                mbar_wait(&full[s], ph);
                 tc_fence_after();
                 if (kb == 0) trace_event(p.trace, 3);
                 if (kb < 8) trace_event(p.trace, 8 + kb);
@@ -518,6 +522,7 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
                 }
                 if constexpr (!mcast) umma_commit(&empty[s]);
                 else umma_commit_mc(&empty[s], cmask);
+                if (++s == stages) s = 0, ph ^= 1;
             }
             trace_event(p.trace, 4);
             if (nkb > 0) umma_commit(accum);
@@ -558,15 +563,16 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
         const uint32_t meta_u32 = smem_u32(meta_s);
+        int s = 0;
+        uint32_t ph = 0;
         for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % stages;
             const int win = kb % kMetaBlocks;
             if (win == 0 && kb > 0) {
                 named_bar<kGT>(2);  // all done with the old window
                 stage_meta(kb);
                 named_bar<kGT>(2);
             }
-            if (kb >= stages) mbar_wait(&empty[s], ((kb / stages) & 1) ^ 1);
+            if (kb >= stages) mbar_wait(&empty[s], ph ^ 1);
             if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
             unsigned char* a_st = smem + s * kStageBytes;
             const int32_t* mk = meta_s + win * kBlockK;
@@ -604,6 +610,7 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
                 cp_async_arrive_noinc(&full[s]);
             }
             __syncwarp();
+            if (++s == stages) s = 0, ph ^= 1;
         }
         if (gw < 4) {  // warps 2-5 run the epilogue; any further gather warps are done
             // output row map for the epilogue, loaded while the MMAs run
@@ -658,6 +665,31 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
 // warps the epilogue.  Used when the grid would need more than one wave of
 // CTAs.
 // ===========================================================================
+
+// (group, column tile) of the units a persistent CTA visits: units advance by
+// a fixed stride (the cluster count), so the pair is stepped with adds -- the
+// divisions happen once per role, not at every unit boundary.
+struct UnitCursor {
+    int u, gl, tile;  // unit, launch-relative group, column tile
+    int stride, step_g, step_t, n_tiles;
+    __device__ __forceinline__ UnitCursor(int u0, int stride_, int nt) : u(u0), stride(stride_), n_tiles(nt) {
+        gl = u0 / nt;
+        tile = u0 - gl * nt;
+        step_g = stride_ / nt;
+        step_t = stride_ - step_g * nt;
+    }
+    __device__ __forceinline__ void next() {
+        u += stride;
+        gl += step_g;
+        tile += step_t;
+        if (tile >= n_tiles) tile -= n_tiles, ++gl;
+    }
+};
+
+// c / d for 0 <= c < 2^31 with inv = 1.0 / d (d < 2^20): exact, like fdiv
+__device__ __forceinline__ int ddiv(int c, double inv) {
+    return __double2int_rz((static_cast<double>(c) + 0.5) * inv);
+}
 
 template <class OT, int VS>
 __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc, int nkb, int m, int q, int lane,
@@ -758,24 +790,25 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         grid_launch_dependents();
         trace_event(p.trace, 1);
     }
-    auto unit_nkb = [&](int u) { const int gl = u / n_tiles; return (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK; };
+    auto group_nkb = [&](int gl) { return (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK; };
 
     if (warp == 0) {
         // ---------------- stage arming + weights ----------------
         if (lane == 0) {
-            int kbg = 0;
-            for (int u = cid; u < units; u += nclusters) {
-                const int gl = u / n_tiles;
+            int kbg = 0, s = 0;
+            uint32_t ph = 0;  // ring slot and round parity, carried across units
+            for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next()) {
+                const int gl = c.gl;
                 const int gp = gptr_s[gl];
                 const int nkb = (gptr_s[gl + 1] - gp) / kBlockK;
                 for (int kb = 0; kb < nkb; ++kb, ++kbg) {
-                    const int s = kbg % stages;
-                    if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
+                    if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&full[s], kStageBytes);
 #pragma unroll
                     for (int sl = 0; sl < WL::kSlabs; ++sl)
                         tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
                                     vbase + sl * 64, gp + kb * kBlockK);
+                    if (++s == stages) s = 0, ph ^= 1;
                 }
             }
         }
@@ -785,17 +818,17 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         const uint32_t a_row = KIND == 0 ? 128u : static_cast<uint32_t>(p.bw) * 2;
         const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
         if (lane == 0) {
-            int kbg = 0, i = 0;
-            for (int u = cid; u < units; u += nclusters, ++i) {
-                const int nkb = unit_nkb(u);
+            int s = 0, i = 0;
+            uint32_t ph = 0;
+            for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next(), ++i) {
+                const int nkb = group_nkb(c.gl);
                 const int b = i & 1;
                 mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
                 tc_fence_after();
                 if (i < 8) trace_event(p.trace, 8 + i);  // MMA: accumulator free for unit i
                 const uint32_t tmem_d = tmem_base + b * kAccCols;
-                for (int kb = 0; kb < nkb; ++kb, ++kbg) {
-                    const int s = kbg % stages;
-                    mbar_wait(&full[s], (kbg / stages) & 1);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
                     const uint32_t w_addr = a_addr + kABytes;
@@ -809,6 +842,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                     }
                     if constexpr (!mcast) umma_commit(&empty[s]);
                     else umma_commit_mc(&empty[s], cmask);
+                    if (++s == stages) s = 0, ph ^= 1;
                 }
                 if (nkb > 0) umma_commit(&acc_full[b]);
                 else mbar_arrive(&acc_full[b]);
@@ -830,8 +864,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         // column-index windows: meta_s[buf] holds kMetaBlocks K blocks of a
         // unit; the first window of unit i+1 is prefetched (cp.async) into the
         // other buffer while unit i issues its gathers
-        auto load_window = [&](int u, int kb0, int buf, bool async) {
-            const int gl = u / n_tiles;
+        auto load_window = [&](int gl, int kb0, int buf, bool async) {
             const int nkb = (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK;
             const int nb = nkb - kb0 < kMetaBlocks ? nkb - kb0 : kMetaBlocks;
             const int32_t* src = p.col_idx + gptr_s[gl] + kb0 * kBlockK;
@@ -842,50 +875,54 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
             }
         };
         // conv: encode a window that arrived raw through cp.async (in place)
-        auto encode_window = [&](int u, int buf) {
+        auto encode_window = [&](int gl, int buf) {
             if constexpr (KIND != 0) {
-                const int gl = u / n_tiles;
                 const int nkb = (gptr_s[gl + 1] - gptr_s[gl]) / kBlockK;
                 const int nb = nkb < kMetaBlocks ? nkb : kMetaBlocks;
                 int4* w = reinterpret_cast<int4*>(meta_s + buf * kMetaBlocks * kBlockK);
                 for (int x = et; x < nb * (kBlockK / 4); x += kGT) w[x] = conv_encode4<KIND>(p, w[x]);
             }
         };
-        if (cid < units) load_window(cid, 0, 0, false);
+        if (cid < units) load_window(cid / n_tiles, 0, 0, false);
         named_bar<kGT>(2);
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
-        int kbg = 0, i = 0;
-        for (int u = cid; u < units; u += nclusters, ++i) {
-            const int buf = i & 1;
+        int kbg = 0, i = 0, s = 0, buf = 0;
+        uint32_t ph = 0;
+        for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next(), ++i) {
             if (et == 0 && i < 8) trace_event(p.trace, 16 + i);  // gathers: unit i starts issuing
-            const int un = u + nclusters;
-            if (un < units) {  // the other buffer was released by the bar.sync ending unit i-1
-                load_window(un, 0, buf ^ 1, true);
+            UnitCursor cn = c;
+            cn.next();
+            const bool more = cn.u < units;
+            const int nkb = group_nkb(c.gl);
+            // the next unit reads the same single window (same group, <= kMetaBlocks
+            // K blocks, e.g. every unit of a one-group conv): keep it, no reload/sync
+            const bool keep = more && cn.gl == c.gl && nkb <= kMetaBlocks;
+            if (more && !keep) {  // the other buffer was released by the bar.sync ending unit i-1
+                load_window(cn.gl, 0, buf ^ 1, true);
                 cp_async_commit();
             }
-            const int n0 = (u % n_tiles) * kBlockN;
-            const int nkb = unit_nkb(u);
+            const int n0 = c.tile * kBlockN;
             const int32_t* mbuf = meta_s + buf * kMetaBlocks * kBlockK;
             int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
             bool g_pos_ok = true;
             if (KIND == 1 || KIND == 2) {
                 const int base_n = n0 + g_b * p.bw;
-                const int pos = base_n / p.Nb;
+                const int pos = ddiv(base_n, p.inv_nb);
                 g_x = base_n - pos * p.Nb;
                 g_pos_ok = pos < p.PQ;
-                g_p0 = (pos / p.Q) * p.stride - p.pad;
-                g_q0 = (pos % p.Q) * p.stride - p.pad;
+                const int pr = ddiv(pos, p.inv_q);
+                g_p0 = pr * p.stride - p.pad;
+                g_q0 = (pos - pr * p.Q) * p.stride - p.pad;
             }
             for (int kb = 0; kb < nkb; ++kb, ++kbg) {
-                const int s = kbg % stages;
                 const int win = kb % kMetaBlocks;
                 if (win == 0 && kb > 0) {  // deep group: later windows of this unit, synchronously
                     named_bar<kGT>(2);
-                    load_window(u, kb, buf, false);
+                    load_window(c.gl, kb, buf, false);
                     named_bar<kGT>(2);
                 }
-                if (kbg >= stages) mbar_wait(&empty[s], ((kbg / stages) & 1) ^ 1);
+                if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
                 if (t_issue) {
                     int4 ci;
                     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -906,33 +943,41 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                         tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci.x, ci.y, ci.z, ci.w);
                 }
                 __syncwarp();
+                if (++s == stages) s = 0, ph ^= 1;
             }
-            cp_async_wait<0>();
-            named_bar<kGT>(2);  // next unit's window visible; this buffer free
-            if (KIND != 0 && un < units) {
-                encode_window(un, buf ^ 1);
-                named_bar<kGT>(2);
+            if (!keep) {
+                cp_async_wait<0>();
+                named_bar<kGT>(2);  // next unit's window visible; this buffer free
+                if (KIND != 0 && more) {
+                    encode_window(cn.gl, buf ^ 1);
+                    named_bar<kGT>(2);
+                }
+                buf ^= 1;
             }
         }
     } else {
         // ---------------- epilogue ----------------
         const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - (64 + 32 * GW);
-        auto row_of = [&](int u, int v) -> int32_t {
-            const int g = p.g_begin + u / n_tiles;
+        auto row_of = [&](int gl, int v) -> int32_t {
+            const int g = p.g_begin + gl;
             return p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
                              : p.row_indices[static_cast<int64_t>(g) * p.V + vbase + v];
         };
-        int32_t next_row = (cid < units && et < VS) ? row_of(cid, et) : 0;  // static: before the wait
+        int32_t next_row = (cid < units && et < VS) ? row_of(cid / n_tiles, et) : 0;  // static: before the wait
         grid_dependency_wait();  // C may still be read by the previous kernel
         int i = 0;
-        for (int u = cid; u < units; u += nclusters, ++i) {
-            const int n0 = (u % n_tiles) * kBlockN;
-            const int nkb = unit_nkb(u);
+        for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next(), ++i) {
+            const int n0 = c.tile * kBlockN;
+            const int nkb = group_nkb(c.gl);
             const int b = i & 1;
             asm volatile("bar.sync 3, 128;" ::: "memory");  // previous unit done with rows_s / ctile
             if (et < VS) rows_s[et] = next_row;
             asm volatile("bar.sync 3, 128;" ::: "memory");
-            if (u + nclusters < units && et < VS) next_row = row_of(u + nclusters, et);  // in flight meanwhile
+            if (c.u + nclusters < units && et < VS) {  // in flight meanwhile
+                UnitCursor cn = c;
+                cn.next();
+                next_row = row_of(cn.gl, et);
+            }
             mbar_wait(&acc_full[b], (i >> 1) & 1);
             tc_fence_after();
             if (et == 0 && i < 8) trace_event(p.trace, 24 + i);  // epilogue: unit i accumulated
