@@ -234,8 +234,10 @@ int shflbw_cu_conv2d(const shflbw_cu_matrix* w, const void* input, int32_t C, in
     Operand b;
     // 128-byte activation rows when the weight is in conv order for this S
     const int ppb = Nb > 0 ? 64 / Nb : 0;  // output positions per 64-element row
+    // (an output width Q that is not a multiple of ppb runs on a padded
+    // position grid, spmm_sm100.cu)
     const bool wide = (w->reserved & SHFLBW_CONV_ORDER) && SHFLBW_CONV_ORDER_S(w->reserved) == S && stride == 1 &&
-                      (Nb == 16 || Nb == 32) && Q % ppb == 0 && (static_cast<int64_t>(C) * H < (1LL << 31));
+                      (Nb == 16 || Nb == 32) && ppb > 0 && (static_cast<int64_t>(C) * H < (1LL << 31));
     b.kind = wide ? 2 : 1;
     b.ptr = input;
     b.K = w->cols;

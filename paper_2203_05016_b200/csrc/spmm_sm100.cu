@@ -144,7 +144,14 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     const int groups = g_end - g_begin;
     if (groups <= 0) return SHFLBW_OK;
     if (groups > 65535) return SHFLBW_UNSUPPORTED;
-    const int n_tiles = (b.N + kBlockN - 1) / kBlockN;
+    // conv KIND 2 with Q not a multiple of the positions per 64-element
+    // activation row: GEMM over a P x qp position grid, padding dropped in the
+    // epilogue (TcParams::remap)
+    const int ppb = b.kind == 2 ? 64 / b.Nb : 1;
+    const int qp = b.kind == 2 ? (b.Q + ppb - 1) / ppb * ppb : b.Q;
+    const int64_t n_gemm = b.kind == 2 ? static_cast<int64_t>(b.P) * qp * b.Nb : b.N;
+    if (n_gemm > 0x7fffff00LL) return SHFLBW_UNSUPPORTED;
+    const int n_tiles = static_cast<int>((n_gemm + kBlockN - 1) / kBlockN);
 
     // Cluster split for grids that would leave SMs idle: CS CTAs share one
     // (group, column tile).  Each SM fills its activation tiles at the TMA
@@ -221,7 +228,10 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.ldc = c.ldc;
     prm.V = V;
     prm.g_begin = g_begin;
-    prm.N = b.N;
+    prm.N = static_cast<int>(n_gemm);
+    prm.qp = qp;
+    prm.remap = qp != b.Q ? 1 : 0;
+    prm.nb_log2 = b.Nb == 16 ? 4 : 5;  // KIND 2: Nb in {16, 32}
     prm.c_dtype = c.dtype;
     prm.compact = c.compact;
     prm.B = b.ptr;
@@ -235,11 +245,11 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.inv_rs = 1.0f / static_cast<float>(prm.RS > 0 ? prm.RS : 1);
     prm.inv_s = 1.0f / static_cast<float>(b.S > 0 ? b.S : 1);
     prm.inv_nb = 1.0 / static_cast<double>(b.Nb > 0 ? b.Nb : 1);
-    prm.inv_q = 1.0 / static_cast<double>(b.Q > 0 ? b.Q : 1);
+    prm.inv_qp = 1.0 / static_cast<double>(qp > 0 ? qp : 1);
     prm.stride = b.stride;
     prm.pad = b.pad;
     prm.Q = b.Q;
-    prm.PQ = b.P * b.Q;
+    prm.PQ = b.P * qp;
     prm.ksplit = hybrid ? 2 : ((cs > 1 && (!vsplit || conv_ksplit)) ? 1 : 0);
     prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
     if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
@@ -254,11 +264,12 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     // "persistent": -1 never, 1 always, 0 auto)
     {
         // "persistent": N > 0 -> persistent kernel with N CTAs per SM, -1 never,
-        // 0 auto: 2 per SM once the grid holds >= 2 full waves of units (the
-        // per-CTA prologue/epilogue then no longer hides behind the co-resident
-        // CTA; measured)
+        // 0 auto: 2 per SM once the units exceed one wave of 2 CTAs per SM
+        // (a partial second wave of one-unit CTAs costs a whole CTA lifetime:
+        // ResNet 3x3 @28, 392 units, 12.4 -> 11.8 us; below that the one-CTA-
+        // per-unit kernel wins: FFN2 N=4096 256 units 7.4 vs 8.3 us)
         int64_t opt = option("persistent");
-        if (opt == 0) opt = (units * cs >= 4LL * num_sms()) ? 2 : -1;
+        if (opt == 0) opt = (units * cs > 2LL * num_sms()) ? 2 : -1;
         prm.persistent = !prm.ksplit && opt > 0 && groups <= 4096 ? 1 : 0;
         prm.per_sm = static_cast<int>(std::min<int64_t>(2, std::max<int64_t>(1, opt)));  // launch bounds: 2
     }

@@ -80,7 +80,11 @@ struct TcParams {
     // implicit-GEMM conv geometry (KIND 1)
     int Nb, H, W, RS, S, stride, pad, Q, PQ;
     float inv_rs, inv_s;  // 1/RS, 1/S for fdiv (column ids < 2^22, checked on the host)
-    double inv_nb, inv_q;  // 1/Nb, 1/Q for ddiv (persistent conv unit positions)
+    double inv_nb, inv_qp;  // 1/Nb, 1/qp for ddiv (conv unit positions)
+    // conv KIND 2 with an odd output width: the GEMM runs over a position grid
+    // P x qp (qp = Q rounded up to the positions per 64-element activation row),
+    // the epilogue drops the qp - Q padding positions (remap = 1)
+    int qp, remap, nb_log2;
     int ksplit;      // 1: the CS CTAs of a cluster split the K blocks (partials reduced via DSMEM)
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
     int per_sm;      // persistent: resident CTAs per SM
@@ -128,6 +132,21 @@ __device__ __forceinline__ void grid_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+// c / d for 0 <= c < 2^31 with inv = 1.0 / d (d < 2^20): exact, like fdiv
+__device__ __forceinline__ int ddiv(int c, double inv) {
+    return __double2int_rz((static_cast<double>(c) + 0.5) * inv);
+}
+
+// Output column of GEMM column n (-1: beyond N or a padding position).
+__device__ __forceinline__ int64_t out_col(const TcParams& p, int n) {
+    if (n >= p.N) return -1;
+    if (!p.remap) return n;
+    const int pos = n >> p.nb_log2, b = n & (p.Nb - 1);
+    const int pr = ddiv(pos, p.inv_qp), q = pos - pr * p.qp;
+    if (q >= p.Q) return -1;
+    return (static_cast<int64_t>(pr) * p.Q + q) * p.Nb + b;
+}
+
 template <class OT> __device__ __forceinline__ OT to_out(float x);
 template <> __device__ __forceinline__ float to_out<float>(float x) { return x; }
 template <> __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
@@ -143,10 +162,10 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
     constexpr int kRowsPerInst = 32 / kLanesPerRow;
     constexpr int kIters = (ROWS + 4 * kRowsPerInst - 1) / (4 * kRowsPerInst);
     const int chunk = lane % kLanesPerRow;
-    const int nn = n0 + chunk * (16 / esz);
+    const int64_t nn = out_col(p, n0 + chunk * (16 / esz));  // a 16-byte chunk never spans two positions
     const int v0 = q * kRowsPerInst + lane / kLanesPerRow;
     if (!BATCH) {  // interleaved: fewer live registers (the persistent kernel's epilogue warps)
-        if (nn < p.N) {
+        if (nn >= 0) {
             // explicit ld.shared, volatile so it stays after the bar.sync above
             // but without a memory clobber, so the compiler may start the next
             // row's reads before this row's global store
@@ -165,7 +184,7 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
         }
         return;
     }
-    if (nn < p.N) {
+    if (nn >= 0) {
         // all shared-memory reads first (explicit ld.shared, so no store below
         // can alias them), then the global stores
         int4 x[kIters];
@@ -197,8 +216,8 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
 template <class OT, int VS>
 __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row, int nkb, int m, int q, int lane,
                                               int n0, const int32_t* rows_s, unsigned char* ctile) {
-    const int n = n0 + m;
-    const bool live = n < p.N;
+    const int64_t n = out_col(p, n0 + m);
+    const bool live = n >= 0;
 #pragma unroll
     for (int c = 0; c < (VS + 31) / 32; ++c) {
         constexpr int kW = VS < 32 ? VS : 32;
@@ -308,13 +327,13 @@ __device__ __forceinline__ void ksplit_epilogue(const TcParams& p, uint32_t t_ro
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (m == 0) trace_event(p.trace, 27);
         store_tile_rows<OT, kRP>(p, ctile, rows_s + kr * kRP, q, lane, n0);
-    } else if (n0 + m < p.N) {
+    } else if (const int64_t n = out_col(p, n0 + m); n >= 0) {
         int32_t row[kRP];
 #pragma unroll
         for (int i = 0; i < kRP; ++i) row[i] = rows_s[kr * kRP + i];
 #pragma unroll
         for (int i = 0; i < kRP; ++i)
-            static_cast<OT*>(p.C)[static_cast<int64_t>(row[i]) * p.ldc + n0 + m] = to_out<OT>(res[i]);
+            static_cast<OT*>(p.C)[static_cast<int64_t>(row[i]) * p.ldc + n] = to_out<OT>(res[i]);
     }
     if (m == 0) trace_event(p.trace, 28);
 }
@@ -552,8 +571,8 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
             const int pos = base_n / p.Nb;
             g_x = base_n - pos * p.Nb;
             g_pos_ok = pos < p.PQ;
-            g_p0 = (pos / p.Q) * p.stride - p.pad;
-            g_q0 = (pos % p.Q) * p.stride - p.pad;
+            g_p0 = (pos / p.qp) * p.stride - p.pad;
+            g_q0 = (pos % p.qp) * p.stride - p.pad;
         }
         // cp.async part (SpMM only): slabs [2-cps, 2): cps*512 16-byte chunks per K block
         const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
@@ -686,17 +705,13 @@ struct UnitCursor {
     }
 };
 
-// c / d for 0 <= c < 2^31 with inv = 1.0 / d (d < 2^20): exact, like fdiv
-__device__ __forceinline__ int ddiv(int c, double inv) {
-    return __double2int_rz((static_cast<double>(c) + 0.5) * inv);
-}
 
 template <class OT, int VS>
 __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc, int nkb, int m, int q, int lane,
                                               int n0, const int32_t* rows_s, unsigned char* ctile,
                                               uint64_t* acc_empty) {
-    const int n = n0 + m;
-    const bool live = n < p.N;
+    const int64_t n = out_col(p, n0 + m);
+    const bool live = n >= 0;
 #pragma unroll
     for (int c = 0; c < (VS + 31) / 32; ++c) {
         constexpr int kW = VS < 32 ? VS : 32;
@@ -911,9 +926,9 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                 const int pos = ddiv(base_n, p.inv_nb);
                 g_x = base_n - pos * p.Nb;
                 g_pos_ok = pos < p.PQ;
-                const int pr = ddiv(pos, p.inv_q);
+                const int pr = ddiv(pos, p.inv_qp);
                 g_p0 = pr * p.stride - p.pad;
-                g_q0 = (pos - pr * p.Q) * p.stride - p.pad;
+                g_q0 = (pos - pr * p.qp) * p.stride - p.pad;
             }
             for (int kb = 0; kb < nkb; ++kb, ++kbg) {
                 const int win = kb % kMetaBlocks;

@@ -17,7 +17,7 @@ import bench  # noqa: E402
 import paper_2203_05016_b200 as sb  # noqa: E402
 
 CONV = {"conv56": (64, 56, 64, 3, 1, 32, 64, 0.25), "conv28": (128, 28, 128, 3, 1, 32, 64, 0.25),
-        "conv14": (256, 14, 256, 3, 1, 32, 64, 0.25)}
+        "conv14": (256, 14, 256, 3, 1, 32, 64, 0.25), "conv7": (512, 7, 512, 3, 1, 32, 64, 0.25)}
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="conv56")
 ap.add_argument("--opts", default="")

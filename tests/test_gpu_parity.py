@@ -650,7 +650,9 @@ def test_conv_prepare_layout(sb, oracle):
 @pytest.mark.parametrize("C,H,Wd,Kf,R,pad,V,Nb", [
     (16, 8, 8, 64, 3, 1, 64, 32),     # 128-byte rows: 2 positions x 32
     (8, 6, 12, 64, 3, 1, 32, 16),     # 4 positions x 16, H != W
-    (8, 7, 7, 64, 3, 1, 64, 32),      # Q odd: falls back to one position per row
+    (8, 7, 7, 64, 3, 1, 64, 32),      # Q odd: padded position grid (qp = 8), padding dropped in the epilogue
+    (16, 6, 6, 64, 3, 1, 64, 16),     # Nb = 16: 4 positions per row, Q = 6 -> qp = 8
+    (8, 9, 5, 64, 3, 1, 64, 32),      # Q = 5, H != W
     (12, 9, 9, 128, 3, 0, 64, 32),    # no padding
     (4, 10, 10, 64, 5, 2, 16, 32),    # 5x5 filter (S = 5)
     (64, 14, 14, 128, 3, 1, 64, 32),  # ResNet-like
