@@ -154,9 +154,10 @@ template <> __device__ __forceinline__ __half to_out<__half>(float x) { return _
 
 // Coalesced 16-byte stores of a staged [ROWS][128] tile of OT through the row
 // map: one output row = 128*sizeof(OT) bytes, 16 or 32 lanes per row.
-template <class OT, int ROWS, bool BATCH = true>
+template <class OT, int ROWS, bool BATCH = true, bool SWZ = false>
 __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigned char* ctile, const int32_t* rows,
                                                 int q, int lane, int n0) {
+    // SWZ: row v's 16-byte chunk c sits at chunk c ^ (v & 7) (stage_tile_stmatrix)
     constexpr int esz = sizeof(OT);
     constexpr int kLanesPerRow = kBlockN * esz / 16;  // 16 (bf16/f16) or 32 (f32)
     constexpr int kRowsPerInst = 32 / kLanesPerRow;
@@ -169,15 +170,16 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
             // explicit ld.shared, volatile so it stays after the bar.sync above
             // but without a memory clobber, so the compiler may start the next
             // row's reads before this row's global store
-            const uint32_t base = smem_u32(ctile) + static_cast<uint32_t>(chunk * 16);
+            const uint32_t cb = smem_u32(ctile);
             const uint32_t rbase = smem_u32(rows);
 #pragma unroll 4
             for (int v = v0; v < ROWS; v += 4 * kRowsPerInst) {
                 int4 x;
                 int32_t row;
+                const int pc = SWZ ? (chunk ^ (v & 7)) : chunk;
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
-                             : "r"(base + static_cast<uint32_t>(v * kBlockN * esz)));
+                             : "r"(cb + static_cast<uint32_t>(v * kBlockN * esz + pc * 16)));
                 asm volatile("ld.shared.b32 %0, [%1];" : "=r"(row) : "r"(rbase + static_cast<uint32_t>(v * 4)));
                 *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(row) * p.ldc + nn) * esz) = x;
             }
@@ -189,14 +191,15 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
         // can alias them), then the global stores
         int4 x[kIters];
         int32_t row[kIters];
-        const uint32_t base = smem_u32(ctile) + static_cast<uint32_t>(chunk * 16);
+        const uint32_t cb = smem_u32(ctile);
 #pragma unroll
         for (int k = 0; k < kIters; ++k) {
             const int v = v0 + k * 4 * kRowsPerInst;
             if (v < ROWS) {
+                const int pc = SWZ ? (chunk ^ (v & 7)) : chunk;
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(x[k].x), "=r"(x[k].y), "=r"(x[k].z), "=r"(x[k].w)
-                             : "r"(base + static_cast<uint32_t>(v * kBlockN * esz)));
+                             : "r"(cb + static_cast<uint32_t>(v * kBlockN * esz + pc * 16)));
                 row[k] = rows[v];
             }
         }
@@ -210,12 +213,73 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
     }
 }
 
+template <class OT> __device__ __forceinline__ uint32_t pack2(uint32_t lo, uint32_t hi);
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(uint32_t lo, uint32_t hi) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+template <> __device__ __forceinline__ uint32_t pack2<__half>(uint32_t lo, uint32_t hi) {
+    const __half2 h = __floats2half2_rn(__uint_as_float(lo), __uint_as_float(hi));
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// 16-bit output tile staged with stmatrix: TMEM (lane = output column n,
+// column = output row v) is read in the 16x256b accumulator-fragment layout,
+// converted to bf16/f16 pairs along v and stored as transposed 8x8 blocks --
+// rows v of 8 consecutive n (16 bytes) -- into ctile [VS][128] with the 16-byte
+// chunk index XOR (v & 7) (conflict-free stores and row reads).  8 stmatrix.x4
+// per warp for VS = 64 instead of 64 two-byte st.shared per thread.
+// t_quarter = the accumulator's TMEM address at this warp's lane quarter q.
+template <class OT, int VS>
+__device__ __forceinline__ void stage_tile_stmatrix(uint32_t t_quarter, int nkb, int q, int lane,
+                                                    unsigned char* ctile) {
+    static_assert(VS % 32 == 0, "16x256b.x4 covers 32 accumulator columns");
+    const uint32_t cb = smem_u32(ctile);
+    const int mi = lane >> 3, mj = lane & 7;  // the matrix / row whose address this lane gives
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        const int nbase = q * 32 + half * 16;
+#pragma unroll
+        for (int col = 0; col < VS; col += 32) {
+            uint32_t r[16];
+            if (nkb > 0) {
+                tmem_ld_16x256b_x4(t_quarter + (static_cast<uint32_t>(half * 16) << 16) + col, r);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) r[i] = 0u;
+            }
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                uint32_t pk[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {  // matrix i: column block k = 2 kk + i / 2, lane half h = i % 2
+                    const int k = kk * 2 + (i >> 1), h = i & 1;
+                    pk[i] = pack2<OT>(r[4 * k + 2 * h], r[4 * k + 2 * h + 1]);
+                }
+                const int k = kk * 2 + (mi >> 1), h = mi & 1;
+                const int v = col + 8 * k + mj;
+                const int chunk = ((nbase + 8 * h) >> 3) ^ (v & 7);
+                stmatrix_x4_trans(cb + static_cast<uint32_t>(v * kBlockN * 2 + chunk * 16), pk);
+            }
+        }
+    }
+}
+
 // Epilogue for one output type: TMEM -> (staged tile -> 16-byte stores) or
 // direct stores, through the row map.  Kept as one straight-line routine per
 // type so the compiler never lowers the type switch per element.
 template <class OT, int VS>
 __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row, int nkb, int m, int q, int lane,
                                               int n0, const int32_t* rows_s, unsigned char* ctile) {
+    if constexpr (sizeof(OT) == 2 && VS % 32 == 0) {
+        if (p.bulk_out) {
+            stage_tile_stmatrix<OT, VS>(t_row, nkb, q, lane, ctile);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            store_tile_rows<OT, VS, true, true>(p, ctile, rows_s, q, lane, n0);
+            return;
+        }
+    }
     const int64_t n = out_col(p, n0 + m);
     const bool live = n >= 0;
 #pragma unroll
@@ -710,6 +774,18 @@ template <class OT, int VS>
 __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc, int nkb, int m, int q, int lane,
                                               int n0, const int32_t* rows_s, unsigned char* ctile,
                                               uint64_t* acc_empty) {
+    if constexpr (sizeof(OT) == 2 && VS % 32 == 0) {
+        if (p.bulk_out) {
+            stage_tile_stmatrix<OT, VS>(t_acc, nkb, q, lane, ctile);
+            // accumulator drained: the MMA warp may start the next unit in it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            store_tile_rows<OT, VS, false, true>(p, ctile, rows_s, q, lane, n0);
+            return;
+        }
+    }
     const int64_t n = out_col(p, n0 + m);
     const bool live = n >= 0;
 #pragma unroll
