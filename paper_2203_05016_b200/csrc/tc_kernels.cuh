@@ -529,6 +529,14 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     constexpr int kGT = 32 * GW;      // gather threads
     const int et = threadIdx.x - 64;  // gather thread 0..kGT-1 (epilogue: et < 128)
     if (threadIdx.x == 0) trace_event(p.trace, 0);
+    // first window of column indices (static data): cp.async right at entry,
+    // so its latency overlaps the barrier / TMEM / cluster setup
+    const int nb0 = nkb < kMetaBlocks ? nkb : kMetaBlocks;
+    if (et >= 0) {
+        const int32_t* src = p.col_idx + gp + kbase * kBlockK;
+        for (int i = et; i < nb0 * (kBlockK / 4); i += kGT) cp_async16(smem_u32(meta_s + 4 * i), src + 4 * i, true);
+        cp_async_commit();
+    }
 
     // gather warps stage a window of column indices (all 64 per K block)
     auto stage_meta = [&](int kb0) {
@@ -641,7 +649,11 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
         // cp.async part (SpMM only): slabs [2-cps, 2): cps*512 16-byte chunks per K block
         const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
         const T* Bp = static_cast<const T*>(p.B);
-        if (nkb > 0) stage_meta(0);  // static metadata: before the dependency wait
+        cp_async_wait<0>();  // this thread's part of the first window
+        if constexpr (KIND != 0) {
+            for (int i = et; i < nb0 * (kBlockK / 4); i += kGT)
+                reinterpret_cast<int4*>(meta_s)[i] = conv_encode4<KIND>(p, reinterpret_cast<int4*>(meta_s)[i]);
+        }
         named_bar<kGT>(2);  // first window visible (overlaps the previous grid)
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
