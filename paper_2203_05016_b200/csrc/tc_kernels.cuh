@@ -611,8 +611,12 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
                                                           WL::kSlabBytes, WL::kSBO, WL::kLayout);
                     umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
                 }
+                // the last `stages` slots are never refilled: no release
+                // signal for them, so nothing targets a peer's shared memory
+                // once that peer has consumed its own stages (no cluster
+                // barrier needed before exit)
                 if constexpr (!mcast) umma_commit(&empty[s]);
-                else umma_commit_mc(&empty[s], cmask);
+                else if (kb + stages < nkb) umma_commit_mc(&empty[s], cmask);
                 if (++s == stages) s = 0, ph ^= 1;
             }
             trace_event(p.trace, 4);
@@ -745,8 +749,12 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     }
     if (et == 0) trace_event(p.trace, 6);
     tc_fence_before();
-    if (CS > 1) cluster_sync_relaxed();  // only smem lifetime matters here
-    else __syncthreads();
+    // Every operation that targets this CTA's shared memory from a peer --
+    // multicast gathers (full barriers), K-split partials (recv_bar), MMA
+    // slot releases (empty barriers of refilled slots only) -- has been
+    // waited for above, so a CTA-local barrier suffices before TMEM release
+    // and exit (a cluster barrier here cost ~0.2 us per launch).
+    __syncthreads();
     if (warp == 1) tmem_dealloc(tmem_d, kTmemCols);
     if (threadIdx.x == 0) trace_event(p.trace, 7);
 }

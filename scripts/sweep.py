@@ -66,7 +66,10 @@ def time_steps(step, steps):
 def spmm_row(name, M, N, K, V, alpha, steps, dev):
     cpg = int(round(alpha * K))
     kpad = (cpg + 63) // 64 * 64
-    n = nsets_for(2 * M * kpad + 2 * K * N + 2 * M * N + 2 * M * K)
+    # enough rotating sets that EACH implementation's own operands exceed L2
+    # (ours: packed weights + indices + B + C; dense: W + B + C)
+    n = max(nsets_for(2 * M * kpad + 4 * (M // V) * kpad + 2 * K * N + 2 * M * N),
+            nsets_for(2 * M * K + 2 * K * N + 2 * M * N))
     mask = torch.from_numpy(bench.synth_mask(M, K, V, cpg, 1234)).to(dev)
     mats, Wd, Bs, Cs, Cd = [], [], [], [], []
     for s in range(n):
@@ -91,7 +94,7 @@ def spmm_row(name, M, N, K, V, alpha, steps, dev):
 def conv_row(name, C, H, Kf, R, pad, Nb, V, alpha, steps, dev):
     crs = C * R * R
     cpg = int(round(alpha * crs))
-    n = nsets_for(2 * C * H * H * Nb * 2 + 2 * Kf * crs)
+    n = max(nsets_for(2 * C * H * H * Nb * 2 + 2 * Kf * crs // 4), nsets_for(2 * C * H * H * Nb * 2 + 2 * Kf * crs))
     mask = torch.from_numpy(bench.synth_mask(Kf, crs, V, cpg, 1234)).to(dev)
     geo = sb.ConvGeometry(R, R, 1, pad)
     P = H + 2 * pad - R + 1
