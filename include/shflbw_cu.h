@@ -101,11 +101,13 @@ int shflbw_cu_version(void);
  * over two pairs, 3 = V split with multicast activation tiles; with mode 0 an
  * explicit "split" means V split), "persistent" (N = 1 or 2: the persistent
  * kernel, N CTAs per SM looping over (group, column tile) units; -1: one CTA
- * per unit; 0 = auto: persistent with 2 CTAs per SM once the grid holds two
- * full waves of units), "cp_async_slabs" (0..2 activation slabs filled by
- * cp.async instead of TMA gather4), "no_bulk_out" (1: per-element output
- * stores).  All variants give results within the same tolerance; V split,
- * cp.async and persistent are bit-identical to the default.
+ * per unit; 0 = auto: persistent with 2 CTAs per SM once the units exceed
+ * one such wave), "gather_warps" (4 or 8 warps issuing the TMA gathers per
+ * CTA; 0 = auto: 8 for unsplit units of >= 5 K blocks), "cp_async_slabs"
+ * (0..2 activation slabs filled by cp.async instead of TMA gather4),
+ * "no_bulk_out" (1: per-element output stores).  All variants give results
+ * within the same tolerance; V split, cp.async, gather warps and persistent
+ * are bit-identical to the default.
  * Unknown key: BAD_PARAMS. */
 int shflbw_cu_set_option(const char* key, int64_t value);
 /* Number of kernels this library launched on the calling thread so far. */
