@@ -894,3 +894,34 @@ def test_gather_warps_conv_bitwise(sb, oracle, prepared):
     assert oracle.rel_frobenius(ref, want) <= TOL
     for k, v in outs.items():
         assert np.array_equal(v, ref), k
+
+
+@pytest.mark.parametrize("M,N,K,V,alpha,persistent,split,mode",
+                         [(2048, 128, 2048, 64, 0.25, 0, 0, 0),      # 2 x 2 K-split epilogue
+                          (512, 4096, 2048, 64, 0.25, -1, 0, 0),     # one CTA per unit, stmatrix staging
+                          (2048, 1000, 512, 64, 0.25, 2, 0, 0),      # persistent, ragged last tile
+                          (1024, 384, 768, 32, 0.3, 2, 0, 0),        # persistent, V = 32
+                          (512, 640, 512, 128, 0.3, -1, 0, 0),       # V = 128 (4 column chunks)
+                          (2048, 256, 1024, 64, 0.25, 0, 4, 1)])     # K split by 4
+def test_16bit_out_is_rne_of_fp32_out(sb, oracle, M, N, K, V, alpha, persistent, split, mode):
+    """Every epilogue (stmatrix-staged tiles, K-split exchange, per-element
+    stores) writes bf16 / f16 = the fp32 accumulator rounded once to nearest
+    even: bit-identical to rounding the fp32-output result."""
+    mask, W, B = synthetic(oracle, M, K, N, V, alpha)
+    a, _ = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("persistent", persistent)
+    sb.set_option("split", split)
+    sb.set_option("split_mode", mode)
+    try:
+        c32 = sb.spmm_execute(a, Bd)
+        for dt in (torch.bfloat16, torch.float16):
+            got = sb.spmm_execute(a, Bd, out_dtype=dt)
+            assert torch.equal(got, c32.to(dt)), dt
+            sb.set_option("no_bulk_out", 1)
+            got_el = sb.spmm_execute(a, Bd, out_dtype=dt)
+            sb.set_option("no_bulk_out", 0)
+            assert torch.equal(got_el, got), dt
+    finally:
+        for k in ("persistent", "split", "split_mode", "no_bulk_out"):
+            sb.set_option(k, 0)
