@@ -1,0 +1,36 @@
+"""Converter (compress_shflbw) timing (development): wall and device time per
+call, warm allocator, north-star and large-FFN shapes."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2203_05016_b200 as sb  # noqa: E402
+
+dev = torch.device("cuda", 0)
+for name, M, K, V in (("ns", 2048, 2048, 64), ("lf", 16384, 4096, 64), ("ffn1", 2048, 512, 64)):
+    mask = torch.from_numpy(bench.synth_mask(M, K, V, K // 4, 1234)).to(dev)
+    W = bench.uniform_bf16(torch, (M, K), 100, dev)
+    for _ in range(3):
+        a = sb.compress_shflbw(W, mask, V)
+        del a
+    torch.cuda.synchronize()
+    walls, gpus = [], []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t = time.perf_counter()
+        e0.record()
+        a = sb.compress_shflbw(W, mask, V)
+        e1.record()
+        torch.cuda.synchronize()
+        walls.append((time.perf_counter() - t) * 1e3)
+        gpus.append(e0.elapsed_time(e1))
+        del a
+    walls.sort(), gpus.sort()
+    print(json.dumps({"shape": name, "M": M, "K": K, "wall_ms_median": round(walls[5], 3),
+                      "event_ms_median": round(gpus[5], 3), "wall_ms_min": round(walls[0], 3)}), flush=True)
