@@ -26,6 +26,10 @@ cases = {
     "ns_v128": lambda: sweep.spmm_row("ns_v128", 2048, 128, 2048, 128, 0.25, 2000, dev),
     "gnmt50": lambda: sweep.spmm_row("gnmt50", 4096, 128, 1024, 64, 0.5, 2000, dev),
     "gnmt75": lambda: sweep.spmm_row("gnmt75", 4096, 128, 1024, 64, 0.25, 2000, dev),
+    "attn128": lambda: sweep.spmm_row("attn128", 512, 128, 512, 64, 0.25, 2000, dev),
+    "ffn1_128": lambda: sweep.spmm_row("ffn1_128", 2048, 128, 512, 64, 0.25, 2000, dev),
+    "ffn2_128": lambda: sweep.spmm_row("ffn2_128", 512, 128, 2048, 64, 0.25, 2000, dev),
+    "gnmt95": lambda: sweep.spmm_row("gnmt95", 4096, 128, 1024, 64, 0.05, 2000, dev),
     "gnmt90": lambda: sweep.spmm_row("gnmt90", 4096, 128, 1024, 64, 0.1, 2000, dev),
     "lf": lambda: sweep.spmm_row("lf", 16384, 8192, 4096, 64, 0.25, 20, dev),
     "conv56": lambda: sweep.conv_row("conv56", 64, 56, 64, 3, 1, 32, 64, 0.25, 300, dev),
