@@ -697,13 +697,15 @@ void by_dtype(int dt, F&& f) {
 }
 
 // allocate meta (row_indices, group_ptr, group_ncols) in one block
-int alloc_meta(shflbw_cu_matrix* out, int M, int K, int V, int dtype) {
+int alloc_meta(shflbw_cu_matrix* out, int M, int K, int V, int dtype, cudaStream_t s) {
     const int G = M / V;
     const size_t a = (static_cast<size_t>(M) * 4 + 255) / 256 * 256;
     const size_t b = (static_cast<size_t>(G + 1) * 4 + 255) / 256 * 256;
     const size_t c = (static_cast<size_t>(G) * 4 + 255) / 256 * 256;
     char* base = nullptr;
-    SBW_CUDA(cudaMalloc(&base, a + b + c + 256));
+    // stream-ordered pool allocation (a plain cudaMalloc synchronises the
+    // device and cost ~0.1-0.5 ms per matrix); freed with cudaFree
+    SBW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), a + b + c + 256, s));
     *out = shflbw_cu_matrix{};
     out->rows = M;
     out->cols = K;
@@ -721,11 +723,11 @@ int alloc_meta(shflbw_cu_matrix* out, int M, int K, int V, int dtype) {
     return SHFLBW_OK;
 }
 
-int alloc_data(shflbw_cu_matrix* out, int64_t total) {
+int alloc_data(shflbw_cu_matrix* out, int64_t total, cudaStream_t s) {
     const size_t a = (static_cast<size_t>(total) * 4 + 255) / 256 * 256;
     const size_t b = static_cast<size_t>(total) * out->v * dtype_bytes(out->dtype);
     char* base = nullptr;
-    SBW_CUDA(cudaMalloc(&base, a + b + 256));
+    SBW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), a + b + 256, s));
     out->col_idx = reinterpret_cast<int32_t*>(base);
     out->values = base + a;
     out->total_cols = total;
@@ -767,14 +769,14 @@ int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M
     if (V <= 0 || M < 0 || K < 0 || M % V != 0) return fail(SHFLBW_BAD_PARAMS, "V must divide M");
     if (fail_row) *fail_row = 0;
     const int G = M / V;
-    if (int st = alloc_meta(out, M, K, V, value_dtype)) return st;
+    if (int st = alloc_meta(out, M, K, V, value_dtype, s)) return st;
     auto cleanup = [&](int st) {
         if (st) free_matrix(out);
         return st;
     };
     if (M == 0) {
         SBW_CUDA(cudaMemsetAsync(out->group_ptr, 0, sizeof(int32_t), s));
-        return cleanup(alloc_data(out, 0));
+        return cleanup(alloc_data(out, 0, s));
     }
     ClassPlan p;
     uint32_t hf[4];
@@ -808,7 +810,7 @@ int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M
     SBW_CUDA(cudaStreamSynchronize(s));
     const int total_cols = sizes[0];
     out->max_group_cols = sizes[1];
-    if ((st = alloc_data(out, total_cols))) return cleanup(st);
+    if ((st = alloc_data(out, total_cols, s))) return cleanup(st);
     if (G > 0) {
         k_pack_cols<<<G, 128, 0, s>>>(p.words.as<uint64_t>(), p.W, leader.as<int32_t>(), out->group_ptr,
                                       out->group_ncols, out->col_idx);
@@ -845,7 +847,7 @@ int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t
     const int G = M / V;
     int64_t nnzc = 0;
     for (int g = 0; g < G; ++g) nnzc += group_ncols[g];
-    if (int st = alloc_meta(out, M, K, V, value_dtype)) return st;
+    if (int st = alloc_meta(out, M, K, V, value_dtype, s)) return st;
     auto cleanup = [&](int st) {
         if (st) free_matrix(out);
         return st;
@@ -890,7 +892,7 @@ int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t
     if (hf[0]) return cleanup(fail(SHFLBW_SHAPE_MISMATCH, "spmm: row index out of range"));
     if (hf[3]) return cleanup(fail(SHFLBW_BAD_PARAMS, "group column count exceeds K"));
     out->max_group_cols = max_cols;
-    if ((st = alloc_data(out, total_cols))) return cleanup(st);
+    if ((st = alloc_data(out, total_cols, s))) return cleanup(st);
     if (G > 0 && total_cols > 0) {
         dim3 grid(grid_for(static_cast<int64_t>(K + SHFLBW_K_TILE) * V, 256 * 4), G);
         by_dtype(value_dtype, [&]<int DT>() {
@@ -937,7 +939,7 @@ int download_impl(const shflbw_cu_matrix* m, uint32_t* row_indices, uint32_t* gr
 int conv_prepare_impl(const shflbw_cu_matrix* w, int S, shflbw_cu_matrix* out, cudaStream_t s) {
     if (S < 1 || S > 32) return fail(SHFLBW_UNSUPPORTED, "conv_prepare: filter width S must be 1..32");
     const int M = w->rows, K = w->cols, V = w->v, G = w->groups;
-    if (int st = alloc_meta(out, M, K, V, w->dtype)) return st;
+    if (int st = alloc_meta(out, M, K, V, w->dtype, s)) return st;
     auto cleanup = [&](int st) {
         if (st) free_matrix(out);
         return st;
@@ -964,7 +966,7 @@ int conv_prepare_impl(const shflbw_cu_matrix* w, int S, shflbw_cu_matrix* out, c
     SBW_CUDA(cudaMemcpyAsync(&widest, widths.as<int>() + G, sizeof(int), cudaMemcpyDeviceToHost, s));
     SBW_CUDA(cudaStreamSynchronize(s));
     out->max_group_cols = widest;
-    if ((st = alloc_data(out, total))) return cleanup(st);
+    if ((st = alloc_data(out, total, s))) return cleanup(st);
     if (total > 0) {
         SBW_CUDA(cudaMemsetAsync(out->col_idx, 0xff, sizeof(int32_t) * static_cast<size_t>(total), s));
         SBW_CUDA(cudaMemsetAsync(out->values, 0, static_cast<size_t>(total) * V * dtype_bytes(w->dtype), s));

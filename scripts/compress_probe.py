@@ -34,3 +34,18 @@ for name, M, K, V in (("ns", 2048, 2048, 64), ("lf", 16384, 4096, 64), ("ffn1", 
     walls.sort(), gpus.sort()
     print(json.dumps({"shape": name, "M": M, "K": K, "wall_ms_median": round(walls[5], 3),
                       "event_ms_median": round(gpus[5], 3), "wall_ms_min": round(walls[0], 3)}), flush=True)
+
+# allocation check: repeated compress + free must not grow device usage
+mask = torch.from_numpy(bench.synth_mask(2048, 2048, 64, 512, 1234)).to(dev)
+W = bench.uniform_bf16(torch, (2048, 2048), 100, dev)
+for _ in range(5):
+    del_a = sb.compress_shflbw(W, mask, 64)
+    del del_a
+torch.cuda.synchronize()
+f0 = torch.cuda.mem_get_info()[0]
+for _ in range(200):
+    a = sb.compress_shflbw(W, mask, 64)
+    del a
+torch.cuda.synchronize()
+f1 = torch.cuda.mem_get_info()[0]
+print(json.dumps({"free_mb_before": f0 // 2**20, "free_mb_after_200": f1 // 2**20}), flush=True)
