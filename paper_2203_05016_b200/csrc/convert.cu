@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include "common.cuh"
@@ -106,6 +107,54 @@ __global__ void k_hash_rows(const uint64_t* __restrict__ words, int M, int W, ui
 }
 
 // ---- stable LSD radix sort of (u64 key, u32 value), 8-bit digits ---------
+
+// Small-n sort (n <= kSmallSort) in one CTA: bitonic network over (key,
+// original position) in shared memory -- the exact order of the stable LSD
+// radix sort (ascending key, ties in input order), in one launch instead of
+// 8 x (histogram, scan, scatter).
+constexpr int kSmallSort = 4096;
+
+__global__ void __launch_bounds__(1024) k_sort_small(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                     int n, int P) {
+    extern __shared__ __align__(16) unsigned char sm_sort[];
+    uint64_t* k = reinterpret_cast<uint64_t*>(sm_sort);
+    uint32_t* v = reinterpret_cast<uint32_t*>(k + P);
+    uint32_t* pos = v + P;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const bool live = i < n;
+        k[i] = live ? keys[i] : ~0ull;
+        v[i] = live ? vals[i] : 0u;
+        pos[i] = static_cast<uint32_t>(i);
+    }
+    __syncthreads();
+    for (int kk = 2; kk <= P; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & kk) == 0;
+                    const uint64_t ka = k[i], kb = k[ixj];
+                    const uint32_t pa = pos[i], pb = pos[ixj];
+                    const bool b_lt_a = kb < ka || (kb == ka && pb < pa);
+                    if (b_lt_a == up) {
+                        k[i] = kb;
+                        k[ixj] = ka;
+                        pos[i] = pb;
+                        pos[ixj] = pa;
+                        const uint32_t t = v[i];
+                        v[i] = v[ixj];
+                        v[ixj] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        keys[i] = k[i];
+        vals[i] = v[i];
+    }
+}
 
 __global__ void k_radix_hist(const uint64_t* __restrict__ keys, int n, int shift,
                              int* __restrict__ hist, int nblocks) {
@@ -538,6 +587,28 @@ __global__ void k_convert(const void* __restrict__ src, int sdt, void* __restric
 
 // ---- host helpers ------------------------------------------------------------
 
+}  // namespace
+
+// The converter's scratch and output matrices come from the device's default
+// stream-ordered pool; with its default release threshold (0) every stream
+// synchronisation handed the memory back to the driver and the next call paid
+// for mapping it again (0.4 -> 2.4 ms swings per compress).  Keep it.
+void retain_pool() {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
+    if (bit && (done.load(std::memory_order_relaxed) & bit)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    if (bit) done.fetch_or(bit, std::memory_order_relaxed);
+}
+
+namespace {
+
 struct DevBuf {
     void* p = nullptr;
     cudaStream_t s = nullptr;
@@ -548,6 +619,7 @@ struct DevBuf {
     }
     cudaError_t alloc(size_t bytes, cudaStream_t st) {
         s = st;
+        retain_pool();
         return cudaMallocAsync(&p, bytes ? bytes : 16, st);
     }
     template <class T> T* as() const { return static_cast<T*>(p); }
@@ -592,6 +664,18 @@ int scan_exclusive(const int* in, int* out, int n, int* total_dev, cudaStream_t 
 // keys_tmp / vals_tmp are scratch of n elements (also used by prune.cu)
 int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int n,
                      cudaStream_t s) {
+    if (n <= 1) return SHFLBW_OK;
+    if (n <= kSmallSort) {
+        int P = 2;
+        while (P < n) P <<= 1;
+        const size_t smem = static_cast<size_t>(P) * 16;
+        if (smem > 48 * 1024)  // per call: the attribute is per device
+            SBW_CUDA(cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+        k_sort_small<<<1, 1024, smem, s>>>(keys, vals, n, P);
+        SBW_LAUNCHED("k_sort_small");
+        return SHFLBW_OK;
+    }
     const int nb = (n + kRadixTile - 1) / kRadixTile;
     DevBuf hist, offs;
     SBW_CUDA(hist.alloc(sizeof(int) * 256 * nb, s));
@@ -705,6 +789,7 @@ int alloc_meta(shflbw_cu_matrix* out, int M, int K, int V, int dtype, cudaStream
     char* base = nullptr;
     // stream-ordered pool allocation (a plain cudaMalloc synchronises the
     // device and cost ~0.1-0.5 ms per matrix); freed with cudaFree
+    retain_pool();
     SBW_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&base), a + b + c + 256, s));
     *out = shflbw_cu_matrix{};
     out->rows = M;

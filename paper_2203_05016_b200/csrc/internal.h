@@ -23,6 +23,8 @@ int decompress_impl(const shflbw_cu_matrix* m, float* dense, cudaStream_t s);
 int conv_prepare_impl(const shflbw_cu_matrix* w, int S, shflbw_cu_matrix* out, cudaStream_t s);
 int convert_impl(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s);
 int scan_exclusive(const int* in, int* out, int n, int* total_dev, cudaStream_t s);
+// keep the default stream-ordered pool's memory across synchronisations (convert.cu)
+void retain_pool();
 int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int n,
                      cudaStream_t s);
 void free_matrix(shflbw_cu_matrix* m);

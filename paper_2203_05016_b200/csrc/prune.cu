@@ -41,6 +41,7 @@ struct Buf {
     }
     cudaError_t alloc(size_t bytes, cudaStream_t st) {
         s = st;
+        retain_pool();
         return cudaMallocAsync(&p, bytes ? bytes : 16, st);
     }
     template <class T> T* as() const { return static_cast<T*>(p); }
