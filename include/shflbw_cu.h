@@ -184,6 +184,21 @@ int shflbw_cu_spmm_groups(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_
                           int32_t c_dtype, int64_t ldc, int32_t compact,
                           shflbw_stream_t stream);
 
+/* The row-sharded SpMM with the all-gather fused into its epilogue (SURVEY.md
+ * §8(e)): groups [g_begin, g_end) computed once, each finished output row
+ * stored at its row_indices position into every buffer of C_dst[0..n_dst)
+ * -- this GPU's full C and the peer GPUs' full C through P2P mappings
+ * (cudaIpcOpenMemHandle / cudaDeviceEnablePeerAccess) -- with the same
+ * 16-byte stores, so the transfer overlaps the remaining tiles' math and no
+ * collective or unpermute pass follows.  The caller orders the consumers
+ * after every rank's call (a cross-GPU barrier).  bf16 / f16 output, the
+ * tcgen05 path (else UNSUPPORTED); n_dst in 1..8; buffers 16-byte aligned
+ * with the same ldc. */
+int shflbw_cu_spmm_groups_peers(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_end,
+                                const void* B, int32_t K_b, int32_t N, int64_t ldb,
+                                void* const* C_dst, int32_t n_dst, int32_t c_dtype,
+                                int64_t ldc, shflbw_stream_t stream);
+
 /* Conv weight layout (cf. a library's one-time filter reorder): *out = a copy
  * of w whose columns are, per group, ordered by filter column s = c % S
  * (ascending c within each s) with every s-run padded to a multiple of 4 by

@@ -67,11 +67,15 @@ int run_spmm(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b
         const int st = spmm_tc(a, g_begin, g_end, b, c, s);
         if (st != SHFLBW_UNSUPPORTED) return st;
     }
+    if (c.n_extra > 0)
+        return fail(SHFLBW_UNSUPPORTED, "spmm with peer destinations: needs the tcgen05 path (bf16/f16 matrix, V in "
+                                        "{16, 32, 64, 128}, 16-byte aligned rows)");
     return spmm_simt(a, g_begin, g_end, b, c, s);
 }
 
 int spmm_groups_impl(const shflbw_cu_matrix* a, int g_begin, int g_end, const void* B, int K_b, int N,
-                     int64_t ldb, void* C, int c_dtype, int64_t ldc, int compact, cudaStream_t s) {
+                     int64_t ldb, void* C, int c_dtype, int64_t ldc, int compact, cudaStream_t s,
+                     void* const* extra = nullptr, int n_extra = 0) {
     if (int st = check_compute_matrix(a)) return st;
     if (int st = check_out_dtype(c_dtype)) return st;
     if (K_b != a->cols) return fail(SHFLBW_SHAPE_MISMATCH, "spmm: A columns != B rows");
@@ -90,6 +94,12 @@ int spmm_groups_impl(const shflbw_cu_matrix* a, int g_begin, int g_end, const vo
     c.dtype = c_dtype;
     c.ldc = ldc;
     c.compact = compact;
+    if (n_extra < 0 || n_extra > kMaxPeers - 1) return fail(SHFLBW_BAD_PARAMS, "spmm: 0..7 peer destinations");
+    for (int d = 0; d < n_extra; ++d) {
+        if (!extra[d]) return fail(SHFLBW_BAD_PARAMS, "spmm: null peer destination");
+        c.extra[d] = extra[d];
+    }
+    c.n_extra = n_extra;
     return run_spmm(a, g_begin, g_end, b, c, s);
 }
 
@@ -186,6 +196,15 @@ int shflbw_cu_spmm_groups(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_
                           int32_t compact, shflbw_stream_t stream) {
     return spmm_groups_impl(a, g_begin, g_end, B, K_b, N, ldb, C, c_dtype, ldc, compact,
                             reinterpret_cast<cudaStream_t>(stream));
+}
+
+int shflbw_cu_spmm_groups_peers(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_end, const void* B,
+                                int32_t K_b, int32_t N, int64_t ldb, void* const* C_dst, int32_t n_dst,
+                                int32_t c_dtype, int64_t ldc, shflbw_stream_t stream) {
+    if (!C_dst || n_dst < 1 || n_dst > kMaxPeers) return fail(SHFLBW_BAD_PARAMS, "spmm_groups_peers: 1..8 destinations");
+    if (c_dtype == SHFLBW_F32) return fail(SHFLBW_UNSUPPORTED, "spmm_groups_peers: 16-bit output only");
+    return spmm_groups_impl(a, g_begin, g_end, B, K_b, N, ldb, C_dst[0], c_dtype, ldc, 0,
+                            reinterpret_cast<cudaStream_t>(stream), C_dst + 1, n_dst - 1);
 }
 
 int shflbw_cu_unpermute_rows(const int32_t* row_indices, int32_t M, int32_t N, const void* C_perm,

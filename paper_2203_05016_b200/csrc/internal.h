@@ -47,11 +47,17 @@ struct Operand {
     int C = 0, H = 0, W = 0, Nb = 0, R = 1, S = 1, stride = 1, pad = 0, P = 0, Q = 0;
 };
 
+constexpr int kMaxPeers = 8;  // output destinations (the fused all-gather)
+
 struct OutSpec {
     void* ptr = nullptr;
     int dtype = SHFLBW_F32;
     int64_t ldc = 0;
     int compact = 0;  // 1: row (g - g_begin)*V + r instead of row_indices
+    // further destinations that receive identical row stores (peer GPUs' C
+    // through P2P mappings: the all-gather fused into the epilogue)
+    void* extra[kMaxPeers - 1] = {};
+    int n_extra = 0;
 };
 
 // spmm_simt.cu: CUDA-core kernel, any V, bit-exact ascending-k order

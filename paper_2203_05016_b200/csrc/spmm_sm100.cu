@@ -259,6 +259,14 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const bool aligned = (reinterpret_cast<uintptr_t>(c.ptr) % 16 == 0) && ((c.ldc * esz) % 16 == 0) &&
                              ((static_cast<int64_t>(b.N) * esz) % 16 == 0);
         prm.bulk_out = aligned && !option("no_bulk_out") ? 1 : 0;
+        if (c.n_extra > 0) {
+            // extra destinations are written by the staged 16-byte stores only
+            if (!prm.bulk_out) return SHFLBW_UNSUPPORTED;
+            for (int d = 0; d < c.n_extra; ++d)
+                if (reinterpret_cast<uintptr_t>(c.extra[d]) % 16 != 0) return SHFLBW_UNSUPPORTED;
+        }
+        prm.n_extra = c.n_extra;
+        for (int d = 0; d < c.n_extra; ++d) prm.C_extra[d] = c.extra[d];
     }
     // persistent when one wave of CTAs cannot cover the units (option
     // "persistent": -1 never, 1 always, 0 auto)
@@ -284,7 +292,10 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const int64_t fixed = 1024 + 2 * kMetaBlocks * kBlockK * 4 + 4 * 128 + 4 * (groups + 2) + 512;
         const int64_t stage = kABytes + static_cast<int64_t>(kBlockK) * vs * 2;
         const int64_t with_tile = (budget - fixed - tile) / stage, without = (budget - fixed) / stage;
-        if (prm.bulk_out && with_tile < 2) prm.bulk_out = 0;  // the staged epilogue is worth a stage
+        if (prm.bulk_out && with_tile < 2) {  // the staged epilogue is worth a stage
+            if (c.n_extra > 0) prm.persistent = 0;  // ... unless it carries the extra destinations
+            else prm.bulk_out = 0;
+        }
         const int64_t fit = prm.bulk_out ? with_tile : without;
         if (fit < 2) prm.persistent = 0;
         else if (stages <= 0 || stages > fit) stages = static_cast<int>(std::min<int64_t>(12, fit));

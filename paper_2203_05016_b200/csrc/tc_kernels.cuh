@@ -89,6 +89,8 @@ struct TcParams {
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
     int per_sm;      // persistent: resident CTAs per SM
     int gw;          // gather warps per CTA (4, 8)
+    int n_extra;     // further output destinations (fused all-gather), staged-store path only
+    void* C_extra[kMaxPeers - 1];
 };
 
 // Development timeline (scripts/trace.py): compiled in only with -DSBW_TRACE.
@@ -181,7 +183,9 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
                              : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
                              : "r"(cb + static_cast<uint32_t>(v * kBlockN * esz + pc * 16)));
                 asm volatile("ld.shared.b32 %0, [%1];" : "=r"(row) : "r"(rbase + static_cast<uint32_t>(v * 4)));
-                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(row) * p.ldc + nn) * esz) = x;
+                const int64_t off = (static_cast<int64_t>(row) * p.ldc + nn) * esz;
+                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + off) = x;
+                for (int d = 0; d < p.n_extra; ++d) *reinterpret_cast<int4*>(static_cast<char*>(p.C_extra[d]) + off) = x;
             }
         }
         return;
@@ -209,6 +213,20 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
             if (v < ROWS)
                 *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(row[k]) * p.ldc + nn) * esz) =
                     x[k];
+        }
+        // further destinations (fused all-gather): the same rows again, read
+        // back from the staged tile so the common path keeps its registers
+        for (int d = 0; d < p.n_extra; ++d) {
+            const uint32_t cbd = smem_u32(ctile);
+            for (int v = v0; v < ROWS; v += 4 * kRowsPerInst) {
+                const int pc = SWZ ? (chunk ^ (v & 7)) : chunk;
+                int4 y;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w)
+                             : "r"(cbd + static_cast<uint32_t>(v * kBlockN * esz + pc * 16)));
+                *reinterpret_cast<int4*>(static_cast<char*>(p.C_extra[d]) +
+                                         (static_cast<int64_t>(rows[v]) * p.ldc + nn) * esz) = y;
+            }
         }
     }
 }

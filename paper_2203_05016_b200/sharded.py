@@ -13,6 +13,14 @@ map (-1 for padding rows).
 
 ``ShardPlan`` is pure host logic (tested with gloo on CPU);
 ``ShardedSpMM`` binds it to the CUDA kernels.
+
+Fused all-gather (``ShardedSpMM.full_fused``): every rank holds a full-size
+output buffer; the buffers are shared through CUDA IPC once
+(``PeerOutputs``), and ``shflbw_cu_spmm_groups_peers`` stores each finished
+row at its final position into all ranks' buffers from the epilogue (P2P
+stores over NVLink, overlapped with the remaining tiles' math) -- no NCCL
+call, no padding, no unpermute pass.  A barrier orders the consumers after
+every rank's kernel.
 """
 from __future__ import annotations
 
@@ -92,3 +100,65 @@ class ShardedSpMM:
         gathered = gather_rows(self.plan, self.local(b, out_dtype), self.group)
         c = torch.empty((self.a.rows, b.shape[1]), dtype=out_dtype, device=b.device)
         return self.sb.unpermute_rows(self.row_map.data_ptr(), gathered, c)
+
+
+class PeerOutputs:
+    """A full-size [M, N] output buffer on every rank, each rank holding P2P
+    device pointers to all the others (CUDA IPC handles exchanged once over
+    the process group).  ``ptrs`` lists this rank's buffer first."""
+
+    def __init__(self, shape, dtype, world: int, rank: int, group=None, device=None):
+        import torch.distributed as dist
+        self.buf = torch.zeros(shape, dtype=dtype, device=device or torch.device("cuda", torch.cuda.current_device()))
+        self.world, self.rank = world, rank
+        self._opened = []
+        peers = [None] * world
+        if world > 1:
+            from cuda.bindings import driver as drv
+            from cuda.bindings import runtime as rt
+            err, base, _ = drv.cuMemGetAddressRange(self.buf.data_ptr())
+            if err != drv.CUresult.CUDA_SUCCESS:
+                raise RuntimeError(f"cuMemGetAddressRange: {err}")
+            offset = self.buf.data_ptr() - int(base)
+            err, handle = rt.cudaIpcGetMemHandle(int(base))
+            if err != rt.cudaError_t.cudaSuccess:
+                raise RuntimeError(f"cudaIpcGetMemHandle: {err}")
+            mine = (bytes(handle.reserved), offset)
+            allh = [None] * world
+            dist.all_gather_object(allh, mine, group=group)
+            for r, (hb, off) in enumerate(allh):
+                if r == rank:
+                    continue
+                h = rt.cudaIpcMemHandle_t()
+                h.reserved = hb
+                err, ptr = rt.cudaIpcOpenMemHandle(h, rt.cudaIpcMemLazyEnablePeerAccess)
+                if err != rt.cudaError_t.cudaSuccess:
+                    raise RuntimeError(f"cudaIpcOpenMemHandle (rank {r}): {err}")
+                self._opened.append(int(ptr))
+                peers[r] = int(ptr) + off
+        self.ptrs = [self.buf.data_ptr()] + [peers[(rank + i) % world] for i in range(1, world)]
+
+    def close(self):
+        if self._opened:
+            from cuda.bindings import runtime as rt
+            for p in self._opened:
+                rt.cudaIpcCloseMemHandle(p)
+            self._opened = []
+
+
+def _full_fused(self, b: torch.Tensor, outputs: PeerOutputs) -> torch.Tensor:
+    """This rank's groups, each row stored into every rank's full output
+    buffer from the epilogue; returns this rank's buffer once all ranks'
+    kernels are complete (barrier)."""
+    import torch.distributed as dist
+    if self.plan.world > 1:
+        dist.barrier(group=self.group)  # every rank is done reading the previous result
+    self.sb.spmm_groups_peers(self.a, self.g0, self.g1, b, outputs.ptrs, dtype=outputs.buf.dtype,
+                              ldc=outputs.buf.stride(0))
+    if self.plan.world > 1:
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)  # all ranks' rows have landed everywhere
+    return outputs.buf
+
+
+ShardedSpMM.full_fused = _full_fused

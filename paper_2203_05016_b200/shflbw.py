@@ -459,6 +459,29 @@ def spmm_groups(a: ShflBWMatrix, g_begin: int, g_end: int, b: torch.Tensor, out:
     return out
 
 
+def spmm_groups_peers(a: ShflBWMatrix, g_begin: int, g_end: int, b: torch.Tensor, outs,
+                      dtype: torch.dtype | None = None, ldc: int | None = None) -> None:
+    """One shard's groups with the all-gather fused into the epilogue: every
+    finished row is stored at its row_indices position into each full-size
+    buffer of `outs` (this GPU's C first, then the peers' C mapped over
+    P2P / CUDA IPC).  `outs`: bf16 / f16 tensors of equal dtype and stride,
+    or raw device pointers (then `dtype` and `ldc` are required)."""
+    b = _check_b(a, b)
+    outs = list(outs)
+    if not outs:
+        raise BadParams("spmm_groups_peers: no destination")
+    if all(isinstance(o, torch.Tensor) for o in outs):
+        if any(o.dtype != outs[0].dtype or o.stride(0) != outs[0].stride(0) for o in outs):
+            raise BadParams("spmm_groups_peers: destinations differ in dtype or stride")
+        dtype, ldc = outs[0].dtype, outs[0].stride(0)
+        outs = [o.data_ptr() for o in outs]
+    elif dtype is None or ldc is None:
+        raise BadParams("spmm_groups_peers: raw pointers need dtype and ldc")
+    ptrs = (C.c_void_p * len(outs))(*[int(o) for o in outs])
+    _check(_lib().shflbw_cu_spmm_groups_peers(a.ptr, g_begin, g_end, b.data_ptr(), b.shape[0], b.shape[1],
+                                              b.stride(0), ptrs, len(outs), _dt(dtype), ldc, _stream()))
+
+
 def unpermute_rows(row_indices_ptr: int, c_perm: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     _check(_lib().shflbw_cu_unpermute_rows(row_indices_ptr, c_perm.shape[0], c_perm.shape[1],
                                            c_perm.data_ptr(), c_perm.stride(0), out.data_ptr(), out.stride(0),

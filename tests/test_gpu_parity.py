@@ -925,3 +925,51 @@ def test_16bit_out_is_rne_of_fp32_out(sb, oracle, M, N, K, V, alpha, persistent,
     finally:
         for k in ("persistent", "split", "split_mode", "no_bulk_out"):
             sb.set_option(k, 0)
+
+
+@pytest.mark.parametrize("M,N,K,V,alpha,persistent,split,mode,world",
+                         [(2048, 256, 1024, 64, 0.25, 0, 0, 0, 2),    # auto plan
+                          (2048, 128, 2048, 64, 0.25, 0, 4, 2, 2),    # 2 x 2 K-split epilogue
+                          (4096, 1024, 512, 64, 0.25, 2, 0, 0, 4),    # persistent
+                          (1024, 1000, 768, 32, 0.3, -1, 0, 0, 3),    # ragged N, uneven shards
+                          (1024, 512, 512, 128, 0.3, -1, 0, 0, 8)])   # V = 128, 8 destinations
+def test_spmm_groups_peers_fused_allgather(sb, oracle, M, N, K, V, alpha, persistent, split, mode, world):
+    """The all-gather fused into the epilogue, every destination on this one
+    device standing in for a peer GPU: each simulated rank computes its row
+    groups once and stores every row into all `world` full-size buffers.
+    After all ranks, every buffer equals the single-GPU result bit for bit
+    (same kernels, same accumulation order)."""
+    mask, W, B = synthetic(oracle, M, K, N, V, alpha)
+    a, _ = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("persistent", persistent)
+    sb.set_option("split", split)
+    sb.set_option("split_mode", mode)
+    try:
+        want = sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16)
+        outs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in range(world)]
+        G = a.group_count()
+        for rank in range(world):
+            g0, g1 = G * rank // world, G * (rank + 1) // world
+            sb.spmm_groups_peers(a, g0, g1, Bd, outs[rank:] + outs[:rank])  # own buffer first
+        torch.cuda.synchronize()
+        for o in outs:
+            assert torch.equal(o, want)
+    finally:
+        for k in ("persistent", "split", "split_mode"):
+            sb.set_option(k, 0)
+
+
+def test_spmm_groups_peers_errors(sb, oracle):
+    mask, W, B = synthetic(oracle, 256, 128, 64, 64, 0.5)
+    a, _ = compress_both(sb, oracle, W, mask, 64)
+    Bd = dev(B, torch.bfloat16)
+    with pytest.raises(sb.BadParams):
+        sb.spmm_groups_peers(a, 0, a.group_count(), Bd, [])
+    o32 = [torch.zeros((256, 64), dtype=torch.float32, device="cuda")]
+    with pytest.raises(sb.Error):  # fp32 output: UNSUPPORTED
+        sb.spmm_groups_peers(a, 0, a.group_count(), Bd, o32)
+    a32 = sb.compress_shflbw(dev(W), dev(mask), 64, dtype=torch.float32)
+    o16 = [torch.zeros((256, 64), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    with pytest.raises(sb.Error):  # exact fp32 matrix: no tcgen05 path, must not silently drop peers
+        sb.spmm_groups_peers(a32, 0, a32.group_count(), dev(B), o16)

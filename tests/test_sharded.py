@@ -87,3 +87,54 @@ def test_gather_unpermute_gloo(world, M):
         p.join(timeout=60)
     assert sorted(r for r, _ in res) == list(range(world))
     assert all(ok for _, ok in res)
+
+
+def _fused_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2203_05016_b200 as sb
+        from paper_2203_05016_b200.sharded import PeerOutputs, ShardedSpMM
+        torch.cuda.set_device(0)
+        g = torch.Generator().manual_seed(7)
+        M, K, N, V = 1024, 512, 384, 64
+        # the same synthetic layer on every rank: vector-wise groups, random columns
+        mask = torch.zeros((M, K), dtype=torch.uint8)
+        for grp in range(M // V):
+            cols = torch.randperm(K, generator=g)[:K // 4]
+            mask[grp * V:(grp + 1) * V, cols] = 1
+        mask = mask[torch.randperm(M, generator=g)]
+        W = (torch.rand((M, K), generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+        B = (torch.rand((K, N), generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+        a = sb.compress_shflbw(W, mask.cuda(), V)
+        want = sb.spmm_execute(a, B, out_dtype=torch.bfloat16)
+        outs = PeerOutputs((M, N), torch.bfloat16, world, rank)
+        got = ShardedSpMM(a, rank, world).full_fused(B, outs)
+        q.put((rank, bool(torch.equal(got, want))))
+        dist.barrier()
+        outs.close()
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, f"error: {e!r}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fused_allgather_two_processes_one_gpu():
+    """The fused all-gather across processes: CUDA IPC handles exchanged over
+    the process group, each rank's epilogue storing its rows into both
+    ranks' full buffers.  Both ranks share cuda:0 here (the kernels never wait
+    on each other; only the host barriers synchronise the ranks), so the
+    IPC + P2P-pointer plumbing runs end to end on one GPU."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    world, port = 2, free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}, res
