@@ -357,7 +357,9 @@ def main():
     ap.add_argument("--workload", default="ns", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--allgather", action="store_true", help="lf: all-gather the full output (NCCL)")
+    ap.add_argument("--allgather", action="store_true",
+                    help="lf, N > 1: also time the full-output gather -- NCCL all-gather + unpermute, and fused "
+                         "into the epilogue (P2P stores)")
     ap.add_argument("--soak", type=float, default=0.3, help="seconds of untimed replays to settle clocks")
     ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baselines, few steps")
@@ -464,6 +466,24 @@ def main():
         gms = max_over_ranks(torch, dist, e0.elapsed_time(e1) / reps)
         gather = {"ms_per_step": gms, "tflops_dense_equiv": flops_dense / (gms * 1e-3) / 1e12,
                   "collective": "ncclAllGather (torch.distributed all_gather_into_tensor) + unpermute"}
+        # the same gather fused into the epilogue: each rank's rows stored at
+        # their final positions into every rank's full output over P2P
+        from paper_2203_05016_b200.sharded import PeerOutputs
+        outs = PeerOutputs((M, N), torch.bfloat16, world, rank)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            sb.spmm_groups_peers(mats[i % nsets], g0, g1, Bs[i % nsets], outs.ptrs, dtype=torch.bfloat16, ldc=N)
+        e1.record()
+        torch.cuda.synchronize()
+        fms = max_over_ranks(torch, dist, e0.elapsed_time(e1) / reps)
+        barrier()
+        outs.close()
+        gather["fused"] = {"ms_per_step": fms, "tflops_dense_equiv": flops_dense / (fms * 1e-3) / 1e12,
+                           "collective": "none: shflbw_cu_spmm_groups_peers stores every row into all ranks' "
+                                         "outputs over P2P (CUDA IPC) from the epilogue"}
 
     if args.profile:
         if rank == 0:
