@@ -14,21 +14,25 @@
 //     N operand (N = VS in {16, 32, 64, 128}): every V the paper uses maps
 //     to one legal tcgen05.mma shape, and the fp32 accumulator lives in TMEM
 //     (128 lanes x VS columns).
-//   * producer warp: for each 64-column K block, 32 TMA tile::gather4
-//     instructions (one per lane) fetch the 64 activation rows named by the
+//   * producer warps (4 or 8): for each 64-column K block, 32 TMA
+//     tile::gather4 instructions fetch the 64 activation rows named by the
 //     group's column indices straight into the 128B-swizzled MN-major operand
 //     layout; pad columns carry index -1, which TMA zero-fills.  One 2D TMA
 //     tile load fetches the group's 64 x VS value block (V contiguous, the
 //     reference's column-major group layout, include/shflbw/formats.hpp:14-18).
 //     A full/empty mbarrier ring of `stages` slots keeps the loads ahead of
 //     the MMAs (the explicit empty barrier is what the literal Alg. 1 lacks,
-//     tests/test_pipeline.cpp:50-79).
+//     tests/test_pipeline.cpp:50-79).  No integer division on any per-K-block
+//     path (ring counters are stepped; conv taps are decoded per staged
+//     window): these loops are single-thread latency chains.
 //   * MMA warp: one elected thread issues 4 x tcgen05.mma (K=16) per block and
 //     releases the slot with tcgen05.commit.
-//   * epilogue (all 4 warps): tcgen05.ld 32 columns at a time; thread t owns
-//     output column n0+t, so for every group row v the warp writes 32
-//     consecutive elements of output row row_indices[g*V+v] -- the permuted
-//     write-back fused into the epilogue with fully coalesced stores.
+//   * epilogue (4 warps, TMEM lane quarters): 16-bit outputs are read with
+//     tcgen05.ld.16x256b, packed and transposed into a [VS][128] shared tile
+//     with stmatrix; fp32 / K-split outputs with tcgen05.ld.32x32b; then every
+//     output row row_indices[g*V+v] is written with coalesced 16-byte stores
+//     -- the permuted write-back fused into the epilogue (optionally into
+//     several GPUs' outputs: the fused all-gather).
 //   * V split across a cluster of CS CTAs (CS*VS = V): each CTA owns VS of the
 //     group's rows; the activation gathers are split between the CTAs and
 //     multicast to all of them, so a group's activation tile is read from L2
