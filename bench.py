@@ -362,6 +362,7 @@ def main():
                          "into the epilogue (P2P stores)")
     ap.add_argument("--soak", type=float, default=0.3, help="seconds of untimed replays to settle clocks")
     ap.add_argument("--e2e-steps", type=int, default=500)
+    ap.add_argument("--e2e-streams", type=int, default=6, help="e2e: steps in flight (round-robin streams)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baselines, few steps")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
@@ -523,7 +524,7 @@ def main():
     # compute of another (the copy engines and the SMs run concurrently).
     a0 = mats[0]
     out_rows = my_groups * V if wl["sharded"] else M
-    nstr = 3
+    nstr = args.e2e_streams
     streams = [torch.cuda.Stream() for _ in range(nstr)]
     Bh = [Bs[i % nsets].cpu().pin_memory() for i in range(nstr)]
     Ch = [torch.empty((out_rows, N), dtype=torch.bfloat16).pin_memory() for _ in range(nstr)]
@@ -579,7 +580,7 @@ def main():
            "h2d_bytes_per_step": Bh[0].numel() * Bh[0].element_size(),
            "d2h_bytes_per_step": Ch[0].numel() * Ch[0].element_size(), "steps": e2e_steps,
            "path": ("C ABI shflbw_cu_spmm (ctypes) with cudaMemcpyAsync (cuda-python) of pinned host B/C: "
-                    "H2D + SpMM + D2H per step, 3 streams round-robin")}
+                    f"H2D + SpMM + D2H per step, {nstr} streams round-robin")}
 
     # ---- roofline of the dominant kernel (the SpMM, one launch per step) ---
     hbm, tfl_burst, tfl_sus, peak_kind = load_peaks()
