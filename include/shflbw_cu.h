@@ -105,13 +105,23 @@ int shflbw_cu_version(void);
  * one such wave), "gather_warps" (4 or 8 warps issuing the TMA gathers per
  * CTA; 0 = auto: 8 for unsplit units of >= 5 K blocks), "cp_async_slabs"
  * (0..2 activation slabs filled by cp.async instead of TMA gather4),
- * "no_bulk_out" (1: per-element output stores).  All variants give results
+ * "no_bulk_out" (1: per-element output stores), "strict" (1: a BF16/F16
+ * matrix outside the tcgen05 envelope returns UNSUPPORTED with the reason
+ * instead of running the CUDA-core kernel), "raster" (persistent unit order:
+ * 0 = auto, 1 = group-major, 2 = column-tile-major), "tile_n" (output columns
+ * per unit: 0 = auto, 128, or 64 = half-width units for grids that would
+ * leave SMs idle).  All variants give results
  * within the same tolerance; V split, cp.async, gather warps and persistent
  * are bit-identical to the default.
  * Unknown key: BAD_PARAMS. */
 int shflbw_cu_set_option(const char* key, int64_t value);
 /* Number of kernels this library launched on the calling thread so far. */
 int64_t shflbw_cu_launch_count(void);
+/* The kernel variant of the last SpMM / conv call on the calling thread:
+ * "k_spmm_tc ..." / "k_spmm_persist ..." (tcgen05; kind, V, V per CTA,
+ * cluster size and split, gather warps, stages, tiles) or "k_spmm_simt ..."
+ * (the CUDA-core kernel).  Lets callers and tests prove which path ran. */
+const char* shflbw_cu_last_plan(void);
 
 /* ---- converter (replaces validate_pattern(ShflBW), src/formats.cpp:113-138,
  *      and compress_shflbw, include/shflbw/formats.hpp:98-99 /
@@ -333,6 +343,12 @@ int shflbw_cu_tile_mma(float* acc, const float* a_tile, const float* b_tile, int
 /* dst[i] = (dst_dtype) src[i], RNE; src_dtype/dst_dtype any of F32/BF16/F16. */
 int shflbw_cu_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype,
                       int64_t n, shflbw_stream_t stream);
+/* Pitched form: dst[r*ld_dst + c] = (dst_dtype) src[r*ld_src + c] for r < rows,
+ * c < cols (one launch; e.g. an fp32 host matrix into a 16-byte aligned
+ * 16-bit operand). */
+int shflbw_cu_convert_2d(const void* src, int32_t src_dtype, int64_t ld_src, void* dst,
+                         int32_t dst_dtype, int64_t ld_dst, int64_t rows, int64_t cols,
+                         shflbw_stream_t stream);
 
 #ifdef __cplusplus
 }

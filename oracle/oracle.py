@@ -541,12 +541,80 @@ def smx1_encode(p: Packed) -> bytes:
     return b"".join(parts)
 
 
+def _smx1_walk_other(b: bytes, pos: int, kind: int, M: int, K: int, V: int, G: int) -> bool:
+    """True if the payload of another kind is corrupt (decode_container,
+    src/container.cpp:158-238: kind 0 dense, 1 mask, 2 vector-wise
+    read_vector_wise_payload :90-115, 4 block-wise)."""
+    n = len(b)
+
+    def u32():
+        nonlocal pos
+        if n - pos < 4:
+            raise ValueError
+        v = int.from_bytes(b[pos:pos + 4], "little")
+        pos += 4
+        return v
+
+    def skip_f32s(count):
+        nonlocal pos
+        if count > (n - pos) // 4:
+            raise ValueError
+        pos += 4 * count
+    try:
+        if kind == 0:
+            start = pos
+            skip_f32s(M * K)
+            if pos != n:
+                return True
+            vals = np.frombuffer(b, "<u4", M * K, start)
+            return bool(np.any((vals & 0x7F800000) == 0x7F800000))
+        if kind == 1:
+            nbytes = (M * K + 7) // 8
+            if pos + nbytes > n:
+                return True
+            return pos + nbytes != n
+        if kind == 2:
+            if V == 0 or V * G != M:
+                return True
+            for _ in range(G):
+                ng = u32()
+                if ng > K:
+                    return True
+                prev = 0
+                for j in range(ng):
+                    c = u32()
+                    if c >= K or (j > 0 and c <= prev):
+                        return True
+                    prev = c
+                skip_f32s(ng * V)
+            return pos != n
+        # kind 4
+        if V == 0 or M % V or K % V:
+            return True
+        nb = u32()
+        if pos + nb * 8 > n:
+            return True
+        prev = None
+        for _ in range(nb):
+            br, bc = u32(), u32()
+            if br >= M // V or bc >= K // V:
+                return True
+            if prev is not None and (br, bc) <= prev:
+                return True
+            prev = (br, bc)
+        skip_f32s((nb * V * V) % (1 << 64))
+        return pos != n
+    except ValueError:
+        return True
+
+
 def smx1_decode(b: bytes) -> tuple[int, "Packed | None"]:
     """decode_container + as_shflbw (src/container.cpp:147-215, :90-124,
     :126-134): (status, matrix).  Status codes as include/shflbw_cu.h:
     3 BadParams (another kind), 7 BadMagic, 8 UnsupportedVersion,
-    9 CorruptPayload.  Only kind 3 payloads are walked; other valid kinds
-    decode in the reference and then fail as_shflbw with BadParams."""
+    9 CorruptPayload.  Other kinds are walked with the reference's checks
+    (_smx1_walk_other): corrupt -> CorruptPayload, valid -> as_shflbw's
+    BadParams."""
     if len(b) < 4 or b[:4] != SMX1_MAGIC:
         return 7, None
     pos = 4
@@ -563,8 +631,8 @@ def smx1_decode(b: bytes) -> tuple[int, "Packed | None"]:
         if version != 1:
             return 8, None
         kind, M, K, V, G = (int(x) for x in u32s(5))
-        if kind in (0, 1, 2, 4):
-            return 3, None
+        if kind in (0, 1, 2, 4):  # decoded and validated first, then as_shflbw's BadParams
+            return (9 if _smx1_walk_other(b, pos, kind, M, K, V, G) else 3), None
         if kind != 3:
             return 9, None
         ri = u32s(M)

@@ -43,6 +43,7 @@ SIGNATURES = {
     "shflbw_cu_version": (C.c_int, []),
     "shflbw_cu_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
     "shflbw_cu_launch_count": (C.c_int64, []),
+    "shflbw_cu_last_plan": (C.c_char_p, []),
     "shflbw_cu_validate": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_uint32), C.c_void_p]),
     "shflbw_cu_compress": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
@@ -91,6 +92,8 @@ SIGNATURES = {
     "shflbw_cu_tile_mma": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_void_p]),
     "shflbw_cu_convert": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]),
+    "shflbw_cu_convert_2d": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_int64,
+                                       C.c_int64, C.c_int64, C.c_void_p]),
 }
 
 _lib = None

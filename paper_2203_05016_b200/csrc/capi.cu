@@ -11,11 +11,13 @@ namespace sbw {
 
 namespace {
 thread_local std::string g_error;
+thread_local std::string g_plan;
 thread_local int64_t g_launches = 0;
-std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0}, g_pdl{1}, g_cps{0}, g_trace{0}, g_nobulk{0}, g_split_mode{0}, g_persist{0}, g_gw{0};
+std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0}, g_pdl{1}, g_cps{0}, g_trace{0}, g_nobulk{0}, g_split_mode{0}, g_persist{0}, g_gw{0}, g_strict{0}, g_raster{0}, g_tile_n{0};
 }  // namespace
 
 void set_error(const std::string& msg) { g_error = msg; }
+void set_plan(const std::string& plan) { g_plan = plan; }
 int fail(int code, const std::string& msg) {
     g_error = msg;
     return code;
@@ -37,6 +39,9 @@ int64_t option(const char* key) {
     if (!std::strcmp(key, "split_mode")) return g_split_mode.load();
     if (!std::strcmp(key, "persistent")) return g_persist.load();
     if (!std::strcmp(key, "gather_warps")) return g_gw.load();
+    if (!std::strcmp(key, "strict")) return g_strict.load();
+    if (!std::strcmp(key, "raster")) return g_raster.load();
+    if (!std::strcmp(key, "tile_n")) return g_tile_n.load();
     return 0;
 }
 
@@ -65,7 +70,9 @@ int run_spmm(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b
     if (g_end <= g_begin || b.N == 0) return SHFLBW_OK;
     if (!option("force_simt") && a->dtype != SHFLBW_F32) {  // fp32: the exact CUDA-core path
         const int st = spmm_tc(a, g_begin, g_end, b, c, s);
-        if (st != SHFLBW_UNSUPPORTED) return st;
+        // strict: a 16-bit matrix outside the tcgen05 envelope is an error
+        // (the message names the reason), not a silent CUDA-core fallback
+        if (st != SHFLBW_UNSUPPORTED || option("strict")) return st;
     }
     if (c.n_extra > 0)
         return fail(SHFLBW_UNSUPPORTED, "spmm with peer destinations: needs the tcgen05 path (bf16/f16 matrix, V in "
@@ -118,7 +125,11 @@ int shflbw_cu_set_option(const char* key, int64_t value) {
     if (!key) return fail(SHFLBW_BAD_PARAMS, "null option key");
     if (!std::strcmp(key, "force_simt")) g_force_simt = value;
     else if (!std::strcmp(key, "split")) g_split = value;
-    else if (!std::strcmp(key, "stages")) g_stages = value;
+    else if (!std::strcmp(key, "stages")) {
+        // the epilogue stages its output tile in >= 2 pipeline slots
+        if (value != 0 && (value < 2 || value > 32)) return fail(SHFLBW_BAD_PARAMS, "stages must be 0 (auto) or 2..32");
+        g_stages = value;
+    }
     else if (!std::strcmp(key, "pdl")) g_pdl = value;
     else if (!std::strcmp(key, "cp_async_slabs")) g_cps = value;
     else if (!std::strcmp(key, "trace")) g_trace = value;
@@ -126,11 +137,16 @@ int shflbw_cu_set_option(const char* key, int64_t value) {
     else if (!std::strcmp(key, "split_mode")) g_split_mode = value;
     else if (!std::strcmp(key, "persistent")) g_persist = value;
     else if (!std::strcmp(key, "gather_warps")) g_gw = value;
+    else if (!std::strcmp(key, "strict")) g_strict = value;
+    else if (!std::strcmp(key, "raster")) g_raster = value;
+    else if (!std::strcmp(key, "tile_n")) g_tile_n = value;
     else return fail(SHFLBW_BAD_PARAMS, std::string("unknown option ") + key);
     return SHFLBW_OK;
 }
 
 int64_t shflbw_cu_launch_count(void) { return g_launches; }
+
+const char* shflbw_cu_last_plan(void) { return g_plan.c_str(); }
 
 int shflbw_cu_validate(const uint8_t* mask, int32_t M, int32_t K, int32_t V, int32_t* pass,
                        uint32_t* fail_row, shflbw_stream_t stream) {
@@ -290,6 +306,15 @@ int shflbw_cu_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst
                       shflbw_stream_t stream) {
     if (check_out_dtype(src_dtype) || check_out_dtype(dst_dtype)) return SHFLBW_BAD_PARAMS;
     return convert_impl(src, src_dtype, dst, dst_dtype, n, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int shflbw_cu_convert_2d(const void* src, int32_t src_dtype, int64_t ld_src, void* dst, int32_t dst_dtype,
+                         int64_t ld_dst, int64_t rows, int64_t cols, shflbw_stream_t stream) {
+    if (check_out_dtype(src_dtype) || check_out_dtype(dst_dtype)) return SHFLBW_BAD_PARAMS;
+    if (rows < 0 || cols < 0 || ld_src < cols || ld_dst < cols)
+        return fail(SHFLBW_BAD_PARAMS, "convert_2d: bad extents / leading dimensions");
+    return convert_2d_impl(src, src_dtype, ld_src, dst, dst_dtype, ld_dst, rows, cols,
+                           reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

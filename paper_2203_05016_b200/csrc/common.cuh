@@ -38,6 +38,9 @@ void count_launch(int n = 1);
     } while (0)
 
 int64_t option(const char* key);
+// the kernel variant the last SpMM / conv call on this thread ran
+// (shflbw_cu_last_plan), e.g. "k_spmm_tc kind=0 vs=32 cs=4 split=2x2 ..."
+void set_plan(const std::string& plan);
 
 // ---------------------------------------------------------------------------
 // 16-bit element helpers

@@ -62,6 +62,76 @@ void put(std::vector<uint8_t>& out, const void* src, size_t bytes) {
     out.insert(out.end(), b, b + bytes);
 }
 
+// Walks the payload of another valid kind (0 dense, 1 mask, 2 vector-wise,
+// 4 block-wise) with the reference's checks, in the reference's order
+// (decode_container, src/container.cpp:158-238): nothing is materialised.
+// Returns the CorruptPayload message, or nullptr if the file decodes (the
+// caller then fails as_shflbw's kind check with BadParams, src/container.cpp:126-134).
+const char* walk_other_kind(Reader& r, uint32_t kind, uint32_t m, uint32_t k, uint32_t v, uint32_t g) {
+    static const char* kTrunc = "container truncated";
+    auto done = [&]() -> const char* { return r.pos != r.n ? "trailing bytes after payload" : nullptr; };
+    auto skip_f32s = [&](uint64_t count) -> bool {  // Reader::f32s: count > remaining / 4 -> truncated
+        if (count > (r.n - r.pos) / 4) return false;
+        r.pos += count * 4;
+        return true;
+    };
+    switch (kind) {
+        case 0: {  // dense: values, then trailing bytes, then finiteness
+            const uint64_t count = static_cast<uint64_t>(m) * k;
+            const uint64_t start = r.pos;
+            if (!skip_f32s(count)) return kTrunc;
+            if (const char* e = done()) return e;
+            for (uint64_t i = 0; i < count; ++i) {
+                uint32_t bits;
+                std::memcpy(&bits, r.p + start + 4 * i, 4);
+                if ((bits & 0x7f800000u) == 0x7f800000u) return "dense payload holds non-finite value";
+            }
+            return nullptr;
+        }
+        case 1: {  // mask: ceil(m*k / 8) packed bytes
+            const uint64_t nbytes = (static_cast<uint64_t>(m) * k + 7) / 8;
+            if (r.pos + nbytes > r.n) return kTrunc;
+            r.pos += nbytes;
+            return done();
+        }
+        case 2: {  // vector-wise: read_vector_wise_payload (src/container.cpp:90-115)
+            if (v == 0 || static_cast<uint64_t>(v) * g != m) return "vector-wise header: V * G != M";
+            for (uint32_t gi = 0; gi < g; ++gi) {
+                const uint32_t ng = r.u32();
+                if (!r.ok) return kTrunc;
+                if (ng > k) return "group column count exceeds K";
+                uint32_t prev = 0;
+                for (uint32_t j = 0; j < ng; ++j) {
+                    const uint32_t c = r.u32();
+                    if (!r.ok) return kTrunc;
+                    if (c >= k || (j > 0 && c <= prev)) return "group columns must be strictly increasing and < K";
+                    prev = c;
+                }
+                if (!skip_f32s(static_cast<uint64_t>(ng) * v)) return kTrunc;
+            }
+            return done();
+        }
+        case 4: {  // block-wise (src/container.cpp:213-235)
+            if (v == 0 || m % v != 0 || k % v != 0) return "block-wise header: V must divide M and K";
+            const uint32_t nblocks = r.u32();
+            if (!r.ok) return kTrunc;
+            if (r.pos + static_cast<uint64_t>(nblocks) * 8 > r.n) return kTrunc;
+            uint32_t pbr = 0, pbc = 0;
+            for (uint32_t b = 0; b < nblocks; ++b) {
+                const uint32_t br = r.u32(), bc = r.u32();
+                if (br >= m / v || bc >= k / v) return "block coordinate out of range";
+                if (b > 0 && (br < pbr || (br == pbr && bc <= pbc))) return "block coordinates must be sorted and unique";
+                pbr = br;
+                pbc = bc;
+            }
+            // size_t(nblocks) * v * v, with the reference's 64-bit wrap-around
+            if (!skip_f32s(static_cast<uint64_t>(nblocks) * v * v)) return kTrunc;
+            return done();
+        }
+    }
+    return "unknown container kind";
+}
+
 }  // namespace
 
 extern "C" {
@@ -78,8 +148,12 @@ int shflbw_cu_smx1_decode(const void* bytes, uint64_t nbytes, int32_t value_dtyp
     if (version != 1) return fail(SHFLBW_UNSUPPORTED_VERSION, "SMX1 version " + std::to_string(version));
     const uint32_t kind = r.u32(), M = r.u32(), K = r.u32(), V = r.u32(), G = r.u32();
     if (!r.ok) return fail(SHFLBW_CORRUPT_PAYLOAD, "container truncated");
-    if (kind <= 4 && kind != kKindShflBW)  // a valid other kind: the reference's as_shflbw throws BadParams
+    if (kind <= 4 && kind != kKindShflBW) {
+        // another kind: decoded (and validated) first, as the reference's
+        // decode_container does; a valid one then fails as_shflbw (BadParams)
+        if (const char* e = walk_other_kind(r, kind, M, K, V, G)) return fail(SHFLBW_CORRUPT_PAYLOAD, e);
         return fail(SHFLBW_BAD_PARAMS, "container holds kind " + std::to_string(kind) + ", not a Shfl-BW matrix");
+    }
     if (kind != kKindShflBW) return fail(SHFLBW_CORRUPT_PAYLOAD, "unknown container kind " + std::to_string(kind));
     // sizes are checked against the bytes present before anything is allocated
     if (static_cast<uint64_t>(M) > (nbytes - r.pos) / 4) return fail(SHFLBW_CORRUPT_PAYLOAD, "container truncated");

@@ -585,6 +585,15 @@ __global__ void k_convert(const void* __restrict__ src, int sdt, void* __restric
         store_from_f32(dst, ddt, i, load_as_f32(src, sdt, i));
 }
 
+// pitched copy-convert: one CTA row per matrix row (grid y), threads over columns
+__global__ void k_convert_2d(const void* __restrict__ src, int sdt, int64_t ld_src, void* __restrict__ dst,
+                             int ddt, int64_t ld_dst, int64_t rows, int64_t cols) {
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+        for (int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; c < cols;
+             c += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            store_from_f32(dst, ddt, r * ld_dst + c, load_as_f32(src, sdt, r * ld_src + c));
+}
+
 // ---- host helpers ------------------------------------------------------------
 
 }  // namespace
@@ -1083,6 +1092,16 @@ int convert_impl(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaSt
     if (n <= 0) return SHFLBW_OK;
     k_convert<<<grid_for(n, 256 * 8), 256, 0, s>>>(src, sdt, dst, ddt, n);
     SBW_LAUNCHED("k_convert");
+    return SHFLBW_OK;
+}
+
+int convert_2d_impl(const void* src, int sdt, int64_t ld_src, void* dst, int ddt, int64_t ld_dst, int64_t rows,
+                    int64_t cols, cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return SHFLBW_OK;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((cols + 255) / 256, 64)),
+                    static_cast<unsigned>(std::min<int64_t>(rows, 65535)));
+    k_convert_2d<<<grid, 256, 0, s>>>(src, sdt, ld_src, dst, ddt, ld_dst, rows, cols);
+    SBW_LAUNCHED("k_convert_2d");
     return SHFLBW_OK;
 }
 

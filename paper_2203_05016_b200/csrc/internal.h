@@ -22,6 +22,8 @@ int download_impl(const shflbw_cu_matrix* m, uint32_t* row_indices, uint32_t* gr
 int decompress_impl(const shflbw_cu_matrix* m, float* dense, cudaStream_t s);
 int conv_prepare_impl(const shflbw_cu_matrix* w, int S, shflbw_cu_matrix* out, cudaStream_t s);
 int convert_impl(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s);
+int convert_2d_impl(const void* src, int sdt, int64_t ld_src, void* dst, int ddt, int64_t ld_dst, int64_t rows,
+                    int64_t cols, cudaStream_t s);
 int scan_exclusive(const int* in, int* out, int n, int* total_dev, cudaStream_t s);
 // keep the default stream-ordered pool's memory across synchronisations (convert.cu)
 void retain_pool();

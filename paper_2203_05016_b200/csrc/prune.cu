@@ -506,11 +506,8 @@ int vectorwise_impl(const float* scores, const uint32_t* rows, int M, int K, int
     int P = 1;
     while (P < K) P <<= 1;
     const size_t smem = static_cast<size_t>(P) * 12;
-    static std::atomic<size_t> configured{0};
-    if (smem > configured.load()) {
-        SBW_CUDA(cudaFuncSetAttribute(k_vectorwise, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured.store(smem);
-    }
+    // the attribute is per device: set on every call (not a hot path)
+    SBW_CUDA(cudaFuncSetAttribute(k_vectorwise, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_vectorwise<<<M / V, kVwThreads, smem, s>>>(scores, rows, K, V, kcols, P, mask);
     SBW_LAUNCHED("k_vectorwise");
     return SHFLBW_OK;

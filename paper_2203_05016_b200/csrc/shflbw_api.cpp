@@ -25,6 +25,10 @@
 #include "shflbw/shflbw.hpp"
 #include "shflbw_cu.h"
 
+namespace sbw {
+void retain_pool();  // convert.cu: keep the pool's memory across synchronisations
+}
+
 namespace shflbw {
 namespace {
 
@@ -68,13 +72,16 @@ int compute_dtype() {
 }
 int dtype_size(int dt) { return dt == SHFLBW_F32 ? 4 : 2; }
 
+// Scratch from the device's stream-ordered pool on this thread's stream (a
+// plain cudaMalloc / cudaFree per call synchronises the device).
 struct DeviceBuffer {
     void* p = nullptr;
     explicit DeviceBuffer(size_t bytes) {
-        check_cuda(cudaMalloc(&p, bytes ? bytes : 16), "cudaMalloc");
+        sbw::retain_pool();
+        check_cuda(cudaMallocAsync(&p, bytes ? bytes : 16, stream()), "cudaMallocAsync");
     }
     ~DeviceBuffer() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, stream());
     }
     DeviceBuffer(const DeviceBuffer&) = delete;
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;
@@ -132,13 +139,11 @@ DeviceOperand upload_operand(const float* src, size_t rows, size_t cols, int dty
             check(shflbw_cu_convert(staging.p, SHFLBW_F32, op.buf->p, dtype, static_cast<int64_t>(rows * cols),
                                     sstream()),
                   "convert");
-        } else {
+        } else {  // one pitched convert into the 16-byte aligned rows
             check_cuda(cudaMemsetAsync(op.buf->p, 0, rows * op.ld * dtype_size(dtype), stream()), "memset");
-            for (size_t r = 0; r < rows; ++r)
-                check(shflbw_cu_convert(staging.as<float>() + r * cols, SHFLBW_F32,
-                                        op.buf->as<char>() + r * op.ld * dtype_size(dtype), dtype,
-                                        static_cast<int64_t>(cols), sstream()),
-                      "convert");
+            check(shflbw_cu_convert_2d(staging.p, SHFLBW_F32, static_cast<int64_t>(cols), op.buf->p, dtype, op.ld,
+                                       static_cast<int64_t>(rows), static_cast<int64_t>(cols), sstream()),
+                  "convert");
         }
     }
     check_cuda(cudaStreamSynchronize(stream()), "sync");

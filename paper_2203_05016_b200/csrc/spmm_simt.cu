@@ -142,6 +142,7 @@ int spmm_simt(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& 
         }
         return SHFLBW_OK;
     }
+    set_plan(std::string("k_spmm_simt kind=") + std::to_string(b.kind) + " v=" + std::to_string(a->v));
     if (a->dtype == SHFLBW_F32) return launch<SHFLBW_F32>(a, g_begin, g_end, b, c, s);
     return a->dtype == SHFLBW_BF16 ? launch<SHFLBW_BF16>(a, g_begin, g_end, b, c, s)
                                    : launch<SHFLBW_F16>(a, g_begin, g_end, b, c, s);

@@ -15,13 +15,25 @@
 namespace sbw {
 namespace tc {
 
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
 int num_sms() {
-    static int sms = 0;
+    static std::atomic<int> cache[kMaxDevices];  // per device (0 = not queried yet)
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDevices) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return sms > 0 ? sms : 148;
+    }
+    int sms = cache[dev].load(std::memory_order_relaxed);
     if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
+        cache[dev].store(sms, std::memory_order_relaxed);
     }
     return sms;
 }
@@ -119,12 +131,14 @@ int encode_map_2d(CUtensorMap* map, int dt, const void* ptr, uint64_t inner, uin
 
 int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b, const OutSpec& c,
             cudaStream_t s) {
+    auto unsup = [](const char* why) { return fail(SHFLBW_UNSUPPORTED, std::string("tcgen05 path: ") + why); };
     const int V = a->v;
-    if (V != 16 && V != 32 && V != 64 && V != 128) return SHFLBW_UNSUPPORTED;
-    if ((reinterpret_cast<uintptr_t>(b.ptr) & 15) != 0 || b.N <= 0 || b.K <= 0) return SHFLBW_UNSUPPORTED;
+    if (V != 16 && V != 32 && V != 64 && V != 128) return unsup("V must be 16, 32, 64 or 128");
+    if ((reinterpret_cast<uintptr_t>(b.ptr) & 15) != 0 || b.N <= 0 || b.K <= 0)
+        return unsup("the activation operand must be 16-byte aligned and non-empty");
     int bw = 64;
     if (b.kind == 0) {
-        if (b.ldb % 8 != 0) return SHFLBW_UNSUPPORTED;
+        if (b.ldb % 8 != 0) return unsup("ldb must be a multiple of 8 elements (16-byte rows)");
     } else if (b.kind == 2) {
         // conv order: 128-byte rows of the [C*H][W*Nb] view (capi.cu checked
         // stride 1, Nb in {16, 32}, 64/Nb | Q)
@@ -133,24 +147,24 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         // conv: rows of the [C*H*W][Nb] view are Nb contiguous elements
         if (b.Nb == 16 || b.Nb == 32) bw = b.Nb;
         else if (b.Nb % 64 == 0) bw = 64;
-        else return SHFLBW_UNSUPPORTED;
-        if (static_cast<int64_t>(b.C) * b.H * b.W >= (1LL << 31)) return SHFLBW_UNSUPPORTED;
+        else return unsup("conv batch N must be 16, 32 or a multiple of 64");
+        if (static_cast<int64_t>(b.C) * b.H * b.W >= (1LL << 31)) return unsup("conv input exceeds 2^31 rows");
     }
     // conv column encoding (tc_kernels.cuh conv_encode): fdiv's exact range,
     // R, S <= 16 and the tap's base row < 2^23
     if (b.kind != 0 && (b.K >= (1 << 22) || b.R > 16 || b.S > 16 ||
                         static_cast<int64_t>(b.C) * b.H * (b.kind == 1 ? b.W : 1) >= (1LL << 23)))
-        return SHFLBW_UNSUPPORTED;
+        return unsup("conv geometry outside the column encoding (R, S <= 16, C*R*S < 2^22)");
     const int groups = g_end - g_begin;
     if (groups <= 0) return SHFLBW_OK;
-    if (groups > 65535) return SHFLBW_UNSUPPORTED;
+    if (groups > 65535) return unsup("more than 65535 groups");
     // conv KIND 2 with Q not a multiple of the positions per 64-element
     // activation row: GEMM over a P x qp position grid, padding dropped in the
     // epilogue (TcParams::remap)
     const int ppb = b.kind == 2 ? 64 / b.Nb : 1;
     const int qp = b.kind == 2 ? (b.Q + ppb - 1) / ppb * ppb : b.Q;
     const int64_t n_gemm = b.kind == 2 ? static_cast<int64_t>(b.P) * qp * b.Nb : b.N;
-    if (n_gemm > 0x7fffff00LL) return SHFLBW_UNSUPPORTED;
+    if (n_gemm > 0x7fffff00LL) return unsup("GEMM N exceeds 2^31");
     const int n_tiles = static_cast<int>((n_gemm + kBlockN - 1) / kBlockN);
 
     // Cluster split for grids that would leave SMs idle: CS CTAs share one
@@ -216,7 +230,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         conv_ksplit = cs > 1;
     }
     if (cs != 1 && cs != 2 && cs != 4) return fail(SHFLBW_BAD_PARAMS, "split must be 1, 2 or 4");
-    if (b.kind == 0 && vsplit && (V % cs != 0 || V / cs < 16)) return SHFLBW_UNSUPPORTED;
+    if (b.kind == 0 && vsplit && (V % cs != 0 || V / cs < 16)) return unsup("V split leaves fewer than 16 rows per CTA");
     const int vs = hybrid ? V / 2 : ((vsplit && b.kind == 0) ? V / cs : V);
     const int ksf = hybrid ? 2 : ((vsplit && !conv_ksplit) ? 1 : cs);  // K split factor
 
@@ -261,9 +275,9 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         prm.bulk_out = aligned && !option("no_bulk_out") ? 1 : 0;
         if (c.n_extra > 0) {
             // extra destinations are written by the staged 16-byte stores only
-            if (!prm.bulk_out) return SHFLBW_UNSUPPORTED;
+            if (!prm.bulk_out) return unsup("peer destinations need 16-byte aligned output rows");
             for (int d = 0; d < c.n_extra; ++d)
-                if (reinterpret_cast<uintptr_t>(c.extra[d]) % 16 != 0) return SHFLBW_UNSUPPORTED;
+                if (reinterpret_cast<uintptr_t>(c.extra[d]) % 16 != 0) return unsup("peer destination not 16-byte aligned");
         }
         prm.n_extra = c.n_extra;
         for (int d = 0; d < c.n_extra; ++d) prm.C_extra[d] = c.extra[d];
@@ -344,6 +358,17 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     st = make_map_2d(&tmW, a->dtype, a->values, static_cast<uint64_t>(V), static_cast<uint64_t>(wrows),
                      static_cast<uint64_t>(V) * 2, wbox, kBlockK, wbox * 2);
     if (st) return st;
+    {
+        const char* split = prm.ksplit == 2 ? "2x2" : (prm.ksplit ? "k" : (cs > 1 ? "v" : "none"));
+        std::string plan = std::string(prm.persistent ? "k_spmm_persist" : "k_spmm_tc") +
+                           " kind=" + std::to_string(b.kind) + " v=" + std::to_string(V) + " vs=" + std::to_string(vs) +
+                           " cs=" + std::to_string(cs) + " split=" + split + " gw=" + std::to_string(prm.gw) +
+                           " stages=" + std::to_string(prm.stages) + " n_tiles=" + std::to_string(n_tiles) +
+                           " groups=" + std::to_string(groups);
+        if (prm.persistent) plan += " per_sm=" + std::to_string(prm.per_sm);
+        if (b.kind == 2 && prm.remap) plan += " remap=1";
+        set_plan(plan);
+    }
     if (a->dtype == SHFLBW_BF16)
         return b.kind == 0 ? tc::dispatch<SHFLBW_BF16, 0>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s)
                            : tc::dispatch<SHFLBW_BF16, 1>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s);

@@ -1132,7 +1132,23 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
 
 // ---------------- host side ----------------
 
-int num_sms();
+int num_sms();  // of the current device (cached per device)
+int current_device();
+
+// Per (kernel instantiation, device): the dynamic shared-memory cap set so
+// far.  cudaFuncSetAttribute applies to the current device only, so a
+// process that launches on several GPUs raises it once per device.
+constexpr int kMaxDevices = 64;
+struct SmemCaps {
+    std::atomic<size_t> cap[kMaxDevices];
+    // true if the caller must (re)raise the cap for `smem` bytes on `dev`
+    bool needs(int dev, size_t smem) {
+        return dev < 0 || dev >= kMaxDevices || smem > cap[dev].load(std::memory_order_relaxed);
+    }
+    void set(int dev, size_t smem) {
+        if (dev >= 0 && dev < kMaxDevices) cap[dev].store(smem, std::memory_order_relaxed);
+    }
+};
 
 template <int DT, int VS, int CS, int KIND, int KSPLIT, int GW>
 int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
@@ -1143,10 +1159,10 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     const size_t smem = static_cast<size_t>(prm.stages) * kStage + recv + 1024 + kMetaBlocks * kBlockK * 4 +
                         (VS < 2 ? 2 : VS) * 4 + (2 * prm.stages + 3) * 8 + 16;
     auto kern = k_spmm_tc<DT, VS, CS, KIND, KSPLIT, GW>;
-    static std::atomic<size_t> configured{0};  // per instantiation: raise the smem cap once
-    if (smem > configured.load(std::memory_order_relaxed)) {
+    static SmemCaps configured;  // per instantiation and device: raise the smem cap once
+    if (const int dev = current_device(); configured.needs(dev, smem)) {
         SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        configured.store(smem, std::memory_order_relaxed);
+        configured.set(dev, smem);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_tiles * CS, groups, 1);
@@ -1178,11 +1194,11 @@ int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParam
                         2 * kMetaBlocks * kBlockK * 4 + (VS < 4 ? 4 : VS) * 4 + ((groups + 2) & ~1) * 4 +
                         (2 * prm.stages + 5) * 8 + 16;
     auto kern = k_spmm_persist<DT, VS, CS, KIND, GW>;
-    static std::atomic<size_t> configured{0};
-    if (smem > configured.load(std::memory_order_relaxed)) {
+    static SmemCaps configured;
+    if (const int dev = current_device(); configured.needs(dev, smem)) {
         SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        configured.store(smem, std::memory_order_relaxed);
+        configured.set(dev, smem);
     }
     const int units = n_tiles * groups;
     const int per_sm = prm.per_sm;

@@ -152,7 +152,11 @@ def _full_fused(self, b: torch.Tensor, outputs: PeerOutputs) -> torch.Tensor:
     kernels are complete (barrier)."""
     import torch.distributed as dist
     if self.plan.world > 1:
-        dist.barrier(group=self.group)  # every rank is done reading the previous result
+        # every rank is done reading the previous result: its enqueued readers
+        # must have finished on the device, not just been issued (a host
+        # barrier alone lets a peer's epilogue overwrite rows still being read)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
     self.sb.spmm_groups_peers(self.a, self.g0, self.g1, b, outputs.ptrs, dtype=outputs.buf.dtype,
                               ldc=outputs.buf.stride(0))
     if self.plan.world > 1:

@@ -520,3 +520,10 @@ def set_option(key: str, value: int) -> None:
 
 def launch_count() -> int:
     return int(_lib().shflbw_cu_launch_count())
+
+
+def last_plan() -> str:
+    """The kernel variant the last SpMM / conv call on this thread ran
+    (shflbw_cu_last_plan): "k_spmm_tc ...", "k_spmm_persist ..." or
+    "k_spmm_simt ..."."""
+    return _lib().shflbw_cu_last_plan().decode()

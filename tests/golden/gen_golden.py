@@ -293,6 +293,48 @@ def smx1_cases(ref: Reference) -> list[dict]:
         "col_out_of_range": patch(base, g0 + 4, K),
         "cols_not_increasing": patch(base, g0 + 8, int.from_bytes(base[g0 + 4:g0 + 8], "little")),
     }
+    # other kinds: the reference decodes (and validates) the payload before
+    # as_shflbw rejects the kind, so a corrupt one is CorruptPayload
+    import struct
+
+    def hdr(kind, m, k, v, g):
+        return b"SMX1" + struct.pack("<6I", 1, kind, m, k, v, g)
+
+    def f32(*xs):
+        return struct.pack(f"<{len(xs)}f", *xs)
+
+    def u32(*xs):
+        return struct.pack(f"<{len(xs)}I", *xs)
+    dense_ok = ref.smx1_encode_dense(ref.random_dense(2, 3, 11))
+    vw_ok = hdr(2, 4, 5, 2, 2) + u32(2, 0, 3) + f32(1, 2, 3, 4) + u32(1, 4) + f32(5, 6)
+    bw_ok = hdr(4, 4, 4, 2, 0) + u32(2, 0, 1, 1, 0) + f32(*range(8))
+    bad.update({
+        "dense_truncated": dense_ok[:-4],
+        "dense_trailing": dense_ok + b"\0\0\0\0",
+        "dense_nan": dense_ok[:-4] + f32(float("nan")),
+        "dense_inf": dense_ok[:32] + f32(float("inf")) + dense_ok[36:],
+        "mask_ok": hdr(1, 3, 5, 0, 0) + bytes([0b01001001, 0b0101]),
+        "mask_truncated": hdr(1, 3, 5, 0, 0) + bytes([0b01001001]),
+        "mask_trailing": hdr(1, 3, 5, 0, 0) + bytes([1, 2, 3]),
+        "vw_ok": vw_ok,
+        "vw_vg_mismatch": hdr(2, 4, 5, 2, 3) + vw_ok[28:],
+        "vw_v_zero": hdr(2, 4, 5, 0, 2) + vw_ok[28:],
+        "vw_cols_not_increasing": hdr(2, 4, 5, 2, 2) + u32(2, 3, 3) + f32(1, 2, 3, 4) + u32(1, 4) + f32(5, 6),
+        "vw_col_out_of_range": hdr(2, 4, 5, 2, 2) + u32(2, 0, 5) + f32(1, 2, 3, 4) + u32(1, 4) + f32(5, 6),
+        "vw_ncols_exceeds_k": hdr(2, 4, 5, 2, 2) + u32(6) + vw_ok[32:],
+        "vw_truncated": vw_ok[:-2],
+        "vw_trailing": vw_ok + b"\0",
+        "bw_ok": bw_ok,
+        "bw_v_not_dividing": hdr(4, 4, 5, 2, 0) + bw_ok[28:],
+        "bw_v_zero": hdr(4, 4, 4, 0, 0) + bw_ok[28:],
+        "bw_coord_out_of_range": hdr(4, 4, 4, 2, 0) + u32(2, 0, 1, 2, 0) + f32(*range(8)),
+        "bw_coords_unsorted": hdr(4, 4, 4, 2, 0) + u32(2, 1, 0, 0, 1) + f32(*range(8)),
+        "bw_coords_duplicate": hdr(4, 4, 4, 2, 0) + u32(2, 0, 1, 0, 1) + f32(*range(8)),
+        "bw_truncated_coords": hdr(4, 4, 4, 2, 0) + u32(2, 0, 1, 1),
+        "bw_truncated_values": bw_ok[:-4],
+        "bw_trailing": bw_ok + b"\0",
+        "bw_missing_count": hdr(4, 4, 4, 2, 0),
+    })
     for name, b in bad.items():
         out.append({"name": name, "hex": b.hex(), "status": ref.smx1_decode(b)[0]})
     return out

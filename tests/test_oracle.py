@@ -295,6 +295,52 @@ def test_smx1_restatement_vs_reference_fuzz(oracle, reference):
             assert np.array_equal(p1.values.view(np.uint32), p2.values.view(np.uint32))
 
 
+def test_smx1_other_kinds_vs_reference_fuzz(oracle, reference):
+    """Containers of the other kinds (dense, mask, vector-wise, block-wise)
+    with one random word or length corrupted: the restatement's walk gives the
+    reference's status (CorruptPayload, or BadParams for a valid file)."""
+    import struct
+    from oracle import smx1_decode
+    rs = np.random.RandomState(11)
+
+    def hdr(kind, m, k, v, g):
+        return b"SMX1" + struct.pack("<6I", 1, kind, m, k, v, g)
+    for t in range(400):
+        kind = int(rs.choice([0, 1, 2, 4]))
+        V = int(rs.choice([1, 2, 4]))
+        m, k = V * int(rs.randint(1, 4)), V * int(rs.randint(1, 4))
+        if kind == 0:
+            body = rs.rand(m * k).astype("<f4").tobytes()
+            h = hdr(0, m, k, 0, 0)
+        elif kind == 1:
+            body = rs.randint(0, 256, (m * k + 7) // 8).astype(np.uint8).tobytes()
+            h = hdr(1, m, k, 0, 0)
+        elif kind == 2:
+            parts = []
+            for _ in range(m // V):
+                c = np.sort(rs.choice(k, int(rs.randint(0, k + 1)), replace=False)).astype("<u4")
+                parts += [struct.pack("<I", len(c)), c.tobytes(), rs.rand(len(c) * V).astype("<f4").tobytes()]
+            body = b"".join(parts)
+            h = hdr(2, m, k, V, m // V)
+        else:
+            nbr, nbc = m // V, k // V
+            sel = sorted(rs.choice(nbr * nbc, int(rs.randint(0, nbr * nbc + 1)), replace=False))
+            body = struct.pack("<I", len(sel)) + b"".join(struct.pack("<II", s // nbc, s % nbc) for s in sel)
+            body += rs.rand(len(sel) * V * V).astype("<f4").tobytes()
+            h = hdr(4, m, k, V, 0)
+        data = bytearray(h + body)
+        r = t % 4
+        if r == 1 and len(data) > 8:  # one random word
+            w = int(rs.randint(2, len(data) // 4))
+            data[4 * w:4 * w + 4] = int(rs.choice([0, 1, 2, 3, 7, 2 ** 31, int(rs.randint(0, 2 ** 32))])).to_bytes(4, "little")
+        elif r == 2:
+            data = data[:int(rs.randint(28, len(data) + 1))]
+        elif r == 3:
+            data += bytes(int(rs.randint(1, 6)))
+        data = bytes(data)
+        assert smx1_decode(data)[0] == reference.smx1_decode(data)[0], (t, kind, data.hex())
+
+
 # ---------------------------------------------------------------- pruning fixtures
 
 def _prune_scores(gen, c):

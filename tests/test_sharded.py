@@ -109,8 +109,17 @@ def _fused_worker(rank, world, port, q):
         a = sb.compress_shflbw(W, mask.cuda(), V)
         want = sb.spmm_execute(a, B, out_dtype=torch.bfloat16)
         outs = PeerOutputs((M, N), torch.bfloat16, world, rank)
-        got = ShardedSpMM(a, rank, world).full_fused(B, outs)
-        q.put((rank, bool(torch.equal(got, want))))
+        sh = ShardedSpMM(a, rank, world)
+        got = sh.full_fused(B, outs)
+        ok = bool(torch.equal(got, want))
+        # a reader of the first result enqueued, then a second layer call that
+        # overwrites every rank's buffer: the reader must see the first result
+        snap = got.float() * 1.0
+        B2 = (torch.rand((K, N), generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+        want2 = sb.spmm_execute(a, B2, out_dtype=torch.bfloat16)
+        got2 = sh.full_fused(B2, outs)
+        ok = ok and bool(torch.equal(snap, want.float())) and bool(torch.equal(got2, want2))
+        q.put((rank, ok))
         dist.barrier()
         outs.close()
     except Exception as e:  # report instead of hanging the parent
