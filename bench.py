@@ -2,7 +2,7 @@
 """bench.py -- Shfl-BW SpMM on B200: dense-equivalent TFLOP/s vs cuBLAS.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload ns|lf|ffn] [--no-cpu-baseline]
+                    [--workload ns|lf|ffn] [--no-cpu-baseline] [--no-sharded]
 
 Default workload (BASELINE.json north star, configs[0]): Shfl-BW SpMM
 M/N/K = 2048/128/2048, V = 64, 75 % sparsity, bf16 operands, fp32
@@ -12,29 +12,39 @@ activations, outputs) that their total exceeds the 126 MB L2, so every step
 streams its operands from HBM; the K steps run as CUDA-graph replays and are
 timed with CUDA events on the launching stream (max over ranks).
 
+`--gpus N` runs N ranks, one per GPU: under torchrun (the driver's launch)
+the env gives WORLD_SIZE = N; without it bench.py re-executes itself under
+`torch.distributed.run --nproc-per-node N`.  At N > 1 the headline runs one
+north-star replica per rank (weak scaling: the 32-group layer does not
+shard usefully) and the `sharded_lf` block measures the sharded large-FFN
+layer (16384 x 4096, N = 8192): each rank owns G/N row groups (strong
+scaling), timed compute-only, with an NCCL all-gather + unpermute, and with
+the all-gather fused into the epilogue (P2P stores).  `sharded_lf` is also
+measured at N = 1 (the whole layer on one GPU), the base of that curve.
+
 Printed: ONE JSON line (rank 0) with the driver's contract keys plus
 `roofline` (dominant kernel vs MEASURED_PEAKS.json), `cpu_baseline` (the
 reference's own spmm_execute, compiled from its sources, on this host's
-cores), `e2e` (the same metric through the public API with pinned host
-buffers and the H2D/D2H copies inside the timed region), `clocks` (NVML,
-sampled during the timed region) and the cuBLAS dense bf16 GEMM of the same
-shape.
+cores), `e2e` (the same metric through the C ABI with pinned host buffers and
+the H2D/D2H copies inside the timed region), `clocks` (NVML, sampled during
+the timed region), the cuBLAS dense GEMM of the same shape (torch.mm and
+cuBLASLt best-of-top-k), the same SpMM without programmatic dependent launch
+(`no_pdl`), with fp32 output and with fp16 operands (configs[0] as written).
 
 `--impl reference` times the reference's CPU implementation
 (oracle/_ref/libshflbw_ref.so: /root/reference/proj/src compiled unmodified)
 on the same workload with all host threads; under torchrun only rank 0 runs.
-
-Workloads: ns (default), ffn (Transformer FFN2 512x2048, N=4096, 75 %),
-lf (large FFN 16384x4096, N=8192, 75 %, row groups sharded over ranks:
-strong scaling, optional NCCL all-gather with --allgather).
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -74,6 +84,22 @@ def dist_env():
     return world, rank, local
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(n):
+    """--gpus N without a torchrun environment: run N ranks through
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # --------------------------------------------------------------------------
 # synthetic inputs (SURVEY.md §8(d) shapes; a vector-wise mask with rows
 # scattered by a random permutation, U[-1,1) values rounded to bf16)
@@ -92,10 +118,10 @@ def synth_mask(M, K, V, cpg, seed):
     return mask
 
 
-def uniform_bf16(torch, shape, seed, device):
+def uniform16(torch, shape, seed, device, dtype=None):
     g = torch.Generator(device=device)
     g.manual_seed(seed)
-    return (torch.rand(shape, generator=g, device=device) * 2 - 1).to(torch.bfloat16)
+    return (torch.rand(shape, generator=g, device=device) * 2 - 1).to(dtype or torch.bfloat16)
 
 
 # --------------------------------------------------------------------------
@@ -162,7 +188,7 @@ class ClockSampler:
 # timing helpers
 # --------------------------------------------------------------------------
 
-def graph_time(torch, step_fn, steps, warmup, soak_s, barrier, sampler=None):
+def graph_time(torch, step_fn, steps, warmup, soak_s, barrier):
     """Run `steps` steps (step_fn(i) enqueues step i) as CUDA-graph replays.
     Returns (elapsed_ms over the K timed steps, t0, t1 host stamps)."""
     stream = torch.cuda.Stream()
@@ -228,125 +254,273 @@ def cpu_backend():
     return Oracle(), "port"
 
 
-def cpu_spmm_rate(wl, budget_s, max_calls=None):
-    """Time the CPU spmm_execute on the workload (host copies of the same
-    kind of synthetic inputs).  Returns (tflops_dense_equiv, calls, seconds,
-    cores, kind, sample_desc)."""
-    be, kind = cpu_backend()
-    M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
-    cpg = int(round(wl["alpha"] * K))
-    mask = synth_mask(M, K, V, cpg, 1234)
-    rs = np.random.RandomState(1)
-    W = (rs.rand(M, K).astype(np.float32) * 2 - 1)
-    B = (rs.rand(K, N).astype(np.float32) * 2 - 1)
-    p = be.compress(W, mask, V)
-    cores = os.cpu_count() or 1
-    # bounded sample: all groups if a call fits the budget, else a prefix
-    G = M // V
-    g_sub = G
-    from oracle import Packed
-    def sub(gs):
+class CpuSpmm:
+    """The reference's spmm_execute (or the C port) on host copies of the
+    workload's synthetic inputs, over the first `g_sub` row groups."""
+
+    def __init__(self, wl):
+        self.be, self.kind = cpu_backend()
+        from oracle import Packed
+        self.wl = wl
+        M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
+        cpg = int(round(wl["alpha"] * K))
+        mask = synth_mask(M, K, V, cpg, 1234)
+        rs = np.random.RandomState(1)
+        W = rs.rand(M, K).astype(np.float32) * 2 - 1
+        self.B = rs.rand(K, N).astype(np.float32) * 2 - 1
+        self.p = self.be.compress(W, mask, V)
+        self.G = M // V
+        self.cores = (os.cpu_count() or 1) if self.kind == "reference" else 1
+        self._Packed = Packed
+        self.h = None
+        self.use(self.G)
+
+    def use(self, gs):
+        p, V, K = self.p, self.wl["V"], self.wl["K"]
         nc = int(p.group_ncols[:gs].sum())
-        return Packed(gs * V, K, V, np.arange(gs * V, dtype=np.uint32), p.group_ncols[:gs].copy(),
-                      p.cols[:nc].copy(), p.values[: nc * V].copy())
-    a = sub(g_sub)
-    if kind == "reference":
-        ha, hb = be.prebuilt(a, B)
-        call = lambda: be.spmm_prebuilt(ha, hb, cores)
-    else:
-        call = lambda: be.spmm(a, B)
-        cores = 1
-    t = time.perf_counter()
-    call()
-    one = time.perf_counter() - t
-    if one > budget_s / 3 and G > 1:  # shrink the sample
-        g_sub = max(1, int(G * (budget_s / 3) / one))
-        if kind == "reference":
-            be.free_prebuilt(ha, hb)
-            a = sub(g_sub)
-            ha, hb = be.prebuilt(a, B)
-            call = lambda: be.spmm_prebuilt(ha, hb, cores)
+        self.a = self._Packed(gs * V, K, V, np.arange(gs * V, dtype=np.uint32), p.group_ncols[:gs].copy(),
+                              p.cols[:nc].copy(), p.values[: nc * V].copy())
+        self.g_sub = gs
+        if self.kind == "reference":
+            if self.h:
+                self.be.free_prebuilt(*self.h)
+            self.h = self.be.prebuilt(self.a, self.B)
+
+    def call(self):
+        if self.kind == "reference":
+            self.be.spmm_prebuilt(*self.h, self.cores)
         else:
-            a = sub(g_sub)
+            self.be.spmm(self.a, self.B)
+
+    def flops(self):
+        return 2.0 * self.g_sub * self.wl["V"] * self.wl["N"] * self.wl["K"]
+
+    def close(self):
+        if self.h:
+            self.be.free_prebuilt(*self.h)
+            self.h = None
+
+
+def cpu_spmm_rate(wl, budget_s):
+    """The cpu_baseline leg: warm, then as many calls as fit `budget_s`."""
+    c = CpuSpmm(wl)
+    t = time.perf_counter()
+    c.call()
+    one = time.perf_counter() - t
+    if one > budget_s / 3 and c.G > 1:  # shrink the sample
+        c.use(max(1, int(c.G * (budget_s / 3) / one)))
+    t_w = time.perf_counter()
+    while time.perf_counter() - t_w < min(1.0, budget_s / 10):  # warm threads / pages / clocks
+        c.call()
     calls, t0 = 0, time.perf_counter()
     while True:
-        call()
+        c.call()
         calls += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or (max_calls and calls >= max_calls):
+        if el >= budget_s:
             break
-    if kind == "reference":
-        be.free_prebuilt(ha, hb)
-    flops = 2.0 * g_sub * V * N * K * calls
-    desc = (f"{calls} spmm_execute calls on {g_sub}/{G} row groups of the {M}x{K} V={V} "
-            f"{int(wl['alpha'] * 100)}% matrix, N={N}, fp32, TileConfig{{}}, threads={cores}")
-    return flops / el / 1e12, calls, el, cores, kind, desc, g_sub
+    v = c.flops() * calls / el / 1e12
+    desc = (f"{calls} spmm_execute calls after a 1 s warm-up on {c.g_sub}/{c.G} row groups of the "
+            f"{wl['M']}x{wl['K']} V={wl['V']} {int(wl['alpha'] * 100)}% matrix, N={wl['N']}, fp32, "
+            f"TileConfig{{}}, threads={c.cores}")
+    res = {"value": v, "unit": UNIT, "cores": c.cores, "kind": c.kind, "sample": desc, "seconds": el,
+           "ms_per_call": el / calls * 1e3}
+    c.close()
+    return res
 
 
 def run_reference_arm(args, wl, world, rank):
+    """The reference arm: the reference's own spmm_execute on the host cores.
+    Each step = `reps` calls, sized so the K timed steps span >= --ref-seconds
+    after >= 1 s of warm-up (short windows were dominated by thread start-up
+    and cold pages: 8.7 vs 5.2 ms per call in round 1)."""
     if rank != 0:
         return
-    be, kind = cpu_backend()
-    M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
-    cpg = int(round(wl["alpha"] * K))
-    mask = synth_mask(M, K, V, cpg, 1234)
-    rs = np.random.RandomState(1)
-    W = rs.rand(M, K).astype(np.float32) * 2 - 1
-    B = rs.rand(K, N).astype(np.float32) * 2 - 1
-    p = be.compress(W, mask, V)
-    cores = os.cpu_count() or 1
-    G = M // V
-    from oracle import Packed
-
-    def sub(gs):
-        nc = int(p.group_ncols[:gs].sum())
-        return Packed(gs * V, K, V, np.arange(gs * V, dtype=np.uint32), p.group_ncols[:gs].copy(),
-                      p.cols[:nc].copy(), p.values[: nc * V].copy())
-    g_sub = G
-    a = sub(G)
-    if kind == "reference":
-        ha, hb = be.prebuilt(a, B)
-        call = lambda: be.spmm_prebuilt(ha, hb, cores)
-    else:
-        cores = 1
-        call = lambda: be.spmm(a, B)
+    c = CpuSpmm(wl)
     t = time.perf_counter()
-    call()
+    c.call()
     one = time.perf_counter() - t
-    budget = 150.0  # whole run stays within a few minutes
     steps, warm = args.steps, args.warmup
-    if one * (steps + warm) > budget and G > 1:
-        g_sub = max(1, int(G * budget / ((steps + warm) * one)))
-        if kind == "reference":
-            be.free_prebuilt(ha, hb)
-            a = sub(g_sub)
-            ha, hb = be.prebuilt(a, B)
-            call = lambda: be.spmm_prebuilt(ha, hb, cores)
-        else:
-            a = sub(g_sub)
-    for _ in range(warm):
-        call()
+    budget = 150.0  # whole run stays within a few minutes
+    if one * (steps + warm) > budget and c.G > 1:
+        c.use(max(1, int(c.G * budget / ((steps + warm) * one))))
+        t = time.perf_counter()
+        c.call()
+        one = time.perf_counter() - t
+    t_w = time.perf_counter()
+    n_w = 0
+    while n_w < warm or time.perf_counter() - t_w < 1.0:
+        c.call()
+        n_w += 1
+    t = time.perf_counter()
+    c.call()
+    one = time.perf_counter() - t
+    reps = max(1, math.ceil(args.ref_seconds / (steps * max(one, 1e-6))))
     t0 = time.perf_counter()
     for _ in range(steps):
-        call()
+        for _ in range(reps):
+            c.call()
     el = time.perf_counter() - t0
-    flops = 2.0 * g_sub * V * N * K
-    value = flops * steps / el / 1e12
-    sample = (f"each step: one spmm_execute over {g_sub}/{G} row groups of the workload "
-              f"({'full problem' if g_sub == G else 'bounded sample'}), fp32, threads={cores}")
+    value = c.flops() * reps * steps / el / 1e12
+    sample = (f"each step: {reps} spmm_execute call(s) over {c.g_sub}/{c.G} row groups of the workload "
+              f"({'full problem' if c.g_sub == c.G else 'bounded sample'}), fp32, threads={c.cores}; "
+              f"{n_w} warm-up calls; {el:.2f} s timed")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": steps, "warmup": warm, "ms_per_step": el / steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl["desc"], "M": M, "N": N, "K": K, "V": V,
+            "config": {"workload": wl["desc"], "M": wl["M"], "N": wl["N"], "K": wl["K"], "V": wl["V"],
                        "sparsity": 1 - wl["alpha"]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "ms_per_call": el / (steps * reps) * 1e3,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": c.cores, "kind": c.kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    c.close()
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
+
+class RotatingSets:
+    """`n` independent (matrix, B, C) sets of one workload, enough that their
+    total exceeds L2 (or one set if a single set already does)."""
+
+    def __init__(self, torch, sb, wl, dev, dtype, mask, groups, profile=False, out_rows=None):
+        M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
+        G = M // V
+        cpg = int(round(wl["alpha"] * K))
+        self.kpad = (cpg + 63) // 64 * 64
+        self.set_bytes = 2 * M * self.kpad + 4 * G * self.kpad + 4 * M + 2 * K * N + 2 * M * N
+        n = 1 if self.set_bytes > L2_BYTES else min(64, max(2, math.ceil(1.25 * L2_BYTES / self.set_bytes)))
+        if profile:
+            n = min(n, 4)
+        self.n = n
+        self.mats, self.Bs, self.Cs = [], [], []
+        self.compress_ms = None
+        for s in range(n):
+            W = uniform16(torch, (M, K), 100 + s, dev)
+            if s == 0 and not profile:
+                # converter (the reference's compress_shflbw) with a warm allocator:
+                # median wall time of 5 calls, device-resident W and mask
+                ts = []
+                for _ in range(6):
+                    torch.cuda.synchronize()
+                    t = time.perf_counter()
+                    tmp = sb.compress_shflbw(W, mask, V, dtype=dtype)
+                    torch.cuda.synchronize()
+                    ts.append((time.perf_counter() - t) * 1e3)
+                    del tmp
+                self.compress_ms = sorted(ts[1:])[2]
+            self.mats.append(sb.compress_shflbw(W, mask, V, dtype=dtype))
+            self.Bs.append(uniform16(torch, (K, N), 200 + s, dev, dtype))
+            self.Cs.append(torch.empty((out_rows or M, N), dtype=dtype, device=dev))
+            del W
+
+
+def lt_baseline(torch, wl, sets_W, Bs, dev, steps, warmup, barrier, dtype_code):
+    """cuBLASLt best-of-top-k (bench_lib/cublaslt_best.cpp): every returned
+    algorithm timed on set 0, the fastest replayed over the rotating sets."""
+    try:
+        from bench_lib.build import build as build_lt
+        lt = ctypes.CDLL(build_lt())
+    except Exception as e:  # compiler / library missing: report, do not fail the bench
+        return {"error": f"cuBLASLt helper unavailable: {e}"}
+    lt.sbw_lt_select.restype = ctypes.c_int
+    lt.sbw_lt_select.argtypes = [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3 + [ctypes.c_int, ctypes.c_int,
+                                                                              ctypes.POINTER(ctypes.c_float),
+                                                                              ctypes.c_void_p]
+    lt.sbw_lt_run.restype = ctypes.c_int
+    lt.sbw_lt_run.argtypes = [ctypes.c_void_p] * 4
+    M, N, K = wl["M"], wl["N"], wl["K"]
+    Cs = [torch.empty((M, N), dtype=Bs[0].dtype, device=dev) for _ in Bs]
+    best = ctypes.c_float(0)
+    st = torch.cuda.current_stream().cuda_stream
+    n = lt.sbw_lt_select(M, N, K, dtype_code, sets_W[0].data_ptr(), Bs[0].data_ptr(), Cs[0].data_ptr(), 16, 20,
+                         ctypes.byref(best), st)
+    torch.cuda.synchronize()
+    if n <= 0:
+        return {"error": "cublasLtMatmulAlgoGetHeuristic returned no usable algorithm"}
+
+    def step(i):
+        s = i % len(Bs)
+        if lt.sbw_lt_run(sets_W[s].data_ptr(), Bs[s].data_ptr(), Cs[s].data_ptr(),
+                         torch.cuda.current_stream().cuda_stream):
+            raise RuntimeError("cublasLtMatmul failed")
+    ms, _, _ = graph_time(torch, step, steps, warmup, 0.0, barrier)
+    return {"ms_per_step": ms / steps, "tflops": 2.0 * M * N * K * steps / (ms * 1e-3) / 1e12,
+            "algos_timed": n, "select_ms_warm": best.value,
+            "impl": "cuBLASLt, fastest of the top-16 heuristic algorithms (timed), same rotating sets + CUDA graph"}
+
+
+def sharded_lf(torch, sb, dist, world, rank, dev, steps, barrier):
+    """The large-FFN layer (16384 x 4096, N = 8192, 75 %) row-group sharded
+    over the ranks (src/spmm.cpp:137-142 split): compute-only, + NCCL
+    all-gather + unpermute, + fused P2P all-gather; times max over ranks."""
+    wl = WORKLOADS["lf"]
+    M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
+    G = M // V
+    cpg = int(round(wl["alpha"] * K))
+    g0, g1 = G * rank // world, G * (rank + 1) // world
+    mask = torch.from_numpy(synth_mask(M, K, V, cpg, 1234)).to(dev)
+    W = uniform16(torch, (M, K), 100, dev)
+    a = sb.compress_shflbw(W, mask, V)
+    del W, mask
+    B = uniform16(torch, (K, N), 200, dev)
+    C = torch.empty(((g1 - g0) * V, N), dtype=torch.bfloat16, device=dev)
+    flops = 2.0 * M * N * K
+
+    def step(i):
+        sb.spmm_groups(a, g0, g1, B, C, compact=True)
+    ms, _, _ = graph_time(torch, step, steps, 3, 0.0, barrier)
+    plan = sb.last_plan()
+    cms = max_over_ranks(torch, dist, ms / steps)
+    out = {"workload": wl["desc"], "ranks": world, "groups_per_rank": g1 - g0, "plan": plan,
+           "compute_only": {"ms_per_step": cms, "value": flops / (cms * 1e-3) / 1e12, "unit": UNIT},
+           "scaling": "strong"}
+    if world > 1:
+        full = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+        gathered = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+        reps = 10
+        for i in range(2):
+            step(i)
+            dist.all_gather_into_tensor(gathered, C)
+            sb.unpermute_rows(a.row_indices_ptr, gathered, full)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            step(i)
+            dist.all_gather_into_tensor(gathered, C)
+            sb.unpermute_rows(a.row_indices_ptr, gathered, full)
+        e1.record()
+        torch.cuda.synchronize()
+        gms = max_over_ranks(torch, dist, e0.elapsed_time(e1) / reps)
+        out["nccl_allgather"] = {"ms_per_step": gms, "value": flops / (gms * 1e-3) / 1e12, "unit": UNIT,
+                                 "collective": "ncclAllGather (all_gather_into_tensor) + shflbw_cu_unpermute_rows"}
+        del full, gathered
+        from paper_2203_05016_b200.sharded import PeerOutputs
+        outs = PeerOutputs((M, N), torch.bfloat16, world, rank)
+        for _ in range(2):
+            sb.spmm_groups_peers(a, g0, g1, B, outs.ptrs, dtype=torch.bfloat16, ldc=N)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            sb.spmm_groups_peers(a, g0, g1, B, outs.ptrs, dtype=torch.bfloat16, ldc=N)
+        e1.record()
+        torch.cuda.synchronize()
+        fms = max_over_ranks(torch, dist, e0.elapsed_time(e1) / reps)
+        barrier()
+        outs.close()
+        out["fused_p2p"] = {"ms_per_step": fms, "value": flops / (fms * 1e-3) / 1e12, "unit": UNIT,
+                            "collective": "none: shflbw_cu_spmm_groups_peers stores every row into all ranks' "
+                                          "outputs over P2P (CUDA IPC) from the epilogue"}
+    del a, B, C
+    torch.cuda.empty_cache()
+    return out
+
 
 def main():
     ap = argparse.ArgumentParser()
@@ -356,19 +530,39 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ns", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the sharded large-FFN block")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--allgather", action="store_true",
-                    help="lf, N > 1: also time the full-output gather -- NCCL all-gather + unpermute, and fused "
-                         "into the epilogue (P2P stores)")
+    ap.add_argument("--ref-seconds", type=float, default=3.0, help="reference arm: seconds in the timed window")
+    ap.add_argument("--lf-steps", type=int, default=20)
     ap.add_argument("--soak", type=float, default=0.3, help="seconds of untimed replays to settle clocks")
     ap.add_argument("--e2e-steps", type=int, default=500)
     ap.add_argument("--e2e-streams", type=int, default=6, help="e2e: steps in flight (round-robin streams)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no baselines, few steps")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the launch plumbing: N ranks over gloo, rank 0 prints n_gpus; no GPU work")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch(args.gpus))
     world, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference_arm(args, wl, world, rank)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N ranks for --gpus N")
+    if args.dry_run:
+        import torch
+        import torch.distributed as tdist
+        if world > 1:
+            tdist.init_process_group("gloo")
+            t = torch.tensor([float(rank)])
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            ranks_seen = int(t.item()) + 1
+            tdist.destroy_process_group()
+        else:
+            ranks_seen = 1
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": ranks_seen}), flush=True)
+        return
 
     import torch
     import paper_2203_05016_b200 as sb
@@ -390,50 +584,27 @@ def main():
         g0, g1 = 0, G
         scaling = "weak"
     my_groups = g1 - g0
+    out_rows = my_groups * V if wl["sharded"] else M
 
     # ---- inputs: rotating sets whose total exceeds L2 --------------------
     mask = torch.from_numpy(synth_mask(M, K, V, cpg, 1234 + 0)).to(dev)
-    kpad = (cpg + 63) // 64 * 64
-    set_bytes = 2 * M * kpad + 4 * G * kpad + 4 * M + 2 * K * N + 2 * M * N
-    nsets = 1 if set_bytes > L2_BYTES else min(64, max(2, math.ceil(1.25 * L2_BYTES / set_bytes)))
-    if args.profile:
-        nsets = min(nsets, 4)
-    mats, Bs, Cs = [], [], []
-    t_c = None
-    for s in range(nsets):
-        W = uniform_bf16(torch, (M, K), 100 + s, dev)
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        mats.append(sb.compress_shflbw(W, mask, V))
-        torch.cuda.synchronize()
-        if t_c is None and (s == 1 or nsets == 1):
-            t_c = (time.perf_counter() - t) * 1e3
-        Bs.append(uniform_bf16(torch, (K, N), 200 + s, dev))
-        Cs.append(torch.empty((my_groups * V, N) if wl["sharded"] else (M, N), dtype=torch.bfloat16, device=dev))
-        if s == 0 and not args.profile:
-            # converter (the reference's compress_shflbw) with a warm allocator:
-            # median wall time of 5 calls, device-resident W and mask
-            ts = []
-            for _ in range(5):
-                torch.cuda.synchronize()
-                t = time.perf_counter()
-                tmp = sb.compress_shflbw(W, mask, V)
-                torch.cuda.synchronize()
-                ts.append((time.perf_counter() - t) * 1e3)
-                del tmp
-            t_c = sorted(ts)[2]
-        del W
+    rot = RotatingSets(torch, sb, wl, dev, torch.bfloat16, mask, G, args.profile, out_rows)
+    nsets, mats, Bs, Cs = rot.n, rot.mats, rot.Bs, rot.Cs
 
-    def step_ours(i):
-        s = i % nsets
-        if wl["sharded"]:
-            sb.spmm_groups(mats[s], g0, g1, Bs[s], Cs[s], compact=True)
-        else:
-            sb.spmm_execute(mats[s], Bs[s], out=Cs[s])
+    def make_step(mats_, Bs_, Cs_):
+        def step(i):
+            s = i % len(mats_)
+            if wl["sharded"]:
+                sb.spmm_groups(mats_[s], g0, g1, Bs_[s], Cs_[s], compact=True)
+            else:
+                sb.spmm_execute(mats_[s], Bs_[s], out=Cs_[s])
+        return step
+    step_ours = make_step(mats, Bs, Cs)
 
     n_before = sb.launch_count()
     step_ours(0)
     launches_per_step = sb.launch_count() - n_before
+    plan = sb.last_plan()
     torch.cuda.synchronize()
 
     sampler = ClockSampler(torch.cuda.current_device())
@@ -448,51 +619,24 @@ def main():
     total_flops = flops_dense * (1 if wl["sharded"] else world)
     value = total_flops * args.steps / (ms * 1e-3) / 1e12
 
-    # ---- multi-GPU all-gather (lf --allgather): compute + NCCL gather ----
-    gather = None
-    if wl["sharded"] and world > 1 and args.allgather:
-        full = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-        gathered = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 20
-        e0.record()
-        for i in range(reps):
-            step_ours(i)
-            dist.all_gather_into_tensor(gathered, Cs[i % nsets])
-            sb.unpermute_rows(mats[i % nsets].row_indices_ptr, gathered, full)
-        e1.record()
-        torch.cuda.synchronize()
-        gms = max_over_ranks(torch, dist, e0.elapsed_time(e1) / reps)
-        gather = {"ms_per_step": gms, "tflops_dense_equiv": flops_dense / (gms * 1e-3) / 1e12,
-                  "collective": "ncclAllGather (torch.distributed all_gather_into_tensor) + unpermute"}
-        # the same gather fused into the epilogue: each rank's rows stored at
-        # their final positions into every rank's full output over P2P
-        from paper_2203_05016_b200.sharded import PeerOutputs
-        outs = PeerOutputs((M, N), torch.bfloat16, world, rank)
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(reps):
-            sb.spmm_groups_peers(mats[i % nsets], g0, g1, Bs[i % nsets], outs.ptrs, dtype=torch.bfloat16, ldc=N)
-        e1.record()
-        torch.cuda.synchronize()
-        fms = max_over_ranks(torch, dist, e0.elapsed_time(e1) / reps)
-        barrier()
-        outs.close()
-        gather["fused"] = {"ms_per_step": fms, "tflops_dense_equiv": flops_dense / (fms * 1e-3) / 1e12,
-                           "collective": "none: shflbw_cu_spmm_groups_peers stores every row into all ranks' "
-                                         "outputs over P2P (CUDA IPC) from the epilogue"}
-
     if args.profile:
         if rank == 0:
-            print(json.dumps({"profile_run": True, "ms_per_step": ms_step, "value": value}), flush=True)
+            print(json.dumps({"profile_run": True, "ms_per_step": ms_step, "value": value, "plan": plan}),
+                  flush=True)
         return
 
-    # ---- cuBLAS dense bf16 GEMM, same shape, same protocol ---------------
-    cub = None
+    steps_b = min(args.steps, 2000)  # the comparison legs: same protocol, shorter windows
+
+    # ---- the same SpMM without programmatic dependent launch --------------
+    sb.set_option("pdl", 0)
+    nms, _, _ = graph_time(torch, step_ours, steps_b, args.warmup, 0.0, barrier)
+    sb.set_option("pdl", 1)
+    nms = max_over_ranks(torch, dist, nms)
+    no_pdl = {"ms_per_step": nms / steps_b, "value": total_flops * steps_b / (nms * 1e-3) / 1e12,
+              "note": "pdl=0: each launch waits for the previous one to finish before its prologue"}
+
+    # ---- cuBLAS dense GEMM, same shape, same protocol ---------------------
+    cub = lt = None
     if not wl["sharded"] or world == 1:
         Wd = [sb.decompress(m).to(torch.bfloat16) for m in mats]
         Cd = [torch.empty((M, N), dtype=torch.bfloat16, device=dev) for _ in range(nsets)]
@@ -500,43 +644,58 @@ def main():
         def step_cublas(i):
             s = i % nsets
             torch.mm(Wd[s], Bs[s], out=Cd[s])
-        cms, _, _ = graph_time(torch, step_cublas, args.steps, args.warmup, 0.0, barrier)
-        cub = {"ms_per_step": cms / args.steps, "tflops": 2.0 * M * N * K * args.steps / (cms * 1e-3) / 1e12,
-               "impl": "torch.mm bf16 (cuBLAS), dense W*mask, bf16 out, same rotating sets + CUDA graph"}
+        cms, _, _ = graph_time(torch, step_cublas, steps_b, args.warmup, 0.0, barrier)
+        cub = {"ms_per_step": cms / steps_b, "tflops": 2.0 * M * N * K * steps_b / (cms * 1e-3) / 1e12,
+               "impl": "torch.mm bf16 (cuBLAS default heuristic), dense W*mask, bf16 out, same rotating sets + "
+                       "CUDA graph"}
+        lt = lt_baseline(torch, wl, Wd, Bs, dev, steps_b, args.warmup, barrier, 1)
         del Wd, Cd
 
     # ---- fp32-output (parity mode) ----------------------------------------
-    C32 = [torch.empty((M, N), dtype=torch.float32, device=dev) for _ in range(nsets)] if not wl["sharded"] else None
     f32 = None
-    if C32 is not None:
-        def step32(i):
-            s = i % nsets
-            sb.spmm_execute(mats[s], Bs[s], out=C32[s])
-        fms, _, _ = graph_time(torch, step32, args.steps, args.warmup, 0.0, barrier)
-        f32 = {"ms_per_step": fms / args.steps,
-               "tflops_dense_equiv": 2.0 * M * N * K * args.steps / (fms * 1e-3) / 1e12}
+    if not wl["sharded"]:
+        C32 = [torch.empty((M, N), dtype=torch.float32, device=dev) for _ in range(nsets)]
+        fms, _, _ = graph_time(torch, make_step(mats, Bs, C32), steps_b, args.warmup, 0.0, barrier)
+        f32 = {"ms_per_step": fms / steps_b,
+               "tflops_dense_equiv": 2.0 * M * N * K * steps_b / (fms * 1e-3) / 1e12}
         del C32
 
+    # ---- fp16 operands (BASELINE configs[0] as written: fp16 in, fp32 accum)
+    f16 = None
+    if not wl["sharded"]:
+        rot16 = RotatingSets(torch, sb, wl, dev, torch.float16, mask, G, True, out_rows)
+        rot16.n = nsets
+        while len(rot16.mats) < nsets:  # same number of rotating sets as the bf16 run
+            s = len(rot16.mats)
+            W = uniform16(torch, (M, K), 100 + s, dev)
+            rot16.mats.append(sb.compress_shflbw(W, mask, V, dtype=torch.float16))
+            rot16.Bs.append(uniform16(torch, (K, N), 200 + s, dev, torch.float16))
+            rot16.Cs.append(torch.empty((out_rows, N), dtype=torch.float16, device=dev))
+            del W
+        hms, _, _ = graph_time(torch, make_step(rot16.mats, rot16.Bs, rot16.Cs), steps_b, args.warmup, 0.0,
+                               barrier)
+        hms = max_over_ranks(torch, dist, hms)
+        f16 = {"ms_per_step": hms / steps_b, "value": total_flops * steps_b / (hms * 1e-3) / 1e12,
+               "dtype": "f16 operands, fp32 accumulation, f16 out"}
+        Wd16 = [sb.decompress(m).to(torch.float16) for m in rot16.mats]
+        f16["cublaslt"] = lt_baseline(torch, wl, Wd16, rot16.Bs, dev, steps_b, args.warmup, barrier, 2)
+        del rot16, Wd16
+
     # ---- e2e through the public API with pinned host buffers ---------------
-    # Every step copies its activations host->device (pinned), runs the SpMM
-    # through the public Python API and reads the result back device->host.
-    # Steps round-robin over 3 streams so copies of one step overlap the
-    # compute of another (the copy engines and the SMs run concurrently).
+    # Every step: cudaMemcpyAsync H2D of B (pinned host), the C-ABI SpMM
+    # (shflbw_cu_spmm / _spmm_groups, the reference-facing boundary) and
+    # cudaMemcpyAsync D2H of C, on one of `e2e_streams` streams round-robin --
+    # issued through cuda-python and ctypes so the host issue cost (~1 us per
+    # call) stays below the PCIe time of the copies.  The window is
+    # --e2e-steps (default 500) steps, independent of --steps.
     a0 = mats[0]
-    out_rows = my_groups * V if wl["sharded"] else M
     nstr = args.e2e_streams
     streams = [torch.cuda.Stream() for _ in range(nstr)]
     Bh = [Bs[i % nsets].cpu().pin_memory() for i in range(nstr)]
     Ch = [torch.empty((out_rows, N), dtype=torch.bfloat16).pin_memory() for _ in range(nstr)]
     Bd = [torch.empty_like(Bs[0]) for _ in range(nstr)]
     Cdv = [torch.empty((out_rows, N), dtype=torch.bfloat16, device=dev) for _ in range(nstr)]
-    e2e_steps = max(3, min(args.steps, args.e2e_steps))
-
-    # Each step: cudaMemcpyAsync H2D of B (pinned host), the C-ABI SpMM
-    # (shflbw_cu_spmm / _spmm_groups, the reference-facing boundary) and
-    # cudaMemcpyAsync D2H of C, on one of 3 streams -- issued through
-    # cuda-python and ctypes so the host issue cost (~1 us per call) stays
-    # below the PCIe time of the copies.
+    e2e_steps = max(200, args.e2e_steps)
     from cuda.bindings import runtime as rt
     lib = sb.shflbw._lib()
     h2d, d2h = rt.cudaMemcpyKind.cudaMemcpyHostToDevice, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost
@@ -560,36 +719,36 @@ def main():
             raise RuntimeError(f"shflbw_cu_spmm status {st}: {lib.shflbw_cu_last_error()}")
         if rt.cudaMemcpyAsync(p_ch[k], p_cd[k], nb_c, d2h, rts[k])[0] != rt.cudaError_t.cudaSuccess:
             raise RuntimeError("cudaMemcpyAsync D2H failed")
-    for i in range(6):
+    for i in range(2 * nstr):
         e2e_step(i)
     torch.cuda.synchronize()
     barrier()
-    main = torch.cuda.current_stream()
+    main_s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(main)
+    e0.record(main_s)
     for st in streams:
         st.wait_event(e0)
     for i in range(e2e_steps):
         e2e_step(i)
     for st in streams:
-        main.wait_stream(st)
-    e1.record(main)
+        main_s.wait_stream(st)
+    e1.record(main_s)
     torch.cuda.synchronize()
     ems = max_over_ranks(torch, dist, e0.elapsed_time(e1)) / e2e_steps
     e2e = {"value": total_flops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
-           "h2d_bytes_per_step": Bh[0].numel() * Bh[0].element_size(),
-           "d2h_bytes_per_step": Ch[0].numel() * Ch[0].element_size(), "steps": e2e_steps,
+           "h2d_bytes_per_step": nb_b, "d2h_bytes_per_step": nb_c, "steps": e2e_steps,
            "path": ("C ABI shflbw_cu_spmm (ctypes) with cudaMemcpyAsync (cuda-python) of pinned host B/C: "
                     f"H2D + SpMM + D2H per step, {nstr} streams round-robin")}
+    del Bh, Ch, Bd, Cdv
 
     # ---- roofline of the dominant kernel (the SpMM, one launch per step) ---
     hbm, tfl_burst, tfl_sus, peak_kind = load_peaks()
-    kprime = cpg
+    kpad = rot.kpad
     q_bytes = (2 * my_groups * V * kpad + 4 * my_groups * kpad + 4 * my_groups * V + 2 * K * N
                + 2 * my_groups * V * N)
-    useful_flops = 2.0 * my_groups * V * N * kprime
+    useful_flops = 2.0 * my_groups * V * N * cpg
     ridge = tfl_burst * 1e12 / (hbm * 1e9)
-    t_launch = ms_step * 1e-3  # the SpMM is the only kernel in a step
+    t_launch = ms_step * 1e-3 / max(1, launches_per_step)  # the SpMM is the only kernel in a step
     if useful_flops / q_bytes < ridge:
         achieved = q_bytes / t_launch / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm}
@@ -598,8 +757,9 @@ def main():
         roof = {"bound": "tensor", "achieved": achieved, "peak": tfl_burst, "unit": "TFLOP/s",
                 "frac": achieved / tfl_burst}
     roof.update({"traffic": None, "algorithmic_bytes_per_launch": q_bytes, "useful_flops_per_launch": useful_flops,
-                 "peak_source": f"MEASURED_PEAKS.json ({peak_kind}, burst)",
-                 "kernel": "k_spmm_tc (tcgen05 + TMA gather4)"})
+                 "peak_source": f"MEASURED_PEAKS.json ({peak_kind}, burst)", "kernel": plan,
+                 "kernel_us": t_launch * 1e6,
+                 "floor_us": max(q_bytes / (hbm * 1e9), useful_flops / (tfl_burst * 1e12)) * 1e6})
     prof_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     util = None
     if os.path.exists(prof_path):
@@ -610,10 +770,16 @@ def main():
             util = prof.get("tensor_pipe_util_pct")
             roof["traffic_source"] = prof.get("source")
 
+    # ---- the sharded large-FFN layer (north_star's 1/2/4/8-GPU shape) ------
+    shard = None
+    if not args.no_sharded and args.workload != "lf":
+        del rot, mats, Bs, Cs
+        torch.cuda.empty_cache()
+        shard = sharded_lf(torch, sb, dist, world, rank, dev, args.lf_steps, barrier)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, calls, el, cores, kind, desc, _ = cpu_spmm_rate(wl, args.cpu_budget)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc, "seconds": el}
+        cpu = cpu_spmm_rate(wl, args.cpu_budget)
 
     if rank == 0:
         line = {
@@ -623,14 +789,17 @@ def main():
             "config": {"workload": wl["desc"], "M": M, "N": N, "K": K, "V": V, "sparsity": 1 - alpha,
                        "kept_cols_per_group": cpg, "groups": G, "out_dtype": "bf16", "accum": "fp32",
                        "parallelism": (f"row-group shards x{world}" if wl["sharded"] else f"replicas x{world}"),
-                       "l2": (f"{nsets} rotating input sets x {set_bytes / 2**20:.1f} MiB > 126 MB L2"
+                       "l2": (f"{nsets} rotating input sets x {rot.set_bytes / 2**20:.1f} MiB > 126 MB L2"
                               if nsets > 1 else "inputs larger than L2"),
                        "timing": "CUDA graph replays, CUDA events on the launching stream, max over ranks"},
+            "plan": plan,
             "speedup_vs_cublas": (value / world / cub["tflops"]) if cub else None,
-            "cublas": cub, "fp32_out": f32, "tensor_pipe_util_pct": util,
-            "compress_ms": t_c, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "speedup_vs_cublaslt_best": (value / world / lt["tflops"]) if lt and "tflops" in lt else None,
+            "cublas": cub, "cublaslt_best": lt, "no_pdl": no_pdl, "fp32_out": f32, "fp16": f16,
+            "tensor_pipe_util_pct": util, "compress_ms": rot.compress_ms, "roofline": roof, "cpu_baseline": cpu,
+            "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
-            "allgather": gather,
+            "sharded_lf": shard,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -241,7 +241,11 @@ def full_size(ref: Reference) -> list[dict]:
                                            (2048, 128, 2048, 128, 0.25, True),
                                            (4096, 128, 1024, 64, 0.25, True),
                                            (512, 256, 512, 64, 0.5, True),
-                                           (2048, 64, 512, 32, 0.1, True)]:
+                                           (2048, 64, 512, 32, 0.1, True),
+                                           # large FFN (M > 4096: the converter's multi-block radix sort)
+                                           (16384, 8192, 4096, 64, 0.25, False),
+                                           (8192, 128, 2048, 32, 0.25, False),
+                                           (8192, 128, 1024, 128, 0.1, False)]:
         cpg = int(np.floor(alpha * K + 0.5))
         mask = ref.random_shflbw_mask(M, K, V, cpg, ref.rng(1234))
         W = orc.round16(ref.random_dense(M, K, 1))
