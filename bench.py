@@ -772,6 +772,7 @@ def main():
 
     # ---- the sharded large-FFN layer (north_star's 1/2/4/8-GPU shape) ------
     shard = None
+    set_bytes, compress_ms = rot.set_bytes, rot.compress_ms
     if not args.no_sharded and args.workload != "lf":
         del rot, mats, Bs, Cs
         torch.cuda.empty_cache()
@@ -789,14 +790,14 @@ def main():
             "config": {"workload": wl["desc"], "M": M, "N": N, "K": K, "V": V, "sparsity": 1 - alpha,
                        "kept_cols_per_group": cpg, "groups": G, "out_dtype": "bf16", "accum": "fp32",
                        "parallelism": (f"row-group shards x{world}" if wl["sharded"] else f"replicas x{world}"),
-                       "l2": (f"{nsets} rotating input sets x {rot.set_bytes / 2**20:.1f} MiB > 126 MB L2"
+                       "l2": (f"{nsets} rotating input sets x {set_bytes / 2**20:.1f} MiB > 126 MB L2"
                               if nsets > 1 else "inputs larger than L2"),
                        "timing": "CUDA graph replays, CUDA events on the launching stream, max over ranks"},
             "plan": plan,
             "speedup_vs_cublas": (value / world / cub["tflops"]) if cub else None,
             "speedup_vs_cublaslt_best": (value / world / lt["tflops"]) if lt and "tflops" in lt else None,
             "cublas": cub, "cublaslt_best": lt, "no_pdl": no_pdl, "fp32_out": f32, "fp16": f16,
-            "tensor_pipe_util_pct": util, "compress_ms": rot.compress_ms, "roofline": roof, "cpu_baseline": cpu,
+            "tensor_pipe_util_pct": util, "compress_ms": compress_ms, "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
             "sharded_lf": shard,

@@ -165,7 +165,22 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     const int qp = b.kind == 2 ? (b.Q + ppb - 1) / ppb * ppb : b.Q;
     const int64_t n_gemm = b.kind == 2 ? static_cast<int64_t>(b.P) * qp * b.Nb : b.N;
     if (n_gemm > 0x7fffff00LL) return unsup("GEMM N exceeds 2^31");
-    const int n_tiles = static_cast<int>((n_gemm + kBlockN - 1) / kBlockN);
+    // Output columns per unit ("tile_n"): 128, or 64 -- half-width units for
+    // SpMM grids whose 128-column units leave most SMs idle (the north star:
+    // 32 groups x 1 tile).  Twice the units, each gathering half the
+    // activation bytes with unicast TMA (cheaper than the V split's
+    // multicast), before any cluster split is considered.  Auto: 64 when
+    // twice the 128-column units still fit one wave.
+    int tile_n = 128;
+    {
+        const int64_t tn = option("tile_n");
+        if (tn != 0 && tn != 64 && tn != 128) return fail(SHFLBW_BAD_PARAMS, "tile_n must be 0, 64 or 128");
+        const int64_t units128 = (n_gemm + kBlockN - 1) / kBlockN * groups;
+        const bool can = b.kind == 0 && option("cp_async_slabs") == 0 && option("persistent") <= 0 && n_gemm > 64;
+        if (tn == 64 && can) tile_n = 64;
+        else if (tn == 0 && can && units128 * 2 <= num_sms()) tile_n = 64;
+    }
+    const int n_tiles = static_cast<int>((n_gemm + tile_n - 1) / tile_n);
 
     // Cluster split for grids that would leave SMs idle: CS CTAs share one
     // (group, column tile).  Each SM fills its activation tiles at the TMA
@@ -265,6 +280,14 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.Q = b.Q;
     prm.PQ = b.P * qp;
     prm.ksplit = hybrid ? 2 : ((cs > 1 && (!vsplit || conv_ksplit)) ? 1 : 0);
+    prm.tile_n = tile_n;
+    {
+        const int64_t r = option("raster");
+        if (r < 0 || r > 2) return fail(SHFLBW_BAD_PARAMS, "raster must be 0, 1 or 2");
+        // auto: column-tile-major once the weights are large and B is shared
+        // by many groups (large FFN: B streams once, weights stay in L2)
+        prm.raster = r ? static_cast<int>(r) : (groups >= 16 && n_tiles >= 2 ? 2 : 1);
+    }
     prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
     if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");
     prm.trace = option("trace") > 1 ? reinterpret_cast<unsigned long long*>(option("trace")) : nullptr;
@@ -292,7 +315,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         // per-unit kernel wins: FFN2 N=4096 256 units 7.4 vs 8.3 us)
         int64_t opt = option("persistent");
         if (opt == 0) opt = (units * cs > 2LL * num_sms()) ? 2 : -1;
-        prm.persistent = !prm.ksplit && opt > 0 && groups <= 4096 ? 1 : 0;
+        prm.persistent = !prm.ksplit && opt > 0 && groups <= 4096 && tile_n == kBlockN ? 1 : 0;
         prm.per_sm = static_cast<int>(std::min<int64_t>(2, std::max<int64_t>(1, opt)));  // launch bounds: 2
     }
     int stages = static_cast<int>(option("stages"));
@@ -365,7 +388,8 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
                            " cs=" + std::to_string(cs) + " split=" + split + " gw=" + std::to_string(prm.gw) +
                            " stages=" + std::to_string(prm.stages) + " n_tiles=" + std::to_string(n_tiles) +
                            " groups=" + std::to_string(groups);
-        if (prm.persistent) plan += " per_sm=" + std::to_string(prm.per_sm);
+        if (prm.persistent) plan += " per_sm=" + std::to_string(prm.per_sm) + " raster=" + std::to_string(prm.raster);
+        plan += " tile_n=" + std::to_string(tile_n);
         if (b.kind == 2 && prm.remap) plan += " remap=1";
         set_plan(plan);
     }

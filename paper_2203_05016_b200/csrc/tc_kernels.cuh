@@ -93,6 +93,8 @@ struct TcParams {
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
     int per_sm;      // persistent: resident CTAs per SM
     int gw;          // gather warps per CTA (4, 8)
+    int raster;      // persistent unit order: 1 group-major, 2 column-tile-major
+    int tile_n;      // output columns per unit: 128, or 64 (k_spmm_tc, SpMM only: half-width units)
     int n_extra;     // further output destinations (fused all-gather), staged-store path only
     void* C_extra[kMaxPeers - 1];
 };
@@ -169,7 +171,8 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
     constexpr int kRowsPerInst = 32 / kLanesPerRow;
     constexpr int kIters = (ROWS + 4 * kRowsPerInst - 1) / (4 * kRowsPerInst);
     const int chunk = lane % kLanesPerRow;
-    const int64_t nn = out_col(p, n0 + chunk * (16 / esz));  // a 16-byte chunk never spans two positions
+    // a 16-byte chunk never spans two positions; chunks past a half-width unit are dead
+    const int64_t nn = chunk * (16 / esz) < p.tile_n ? out_col(p, n0 + chunk * (16 / esz)) : -1;
     const int v0 = q * kRowsPerInst + lane / kLanesPerRow;
     if (!BATCH) {  // interleaved: fewer live registers (the persistent kernel's epilogue warps)
         if (nn >= 0) {
@@ -302,7 +305,7 @@ __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row,
             return;
         }
     }
-    const int64_t n = out_col(p, n0 + m);
+    const int64_t n = m < p.tile_n ? out_col(p, n0 + m) : -1;
     const bool live = n >= 0;
 #pragma unroll
     for (int c = 0; c < (VS + 31) / 32; ++c) {
@@ -363,10 +366,11 @@ __device__ __forceinline__ void ksplit_epilogue(const TcParams& p, uint32_t t_ro
         for (int i = 0; i < kW; ++i) vals[c * 32 + i] = __uint_as_float(r[i]);
     }
     // recv holds the KSF-1 peers' partials: peer c's rows land in slot
-    // (c < receiver ? c : c - 1)
+    // (c < receiver ? c : c - 1); columns beyond a half-width unit push nothing
+    const bool mlive = m < p.tile_n;
 #pragma unroll
     for (int c = 0; c < KSF; ++c) {
-        if (c == kr) continue;
+        if (c == kr || !mlive) continue;
         const uint32_t peer = static_cast<uint32_t>(c * VSF + vr);
         const int my_slot = kr < c ? kr : kr - 1;
         const uint32_t slot = smem_u32(recv) + static_cast<uint32_t>((my_slot * kRP * kBlockN + m) * 4);
@@ -413,7 +417,7 @@ __device__ __forceinline__ void ksplit_epilogue(const TcParams& p, uint32_t t_ro
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (m == 0) trace_event(p.trace, 27);
         store_tile_rows<OT, kRP>(p, ctile, rows_s + kr * kRP, q, lane, n0);
-    } else if (const int64_t n = out_col(p, n0 + m); n >= 0) {
+    } else if (const int64_t n = mlive ? out_col(p, n0 + m) : -1; n >= 0) {
         int32_t row[kRP];
 #pragma unroll
         for (int i = 0; i < kRP; ++i) row[i] = rows_s[kr * kRP + i];
@@ -536,7 +540,7 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
     const int n_tile = blockIdx.x / CS;
-    const int n0 = n_tile * kBlockN;
+    const int n0 = n_tile * p.tile_n;  // 128, or 64: half-width units (SpMM only; MMA rows >= 64 unused)
     const int g = p.g_begin + blockIdx.y;
     const int gp = p.group_ptr[g];
     const int nkb_all = (p.group_ptr[g + 1] - gp) / kBlockK;
@@ -577,8 +581,8 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
         }
         mbar_init(accum, 1);
         mbar_init(recv_bar, 1);
-        if (kKSplit)  // the KSF-1 K peers' partial rows for this CTA
-            mbar_arrive_expect_tx(recv_bar, (KSF - 1) * (VS / KSF) * kBlockN * 4);
+        if (kKSplit)  // the KSF-1 K peers' partial rows for this CTA (tile_n live columns each)
+            mbar_arrive_expect_tx(recv_bar, (KSF - 1) * (VS / KSF) * p.tile_n * 4);
         fence_mbar_init();
         tma_prefetch_desc(&tmB);
         tma_prefetch_desc(&tmW);
@@ -601,7 +605,7 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
             uint32_t ph = 0;  // ring slot and round parity (no runtime division by `stages`)
             for (int kb = 0; kb < nkb; ++kb) {
                 if (kb >= stages) mbar_wait(&empty[s], ph ^ 1);
-                mbar_arrive_expect_tx(&full[s], (2 - cps) * (kABytes / 2) + WL::kBytes);
+                mbar_arrive_expect_tx(&full[s], (p.tile_n / 64 - cps) * (kABytes / 2) + WL::kBytes);
 #pragma unroll
                 for (int sl = 0; sl < WL::kSlabs; ++sl)
                     tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
         const int gw = warp - 2;
         // TMA part: slabs [0, 2-cps): row group rg of slab sl, 16 row groups
         // per slab, spread over the 4 warps' first lanes
-        const int tma_slabs = 2 - cps;
+        const int tma_slabs = p.tile_n / 64 - cps;
         const int nblk = KIND == 0 ? tma_slabs : kBlockN / p.bw;  // MN blocks filled by TMA
         const int blk_bytes = kBlockK * p.bw * 2;
         constexpr int kRGW = 16 / GW;                               // row groups (4 rows) per warp
@@ -793,21 +797,35 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
 
 // (group, column tile) of the units a persistent CTA visits: units advance by
 // a fixed stride (the cluster count), so the pair is stepped with adds -- the
-// divisions happen once per role, not at every unit boundary.
+// divisions happen once per role, not at every unit boundary.  Raster:
+// group-major (unit u = group * n_tiles + tile: consecutive units share a
+// group's weights and column indices) or column-tile-major (u = tile *
+// ngroups + group: the resident CTAs share one activation column slab, so B
+// streams from HBM once while the weights -- re-read once per slab -- stay
+// L2-resident; the large-FFN order).
 struct UnitCursor {
     int u, gl, tile;  // unit, launch-relative group, column tile
-    int stride, step_g, step_t, n_tiles;
-    __device__ __forceinline__ UnitCursor(int u0, int stride_, int nt) : u(u0), stride(stride_), n_tiles(nt) {
-        gl = u0 / nt;
-        tile = u0 - gl * nt;
-        step_g = stride_ / nt;
-        step_t = stride_ - step_g * nt;
+    int stride, o, i, step_o, step_i, n_inner;
+    bool tm;  // column-tile-major
+    __device__ __forceinline__ UnitCursor(int u0, int stride_, int n_tiles, int ngroups, bool tile_major)
+        : u(u0), stride(stride_), tm(tile_major) {
+        n_inner = tm ? ngroups : n_tiles;
+        o = u0 / n_inner;
+        i = u0 - o * n_inner;
+        step_o = stride_ / n_inner;
+        step_i = stride_ - step_o * n_inner;
+        set();
+    }
+    __device__ __forceinline__ void set() {
+        gl = tm ? i : o;
+        tile = tm ? o : i;
     }
     __device__ __forceinline__ void next() {
         u += stride;
-        gl += step_g;
-        tile += step_t;
-        if (tile >= n_tiles) tile -= n_tiles, ++gl;
+        o += step_o;
+        i += step_i;
+        if (i >= n_inner) i -= n_inner, ++o;
+        set();
     }
 };
 
@@ -879,6 +897,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int stages = p.stages;
     const int ngroups = (units + n_tiles - 1) / n_tiles;
+    const bool tmaj = p.raster == 2;  // column-tile-major unit order
     const int out_esz = p.c_dtype == SHFLBW_F32 ? 4 : 2;
     unsigned char* ctile = smem + stages * kStageBytes;  // [VS][128] out (staged stores only)
     int32_t* meta_s = reinterpret_cast<int32_t*>(ctile + (p.bulk_out ? VS * kBlockN * out_esz : 0));  // [2][kMetaBlocks][64]
@@ -930,7 +949,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         if (lane == 0) {
             int kbg = 0, s = 0;
             uint32_t ph = 0;  // ring slot and round parity, carried across units
-            for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next()) {
+            for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next()) {
                 const int gl = c.gl;
                 const int gp = gptr_s[gl];
                 const int nkb = (gptr_s[gl + 1] - gp) / kBlockK;
@@ -953,7 +972,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         if (lane == 0) {
             int s = 0, i = 0;
             uint32_t ph = 0;
-            for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next(), ++i) {
+            for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
                 const int nkb = group_nkb(c.gl);
                 const int b = i & 1;
                 mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
@@ -1016,13 +1035,13 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                 for (int x = et; x < nb * (kBlockK / 4); x += kGT) w[x] = conv_encode4<KIND>(p, w[x]);
             }
         };
-        if (cid < units) load_window(cid / n_tiles, 0, 0, false);
+        if (cid < units) load_window(UnitCursor(cid, nclusters, n_tiles, ngroups, tmaj).gl, 0, 0, false);
         named_bar<kGT>(2);
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
         int kbg = 0, i = 0, s = 0, buf = 0;
         uint32_t ph = 0;
-        for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next(), ++i) {
+        for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
             if (et == 0 && i < 8) trace_event(p.trace, 16 + i);  // gathers: unit i starts issuing
             UnitCursor cn = c;
             cn.next();
@@ -1096,10 +1115,12 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
             return p.compact ? static_cast<int32_t>(static_cast<int64_t>(g - p.g_begin) * p.V + vbase + v)
                              : p.row_indices[static_cast<int64_t>(g) * p.V + vbase + v];
         };
-        int32_t next_row = (cid < units && et < VS) ? row_of(cid / n_tiles, et) : 0;  // static: before the wait
+        int32_t next_row = (cid < units && et < VS)  // static: before the wait
+                               ? row_of(UnitCursor(cid, nclusters, n_tiles, ngroups, tmaj).gl, et)
+                               : 0;
         grid_dependency_wait();  // C may still be read by the previous kernel
         int i = 0;
-        for (UnitCursor c(cid, nclusters, n_tiles); c.u < units; c.next(), ++i) {
+        for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
             const int n0 = c.tile * kBlockN;
             const int nkb = group_nkb(c.gl);
             const int b = i & 1;

@@ -139,7 +139,7 @@ def test_large_ffn_spmm_auto_plan(sb, oracle):
     plan = tc_plan(sb)
     assert plan.startswith("k_spmm_persist"), plan
     C16 = sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16)
-    assert sb.last_plan() == plan
+    assert sb.last_plan().startswith("k_spmm_persist"), sb.last_plan()  # (stages depend on the output tile)
     for c0 in (0, N - 128):
         want = oracle.spmm(p, np.ascontiguousarray(B[:, c0:c0 + 128]))
         got = C[:, c0:c0 + 128].cpu().numpy()

@@ -973,3 +973,58 @@ def test_spmm_groups_peers_errors(sb, oracle):
     o16 = [torch.zeros((256, 64), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
     with pytest.raises(sb.Error):  # exact fp32 matrix: no tcgen05 path, must not silently drop peers
         sb.spmm_groups_peers(a32, 0, a32.group_count(), dev(B), o16)
+
+
+# ------------------------------------------- unit shape / order variants (round 2)
+
+@pytest.mark.parametrize("N", [128, 72, 200, 1000])
+@pytest.mark.parametrize("split,mode", [(1, 0), (2, 1), (4, 1), (2, 3), (4, 2)])
+def test_half_width_units_bitwise(sb, oracle, N, split, mode):
+    """tile_n = 64 (half-width units: twice the CTAs, each gathering one
+    64-column activation slab) computes every output column with the same
+    MMA sequence and K-split reduction order as the 128-column units:
+    identical bits, fp32 and bf16 out, ragged N included."""
+    M, K, V = 1024, 1024, 64
+    mask, W, B = synthetic(oracle, M, K, N, V, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("split", split)
+    sb.set_option("split_mode", mode)
+    outs = {}
+    for tn in (128, 64):
+        sb.set_option("tile_n", tn)
+        outs[tn] = (sb.spmm_execute(a, Bd).cpu().numpy(),
+                    sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
+        assert f"tile_n={tn}" in sb.last_plan(), sb.last_plan()
+    for k in ("tile_n", "split", "split_mode"):
+        sb.set_option(k, 0)
+    assert np.array_equal(outs[64][0], outs[128][0]) and np.array_equal(outs[64][1], outs[128][1])
+    assert oracle.rel_frobenius(outs[64][0], oracle.spmm(p, B)) <= TOL
+
+
+def test_auto_half_width_north_star(sb, oracle):
+    """The auto plan picks half-width units for the north-star grid (32
+    groups x 1 column tile) and stays within tolerance of the oracle."""
+    mask, W, B = synthetic(oracle, 2048, 2048, 128, 64, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, 64)
+    got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
+    assert "tile_n=64" in sb.last_plan(), sb.last_plan()
+    assert oracle.rel_frobenius(got, oracle.spmm(p, B)) <= TOL
+
+
+@pytest.mark.parametrize("V", [32, 64, 128])
+def test_persistent_raster_orders_bitwise(sb, oracle, V):
+    """Persistent unit order (group-major vs column-tile-major) changes only
+    which CTA computes a unit, never how: identical bits."""
+    M, K, N = 4096, 1024, 2048
+    mask, W, B = synthetic(oracle, M, K, N, V, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    outs = {}
+    for r in (1, 2):
+        sb.set_option("raster", r)
+        outs[r] = sb.spmm_execute(a, Bd).cpu().numpy()
+        assert sb.last_plan().startswith("k_spmm_persist") and f"raster={r}" in sb.last_plan(), sb.last_plan()
+    sb.set_option("raster", 0)
+    assert np.array_equal(outs[1], outs[2])
+    assert oracle.rel_frobenius(outs[2][:, :128], oracle.spmm(p, np.ascontiguousarray(B[:, :128]))) <= TOL
