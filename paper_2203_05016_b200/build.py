@@ -70,10 +70,13 @@ def _compile(src: str, force: bool) -> str:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
-    if os.environ.get("SBW_TRACE"):
+    global OBJ, LIB
+    if os.environ.get("SBW_TRACE"):  # development timeline build: own objects, abl/trace.so
         NVCC_FLAGS.append("-DSBW_TRACE")
+        OBJ = os.path.join(PKG, "build_trace")
+        LIB = os.path.join(ROOT, "abl", "trace.so")
     os.makedirs(OBJ, exist_ok=True)
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), srcs))

@@ -165,28 +165,8 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     const int qp = b.kind == 2 ? (b.Q + ppb - 1) / ppb * ppb : b.Q;
     const int64_t n_gemm = b.kind == 2 ? static_cast<int64_t>(b.P) * qp * b.Nb : b.N;
     if (n_gemm > 0x7fffff00LL) return unsup("GEMM N exceeds 2^31");
-    // Output columns per unit ("tile_n"): 128, or 64 -- half-width units for
-    // SpMM grids whose 128-column units leave most SMs idle (the north star:
-    // 32 groups x 1 tile).  Twice the units, each gathering half the
-    // activation bytes with unicast TMA (cheaper than the V split's
-    // multicast), before any cluster split is considered.  Auto: 64 when
-    // twice the 128-column units still fit one wave.
-    int tile_n = 128;
-    {
-        const int64_t tn = option("tile_n");
-        if (tn != 0 && tn != 64 && tn != 128) return fail(SHFLBW_BAD_PARAMS, "tile_n must be 0, 64 or 128");
-        const int64_t units128 = (n_gemm + kBlockN - 1) / kBlockN * groups;
-        const bool can = b.kind == 0 && option("cp_async_slabs") == 0 && option("persistent") <= 0 && n_gemm > 64;
-        if (tn == 64 && can) tile_n = 64;
-        else if (tn == 0 && can && units128 * 2 <= num_sms()) tile_n = 64;
-    }
-    const int n_tiles = static_cast<int>((n_gemm + tile_n - 1) / tile_n);
-
     // Cluster split for grids that would leave SMs idle: CS CTAs share one
-    // (group, column tile).  Each SM fills its activation tiles at the TMA
-    // gather rate (~20 B/cycle received, multicast or not -- DESIGN.md §5),
-    // so splitting K is what shortens a deep group's main loop.  Modes
-    // ("split_mode"):
+    // (group, column tile).  Modes ("split_mode"):
     //   3  V split: each CTA owns V/CS rows; the activation tile is multicast
     //      to all CS CTAs (bit-identical to CS = 1);
     //   1  K split: each gathers 1/CS of the K blocks, fp32 partials reduced
@@ -202,37 +182,66 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     const int min_kb = 2;  // K blocks per CTA worth splitting for
     const int kb_all = (a->cols + kBlockK - 1) / kBlockK;
     const int kb_grp = a->max_group_cols > 0 ? a->max_group_cols / kBlockK : kb_all;  // widest group
-    int cs = static_cast<int>(option("split"));
-    int64_t mode = option("split_mode");
-    if (mode < 0 || mode > 3) return fail(SHFLBW_BAD_PARAMS, "split_mode must be 0..3");
-    const int64_t units = static_cast<int64_t>(n_tiles) * groups;
-    if (mode == 0) {
-        mode = 3;
-        if (cs <= 0 && b.kind == 0 && kb_grp >= 8) {
-            const bool fit4 = units * 4 <= num_sms(), fit2 = units * 2 <= num_sms();
-            if (fit4 && kb_grp >= 24) {
-                mode = 1;
-                cs = 4;
-            } else if (fit4 && V >= 64) {
-                mode = 2;
-            } else if (fit2) {
-                mode = 1;
-                cs = 2;
+    const int64_t mode_opt = option("split_mode");
+    if (mode_opt < 0 || mode_opt > 3) return fail(SHFLBW_BAD_PARAMS, "split_mode must be 0..3");
+    struct Split {
+        int cs;
+        int64_t mode;
+        bool hybrid, vsplit;
+    };
+    auto choose_split = [&](int64_t units) {
+        Split r{static_cast<int>(option("split")), mode_opt, false, false};
+        if (r.mode == 0) {
+            r.mode = 3;
+            if (r.cs <= 0 && b.kind == 0 && kb_grp >= 8) {
+                const bool fit4 = units * 4 <= num_sms(), fit2 = units * 2 <= num_sms();
+                if (fit4 && kb_grp >= 24) {
+                    r.mode = 1;
+                    r.cs = 4;
+                } else if (fit4 && V >= 64) {
+                    r.mode = 2;
+                } else if (fit2) {
+                    r.mode = 1;
+                    r.cs = 2;
+                }
             }
         }
-    }
-    bool hybrid = mode == 2 && V >= 32 && (cs == 4 || (cs <= 0 && units * 4 <= num_sms()));
-    const bool vsplit = mode != 1 && !hybrid;
-    if (hybrid) {
-        cs = 4;
-    } else if (cs <= 0) {
-        cs = 1;
-        if (vsplit) {
-            while (cs < 4 && V / (cs * 2) >= 16 && units * cs * 2 <= num_sms()) cs *= 2;
-        } else {
-            while (cs < 4 && units * cs * 2 <= num_sms() && kb_all / (cs * 2) >= min_kb) cs *= 2;
+        r.hybrid = r.mode == 2 && V >= 32 && (r.cs == 4 || (r.cs <= 0 && units * 4 <= num_sms()));
+        r.vsplit = r.mode != 1 && !r.hybrid;
+        if (r.hybrid) {
+            r.cs = 4;
+        } else if (r.cs <= 0) {
+            r.cs = 1;
+            if (r.vsplit) {
+                while (r.cs < 4 && V / (r.cs * 2) >= 16 && units * r.cs * 2 <= num_sms()) r.cs *= 2;
+            } else {
+                while (r.cs < 4 && units * r.cs * 2 <= num_sms() && kb_all / (r.cs * 2) >= min_kb) r.cs *= 2;
+            }
         }
+        return r;
+    };
+    // Output columns per unit ("tile_n"): 128, or 64 -- half-width units
+    // (SpMM only): twice the units, each gathering one 64-column activation
+    // slab.  Auto: 64 when the 128-column plan (units x cluster split) would
+    // still use at most half the SMs -- measured better there (V = 128 north
+    // star 5.03 -> 4.54 us, attention projection 2.62 -> 2.56, FFN2 N=128
+    // 3.99 -> 3.94) and worse where it only trades a K split for deeper
+    // single-CTA units (north star V = 64: 4.2 -> 4.6 us).
+    int tile_n = 128;
+    {
+        const int64_t tn = option("tile_n");
+        if (tn != 0 && tn != 64 && tn != 128) return fail(SHFLBW_BAD_PARAMS, "tile_n must be 0, 64 or 128");
+        const int64_t units128 = (n_gemm + kBlockN - 1) / kBlockN * groups;
+        const bool can = b.kind == 0 && option("cp_async_slabs") == 0 && option("persistent") <= 0 && n_gemm > 64;
+        if (tn == 64 && can) tile_n = 64;
+        else if (tn == 0 && can && units128 * choose_split(units128).cs * 2 <= num_sms()) tile_n = 64;
     }
+    const int n_tiles = static_cast<int>((n_gemm + tile_n - 1) / tile_n);
+    const int64_t units = static_cast<int64_t>(n_tiles) * groups;
+    const Split sp = choose_split(units);
+    int cs = sp.cs;
+    bool hybrid = sp.hybrid;
+    const bool vsplit = sp.vsplit;
     bool conv_ksplit = false;
     if (b.kind != 0) {
         // conv: K split only (the gathers' positions depend on the CTA's
@@ -284,9 +293,10 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     {
         const int64_t r = option("raster");
         if (r < 0 || r > 2) return fail(SHFLBW_BAD_PARAMS, "raster must be 0, 1 or 2");
-        // auto: column-tile-major once the weights are large and B is shared
-        // by many groups (large FFN: B streams once, weights stay in L2)
-        prm.raster = r ? static_cast<int>(r) : (groups >= 16 && n_tiles >= 2 ? 2 : 1);
+        // auto: column-tile-major (measured: large FFN 474-484 -> 436-454 us,
+        // ResNet 3x3 @28 11.8 -> 11.1 us, FFN1 N=4096 9.37 -> 9.16 us; ncu
+        // DRAM reads of the large FFN 552 -> 185 MB per launch)
+        prm.raster = r ? static_cast<int>(r) : 2;
     }
     prm.cps = b.kind == 0 ? static_cast<int>(option("cp_async_slabs")) : 0;
     if (prm.cps < 0 || prm.cps > 2) return fail(SHFLBW_BAD_PARAMS, "cp_async_slabs must be 0, 1 or 2");

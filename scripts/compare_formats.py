@@ -66,9 +66,9 @@ def main():
             cpg = int(round(alpha * K))
             set_bytes = 2 * M * cpg + 2 * K * N + 2 * M * N
             n = 1 if set_bytes > bench.L2_BYTES else min(64, max(2, math.ceil(1.25 * bench.L2_BYTES / set_bytes)))
-            Bs = [bench.uniform_bf16(torch, (K, N), 200 + s, dev) for s in range(n)]
+            Bs = [bench.uniform16(torch, (K, N), 200 + s, dev) for s in range(n)]
             Cs = [torch.empty((M, N), dtype=torch.bfloat16, device=dev) for _ in range(n)]
-            Ws = [bench.uniform_bf16(torch, (M, K), 100 + s, dev) for s in range(n)]
+            Ws = [bench.uniform16(torch, (M, K), 100 + s, dev) for s in range(n)]
             res = {"shape": name, "M": M, "N": N, "K": K, "V": V, "sparsity": 1 - alpha}
             for fmt, mk in (("shflbw", lambda: bench.synth_mask(M, K, V, cpg, 1234)),
                             ("vw", lambda: vw_mask(M, K, V, cpg, 1234))):

@@ -15,7 +15,7 @@ import paper_2203_05016_b200 as sb  # noqa: E402
 dev = torch.device("cuda", 0)
 for name, M, K, V in (("ns", 2048, 2048, 64), ("lf", 16384, 4096, 64), ("ffn1", 2048, 512, 64)):
     mask = torch.from_numpy(bench.synth_mask(M, K, V, K // 4, 1234)).to(dev)
-    W = bench.uniform_bf16(torch, (M, K), 100, dev)
+    W = bench.uniform16(torch, (M, K), 100, dev)
     for _ in range(3):
         a = sb.compress_shflbw(W, mask, V)
         del a
@@ -37,7 +37,7 @@ for name, M, K, V in (("ns", 2048, 2048, 64), ("lf", 16384, 4096, 64), ("ffn1", 
 
 # allocation check: repeated compress + free must not grow device usage
 mask = torch.from_numpy(bench.synth_mask(2048, 2048, 64, 512, 1234)).to(dev)
-W = bench.uniform_bf16(torch, (2048, 2048), 100, dev)
+W = bench.uniform16(torch, (2048, 2048), 100, dev)
 for _ in range(5):
     del_a = sb.compress_shflbw(W, mask, 64)
     del del_a

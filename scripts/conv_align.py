@@ -20,9 +20,9 @@ for name, H, W, pad in (("aligned pad0", 58, 56, 0), ("misaligned pad1", 56, 54,
     crs = C * 3
     mask = torch.from_numpy(bench.synth_mask(Kf, crs, V, crs // 4, 1234)).to(dev)
     n = 8
-    ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform_bf16(torch, (Kf, crs), 100 + s, dev), mask, V), 1)
+    ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform16(torch, (Kf, crs), 100 + s, dev), mask, V), 1)
           for s in range(n)]
-    xs = [bench.uniform_bf16(torch, (C, H, W, Nb), 300 + s, dev) for s in range(n)]
+    xs = [bench.uniform16(torch, (C, H, W, Nb), 300 + s, dev) for s in range(n)]
     P, Q = H + 2 * pad - 3 + 1, W + 2 * pad - 1 + 1
     outs = [torch.empty((Kf, P, Q, Nb), dtype=torch.bfloat16, device=dev) for _ in range(n)]
     lib = sb.shflbw._lib()

@@ -52,9 +52,9 @@ def main():
         mask = torch.from_numpy(bench.synth_mask(Kf, crs, V, crs // 4, 1234)).to(dev)
         geo = sb.ConvGeometry(R, R, 1, pad)
         n = 6
-        ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform_bf16(torch, (Kf, crs), 100 + s, dev), mask, V), geo)
+        ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform16(torch, (Kf, crs), 100 + s, dev), mask, V), geo)
               for s in range(n)]
-        xs = [bench.uniform_bf16(torch, (C, H, H, Nb), 300 + s, dev) for s in range(n)]
+        xs = [bench.uniform16(torch, (C, H, H, Nb), 300 + s, dev) for s in range(n)]
         outs = [torch.empty((Kf, H, H, Nb), dtype=torch.bfloat16, device=dev) for _ in range(n)]
 
         def conv_step(i):
@@ -67,8 +67,8 @@ def main():
         N = H * H * Nb
         K = kp
         smask = torch.ones((Kf, K), dtype=torch.uint8, device=dev)
-        mats = [sb.compress_shflbw(bench.uniform_bf16(torch, (Kf, K), 100 + s, dev), smask, V) for s in range(n)]
-        Bs = [bench.uniform_bf16(torch, (K, N), 200 + s, dev) for s in range(n)]
+        mats = [sb.compress_shflbw(bench.uniform16(torch, (Kf, K), 100 + s, dev), smask, V) for s in range(n)]
+        Bs = [bench.uniform16(torch, (K, N), 200 + s, dev) for s in range(n)]
         Cs = [torch.empty((Kf, N), dtype=torch.bfloat16, device=dev) for _ in range(n)]
 
         def spmm_step(i):

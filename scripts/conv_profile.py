@@ -16,9 +16,9 @@ crs = C * R * R
 mask = torch.from_numpy(bench.synth_mask(Kf, crs, V, crs // 4, 1234)).to(dev)
 n = 12
 geo = sb.ConvGeometry(R, R, 1, pad)
-ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform_bf16(torch, (Kf, crs), 100 + s, dev), mask, V), geo)
+ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform16(torch, (Kf, crs), 100 + s, dev), mask, V), geo)
       for s in range(n)]
-xs = [bench.uniform_bf16(torch, (C, H, H, Nb), 300 + s, dev) for s in range(n)]
+xs = [bench.uniform16(torch, (C, H, H, Nb), 300 + s, dev) for s in range(n)]
 outs = [torch.empty((Kf, H, H, Nb), dtype=torch.bfloat16, device=dev) for _ in range(n)]
 lib = sb.shflbw._lib()
 for it in range(3 * n):

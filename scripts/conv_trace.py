@@ -31,10 +31,10 @@ dev = torch.device("cuda", 0)
 crs = C * R * R
 mask = torch.from_numpy(bench.synth_mask(Kf, crs, V, int(round(alpha * crs)), 1234)).to(dev)
 nset = max(1, args.chain)
-ws = [sb.compress_shflbw(bench.uniform_bf16(torch, (Kf, crs), 100 + i, dev), mask, V) for i in range(nset)]
+ws = [sb.compress_shflbw(bench.uniform16(torch, (Kf, crs), 100 + i, dev), mask, V) for i in range(nset)]
 if args.prepared:
     ws = [sb.conv_prepare(w, R) for w in ws]
-xs = [bench.uniform_bf16(torch, (C, H, H, Nb), 300 + i, dev) for i in range(nset)]
+xs = [bench.uniform16(torch, (C, H, H, Nb), 300 + i, dev) for i in range(nset)]
 P = H + 2 * pad - R + 1
 outs = [torch.empty((Kf, P, P, Nb), dtype=torch.bfloat16, device=dev) for _ in range(nset)]
 for kv in [x for x in args.opts.split(",") if x]:

@@ -21,9 +21,9 @@ for (C, H, Kf) in ((64, 56, 64), (128, 28, 128), (256, 14, 256)):
     mask = torch.from_numpy(bench.synth_mask(Kf, crs, V, crs // 4, 1234)).to(dev)
     geo = sb.ConvGeometry(R, R, 1, pad)
     for n in (1, 12):
-        ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform_bf16(torch, (Kf, crs), 100 + s, dev), mask, V), geo)
+        ws = [sb.conv_prepare(sb.compress_shflbw(bench.uniform16(torch, (Kf, crs), 100 + s, dev), mask, V), geo)
               for s in range(n)]
-        xs = [bench.uniform_bf16(torch, (C, H, H, Nb), 300 + s, dev) for s in range(n)]
+        xs = [bench.uniform16(torch, (C, H, H, Nb), 300 + s, dev) for s in range(n)]
         outs = [torch.empty((Kf, H, H, Nb), dtype=torch.bfloat16, device=dev) for _ in range(n)]
 
         def step(i):
@@ -36,8 +36,8 @@ for name, M, N, K in (("FFN2", 512, 4096, 2048), ("FFN1", 2048, 4096, 512)):
     V = 64
     mask = torch.from_numpy(bench.synth_mask(M, K, V, K // 4, 1234)).to(dev)
     for n in (1, 12):
-        mats = [sb.compress_shflbw(bench.uniform_bf16(torch, (M, K), 100 + s, dev), mask, V) for s in range(n)]
-        Bs = [bench.uniform_bf16(torch, (K, N), 200 + s, dev) for s in range(n)]
+        mats = [sb.compress_shflbw(bench.uniform16(torch, (M, K), 100 + s, dev), mask, V) for s in range(n)]
+        Bs = [bench.uniform16(torch, (K, N), 200 + s, dev) for s in range(n)]
         Cs = [torch.empty((M, N), dtype=torch.bfloat16, device=dev) for _ in range(n)]
         us = sweep.time_steps(lambda i: sb.spmm_execute(mats[i % n], Bs[i % n], out=Cs[i % n]), 300) * 1e3
         print(json.dumps({"spmm": name, "sets": n, "us": round(us, 2)}), flush=True)

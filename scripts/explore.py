@@ -41,8 +41,8 @@ def main():
     kpad = (cpg + 63) // 64 * 64
     set_bytes = 2 * M * kpad + 4 * (M // V) * kpad + 2 * K * N + 2 * M * N
     nsets = 1 if set_bytes > bench.L2_BYTES else min(64, max(2, math.ceil(1.25 * bench.L2_BYTES / set_bytes)))
-    mats = [sb.compress_shflbw(bench.uniform_bf16(torch, (M, K), 100 + s, dev), mask, V) for s in range(nsets)]
-    Bs = [bench.uniform_bf16(torch, (K, N), 200 + s, dev) for s in range(nsets)]
+    mats = [sb.compress_shflbw(bench.uniform16(torch, (M, K), 100 + s, dev), mask, V) for s in range(nsets)]
+    Bs = [bench.uniform16(torch, (K, N), 200 + s, dev) for s in range(nsets)]
     Cs = [torch.empty((M, N), dtype=torch.bfloat16, device=dev) for _ in range(nsets)]
 
     def step(i):

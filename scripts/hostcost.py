@@ -11,8 +11,8 @@ from paper_2203_05016_b200 import _lib as L
 dev = torch.device("cuda", 0)
 M, N, K, V = 2048, 128, 2048, 64
 mask = torch.from_numpy(bench.synth_mask(M, K, V, 512, 1)).to(dev)
-a = sb.compress_shflbw(bench.uniform_bf16(torch, (M, K), 1, dev), mask, V)
-B = bench.uniform_bf16(torch, (K, N), 2, dev)
+a = sb.compress_shflbw(bench.uniform16(torch, (M, K), 1, dev), mask, V)
+B = bench.uniform16(torch, (K, N), 2, dev)
 Cc = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
 lib = L.load()
 s = torch.cuda.current_stream().cuda_stream

@@ -70,13 +70,15 @@ def spmm_row(name, M, N, K, V, alpha, steps, dev):
     # (ours: packed weights + indices + B + C; dense: W + B + C)
     n = max(nsets_for(2 * M * kpad + 4 * (M // V) * kpad + 2 * K * N + 2 * M * N),
             nsets_for(2 * M * K + 2 * K * N + 2 * M * N))
+    if os.environ.get("SBW_WARM"):  # development: one L2-resident operand set
+        n = 1
     mask = torch.from_numpy(bench.synth_mask(M, K, V, cpg, 1234)).to(dev)
     mats, Wd, Bs, Cs, Cd = [], [], [], [], []
     for s in range(n):
-        W = bench.uniform_bf16(torch, (M, K), 100 + s, dev)
+        W = bench.uniform16(torch, (M, K), 100 + s, dev)
         mats.append(sb.compress_shflbw(W, mask, V))
         Wd.append((W * mask).contiguous())
-        Bs.append(bench.uniform_bf16(torch, (K, N), 200 + s, dev))
+        Bs.append(bench.uniform16(torch, (K, N), 200 + s, dev))
         Cs.append(torch.empty((M, N), dtype=torch.bfloat16, device=dev))
         Cd.append(torch.empty((M, N), dtype=torch.bfloat16, device=dev))
     t_ours = time_steps(lambda i: sb.spmm_execute(mats[i % n], Bs[i % n], out=Cs[i % n]), steps)
@@ -100,10 +102,10 @@ def conv_row(name, C, H, Kf, R, pad, Nb, V, alpha, steps, dev):
     P = H + 2 * pad - R + 1
     mats, xs, outs, Wc, xc = [], [], [], [], []
     for s in range(n):
-        W = bench.uniform_bf16(torch, (Kf, crs), 100 + s, dev)
+        W = bench.uniform16(torch, (Kf, crs), 100 + s, dev)
         mats.append(sb.conv_prepare(sb.compress_shflbw(W, mask, V), geo))  # one-time conv weight order
         Wc.append((W * mask).reshape(Kf, C, R, R).contiguous())
-        x = bench.uniform_bf16(torch, (C, H, H, Nb), 300 + s, dev)
+        x = bench.uniform16(torch, (C, H, H, Nb), 300 + s, dev)
         xs.append(x)
         xc.append(x.permute(3, 0, 1, 2).contiguous(memory_format=torch.channels_last))  # NCHW, channels-last
         outs.append(torch.empty((Kf, P, P, Nb), dtype=torch.bfloat16, device=dev))

@@ -29,8 +29,10 @@ dev = torch.device("cuda", 0)
 cpg = int(round(alpha * K))
 mask = torch.from_numpy(bench.synth_mask(M, K, V, cpg, 1234)).to(dev)
 nset = max(1, args.chain)
-mats = [sb.compress_shflbw(bench.uniform_bf16(torch, (M, K), 100 + i, dev), mask, V) for i in range(nset)]
-Bs = [bench.uniform_bf16(torch, (K, N), 200 + i, dev) for i in range(nset)]
+if os.environ.get("SBW_WARM"):  # development: one L2-resident operand set, reused by every launch
+    nset = 1
+mats = [sb.compress_shflbw(bench.uniform16(torch, (M, K), 100 + i, dev), mask, V) for i in range(nset)]
+Bs = [bench.uniform16(torch, (K, N), 200 + i, dev) for i in range(nset)]
 Cs = [torch.empty((M, N), dtype=torch.bfloat16, device=dev) for i in range(nset)]
 a, B, C = mats[0], Bs[0], Cs[0]
 for kv in [x for x in args.opts.split(",") if x]:
@@ -39,13 +41,14 @@ for kv in [x for x in args.opts.split(",") if x]:
 tr = torch.zeros(1 << 20, dtype=torch.int64, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 for it in range(3):
-    flush.fill_(it)  # cold L2
+    if not os.environ.get("SBW_WARM"):
+        flush.fill_(it)  # cold L2
     torch.cuda.synchronize()
     tr.zero_()
     sb.set_option("trace", tr.data_ptr())
     if args.chain:
         for i in range(args.chain):
-            sb.spmm_execute(mats[i], Bs[i], out=Cs[i])
+            sb.spmm_execute(mats[i % nset], Bs[i % nset], out=Cs[i % nset])
     else:
         sb.spmm_execute(a, B, out=C)
     torch.cuda.synchronize()

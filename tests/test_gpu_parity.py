@@ -501,6 +501,10 @@ def test_persistent_kernel_bitwise(sb, oracle, M, N, K, V, alpha, split):
     a, p = compress_both(sb, oracle, W, mask, V)
     Bd = dev(B, torch.bfloat16)
     sb.set_option("split", split)
+    # no K split (its partial sums round differently) and full-width units on
+    # the one-CTA-per-unit side, so both kernels run the same MMA sequence
+    sb.set_option("split_mode", 3)
+    sb.set_option("tile_n", 128)
     outs = {}
     for mode in (-1, 1, 2, 0):  # one CTA per unit, persistent x1 / x2 per SM, auto
         sb.set_option("persistent", mode)
@@ -513,6 +517,8 @@ def test_persistent_kernel_bitwise(sb, oracle, M, N, K, V, alpha, split):
     sb.set_option("no_bulk_out", 0)
     sb.set_option("persistent", 0)
     sb.set_option("split", 0)
+    sb.set_option("split_mode", 0)
+    sb.set_option("tile_n", 0)
     assert oracle.rel_frobenius(outs[1][0], oracle.spmm(p, B)) <= TOL
     for mode in (1, 2, 0, "nb"):
         assert np.array_equal(outs[mode][0], outs[-1][0]) and np.array_equal(outs[mode][1], outs[-1][1]), mode
@@ -1002,11 +1008,12 @@ def test_half_width_units_bitwise(sb, oracle, N, split, mode):
     assert oracle.rel_frobenius(outs[64][0], oracle.spmm(p, B)) <= TOL
 
 
-def test_auto_half_width_north_star(sb, oracle):
-    """The auto plan picks half-width units for the north-star grid (32
-    groups x 1 column tile) and stays within tolerance of the oracle."""
-    mask, W, B = synthetic(oracle, 2048, 2048, 128, 64, 0.25)
-    a, p = compress_both(sb, oracle, W, mask, 64)
+def test_auto_half_width_north_star_v128(sb, oracle):
+    """The auto plan picks half-width units for the V = 128 north-star grid
+    (16 groups x 1 column tile: the 128-column plan would use 64 CTAs) and
+    stays within tolerance of the oracle."""
+    mask, W, B = synthetic(oracle, 2048, 2048, 128, 128, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, 128)
     got = sb.spmm_execute(a, dev(B, torch.bfloat16)).cpu().numpy()
     assert "tile_n=64" in sb.last_plan(), sb.last_plan()
     assert oracle.rel_frobenius(got, oracle.spmm(p, B)) <= TOL
