@@ -291,6 +291,18 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.ksplit = hybrid ? 2 : ((cs > 1 && (!vsplit || conv_ksplit)) ? 1 : 0);
     prm.tile_n = tile_n;
     {
+        // SpMM gather issue ("gather_issue"): 1 = one elected lane per warp
+        // issues the warp's gathers back to back, 2 = each issuing lane its
+        // own (a hardware-serialised per-lane loop); auto = elected for
+        // unicast gathers (measured: north star V = 32 4.03 -> 3.64 us, GNMT
+        // 50 % 4.58 -> 4.47) and per-lane for multicast ones (north star
+        // 3.55 vs 3.80 us, attention projection 2.19 vs 2.37)
+        const int64_t gi = option("gather_issue");
+        if (gi < 0 || gi > 2) return fail(SHFLBW_BAD_PARAMS, "gather_issue must be 0, 1 or 2");
+        const bool multicast = (hybrid || (vsplit && b.kind == 0)) && cs > 1;
+        prm.issue1 = b.kind == 0 && (gi == 1 || (gi == 0 && !multicast)) ? 1 : 0;
+    }
+    {
         const int64_t r = option("raster");
         if (r < 0 || r > 2) return fail(SHFLBW_BAD_PARAMS, "raster must be 0, 1 or 2");
         // auto: column-tile-major (measured: large FFN 474-484 -> 436-454 us,

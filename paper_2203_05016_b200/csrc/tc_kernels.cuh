@@ -93,6 +93,7 @@ struct TcParams {
     int persistent;  // 1: k_spmm_persist (units loop inside the CTA)
     int per_sm;      // persistent: resident CTAs per SM
     int gw;          // gather warps per CTA (4, 8)
+    int issue1;      // 1: SpMM gathers issued by one elected lane per warp (option "gather_issue")
     int raster;      // persistent unit order: 1 group-major, 2 column-tile-major
     int tile_n;      // output columns per unit: 128, or 64 (k_spmm_tc, SpMM only: half-width units)
     int n_extra;     // further output destinations (fused all-gather), staged-store path only
@@ -616,36 +617,49 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
         __syncwarp();
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
+        // The whole warp walks the ring (warp-uniform state, so descriptors and
+        // counters stay in uniform registers) and one elected lane issues: a
+        // lane-0-only loop made every tcgen05.mma a serialised
+        // ELECT / R2UR.BROADCAST sequence (~0.25 us per K block).  The
+        // descriptors are built once and advanced by adds (the 14-bit
+        // address field never carries: shared memory < 256 KB).
         // activation operand: MN-major, MN blocks of p.bw elements, swizzle = block row bytes
-        const uint32_t a_row = static_cast<uint32_t>(p.bw) * 2;
+        const uint32_t a_row = KIND == 0 ? 128u : static_cast<uint32_t>(p.bw) * 2;
         const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
-        if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            for (int kb = 0; kb < nkb; ++kb) {
-                mbar_wait(&full[s], ph);
-                tc_fence_after();
+        const uint64_t adesc0 = umma_smem_desc(smem_u32(smem), kBlockK * a_row, 8 * a_row, a_layout);
+        const uint64_t bdesc0 = umma_smem_desc(smem_u32(smem) + kABytes, WL::kSlabBytes, WL::kSBO, WL::kLayout);
+        const uint64_t a_ks = (16 * a_row) >> 4;                           // per K=16 slice
+        constexpr uint64_t b_ks = (16 * WL::kRowBytes) >> 4;
+        constexpr uint64_t st_step = kStageBytes >> 4;
+        int s = 0;
+        uint32_t ph = 0;
+        uint64_t st_off = 0;
+        for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            if (lane == 0) {
                 if (kb == 0) trace_event(p.trace, 3);
                 if (kb < 8) trace_event(p.trace, 8 + kb);
-                const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
-                const uint32_t w_addr = a_addr + kABytes;
+            }
+            const uint64_t ad = adesc0 + st_off, bd = bdesc0 + st_off;
+            if (elect_one_sync()) {
 #pragma unroll
-                for (int ks = 0; ks < kBlockK / 16; ++ks) {
-                    const uint64_t adesc = umma_smem_desc(a_addr + ks * 16 * a_row, kBlockK * a_row, 8 * a_row,
-                                                          a_layout);
-                    const uint64_t bdesc = umma_smem_desc(w_addr + ks * 16 * WL::kRowBytes,
-                                                          WL::kSlabBytes, WL::kSBO, WL::kLayout);
-                    umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
-                }
+                for (int ks = 0; ks < kBlockK / 16; ++ks)
+                    umma_f16(tmem_d, ad + ks * a_ks, bd + ks * b_ks, kIdesc, (kb | ks) != 0);
                 // the last `stages` slots are never refilled: no release
                 // signal for them, so nothing targets a peer's shared memory
                 // once that peer has consumed its own stages (no cluster
                 // barrier needed before exit)
                 if constexpr (!mcast) umma_commit(&empty[s]);
                 else if (kb + stages < nkb) umma_commit_mc(&empty[s], cmask);
-                if (++s == stages) s = 0, ph ^= 1;
             }
-            trace_event(p.trace, 4);
+            __syncwarp();
+            if (lane == 0 && kb < 3) trace_event(p.trace, 29 + kb);  // MMAs of K block kb issued
+            if (++s == stages) s = 0, ph ^= 1, st_off = 0;
+            else st_off += st_step;
+        }
+        if (lane == 0) trace_event(p.trace, 4);
+        if (elect_one_sync()) {
             if (nkb > 0) umma_commit(accum);
             else mbar_arrive(accum);
         }
@@ -701,7 +715,36 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
             if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
             unsigned char* a_st = smem + s * kStageBytes;
             const int32_t* mk = meta_s + win * kBlockK;
-            if (t_issue) {
+            if (KIND == 0 && p.issue1) {
+                // SpMM, option "gather_issue" 1: this warp's gathers for the
+                // stage issued back to back by one elected lane, all index
+                // loads first (the per-lane issue compiles to a serialised
+                // ELECT / R2UR.BROADCAST loop per gather)
+                if (elect_one_sync()) {
+                    int4 ci[8];
+                    const uint32_t mrow = meta_u32 + static_cast<uint32_t>(win * kBlockK * 4);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int rg = gw * kRGW + j % kRGW;
+                        if (j < per_warp)
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(ci[j].x), "=r"(ci[j].y), "=r"(ci[j].z), "=r"(ci[j].w)
+                                         : "r"(mrow + static_cast<uint32_t>(rg * 16)));
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int jg = gw * per_warp + j;
+                        if (j >= per_warp || (mcast && (jg % VSF) != vr)) continue;
+                        const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
+                        void* dst = a_st + bb * blk_bytes + rg * (4 * 64 * 2);
+                        if constexpr (!mcast)
+                            tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                        else
+                            tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
+                                           ci[j].w);
+                    }
+                }
+            } else if (t_issue) {
                 int4 ci;  // explicit ld.shared (a generic load would take the slower generic path)
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
@@ -966,41 +1009,45 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         }
         __syncwarp();
     } else if (warp == 1) {
-        // ---------------- MMA issuer ----------------
+        // ---------------- MMA issuer (converged warp, elected lane: see k_spmm_tc) ----------------
         const uint32_t a_row = KIND == 0 ? 128u : static_cast<uint32_t>(p.bw) * 2;
         const uint32_t a_layout = a_row == 128 ? 2u : (a_row == 64 ? 4u : 6u);
-        if (lane == 0) {
-            int s = 0, i = 0;
-            uint32_t ph = 0;
-            for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
-                const int nkb = group_nkb(c.gl);
-                const int b = i & 1;
-                mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
+        const uint64_t adesc0 = umma_smem_desc(smem_u32(smem), kBlockK * a_row, 8 * a_row, a_layout);
+        const uint64_t bdesc0 = umma_smem_desc(smem_u32(smem) + kABytes, WL::kSlabBytes, WL::kSBO, WL::kLayout);
+        const uint64_t a_ks = (16 * a_row) >> 4;
+        constexpr uint64_t b_ks = (16 * WL::kRowBytes) >> 4;
+        constexpr uint64_t st_step = kStageBytes >> 4;
+        int s = 0, i = 0;
+        uint32_t ph = 0;
+        uint64_t st_off = 0;
+        for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
+            const int nkb = group_nkb(c.gl);
+            const int b = i & 1;
+            mbar_wait(&acc_empty[b], ((i >> 1) & 1) ^ 1);
+            tc_fence_after();
+            if (lane == 0 && i < 8) trace_event(p.trace, 8 + i);  // MMA: accumulator free for unit i
+            const uint32_t tmem_d = tmem_base + b * kAccCols;
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&full[s], ph);
                 tc_fence_after();
-                if (i < 8) trace_event(p.trace, 8 + i);  // MMA: accumulator free for unit i
-                const uint32_t tmem_d = tmem_base + b * kAccCols;
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&full[s], ph);
-                    tc_fence_after();
-                    const uint32_t a_addr = smem_u32(smem + s * kStageBytes);
-                    const uint32_t w_addr = a_addr + kABytes;
+                const uint64_t ad = adesc0 + st_off, bd = bdesc0 + st_off;
+                if (elect_one_sync()) {
 #pragma unroll
-                    for (int ks = 0; ks < kBlockK / 16; ++ks) {
-                        const uint64_t adesc = umma_smem_desc(a_addr + ks * 16 * a_row, kBlockK * a_row, 8 * a_row,
-                                                              a_layout);
-                        const uint64_t bdesc = umma_smem_desc(w_addr + ks * 16 * WL::kRowBytes, WL::kSlabBytes,
-                                                              WL::kSBO, WL::kLayout);
-                        umma_f16(tmem_d, adesc, bdesc, kIdesc, (kb | ks) != 0);
-                    }
+                    for (int ks = 0; ks < kBlockK / 16; ++ks)
+                        umma_f16(tmem_d, ad + ks * a_ks, bd + ks * b_ks, kIdesc, (kb | ks) != 0);
                     if constexpr (!mcast) umma_commit(&empty[s]);
                     else umma_commit_mc(&empty[s], cmask);
-                    if (++s == stages) s = 0, ph ^= 1;
                 }
+                __syncwarp();
+                if (++s == stages) s = 0, ph ^= 1, st_off = 0;
+                else st_off += st_step;
+            }
+            if (elect_one_sync()) {
                 if (nkb > 0) umma_commit(&acc_full[b]);
                 else mbar_arrive(&acc_full[b]);
             }
+            __syncwarp();
         }
-        __syncwarp();
     } else if (warp < 2 + GW) {
         // ---------------- activation gathers ----------------
         constexpr int kGT = 32 * GW;
@@ -1075,7 +1122,34 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                     named_bar<kGT>(2);
                 }
                 if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
-                if (t_issue) {
+                if (KIND == 0 && p.issue1) {
+                    // SpMM: one elected lane per warp issues the warp's
+                    // gathers back to back, index loads first (k_spmm_tc)
+                    if (elect_one_sync()) {
+                        int4 ci[8];
+                        const uint32_t mrow = smem_u32(mbuf) + static_cast<uint32_t>(win * kBlockK * 4);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int rg = gw * kRGW + j % kRGW;
+                            if (j < per_warp)
+                                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(ci[j].x), "=r"(ci[j].y), "=r"(ci[j].z), "=r"(ci[j].w)
+                                             : "r"(mrow + static_cast<uint32_t>(rg * 16)));
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int jg = gw * per_warp + j;
+                            if (j >= per_warp || (mcast && (jg % CS) != static_cast<int>(rank))) continue;
+                            const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
+                            void* dst = smem + s * kStageBytes + bb * blk_bytes + rg * (4 * 64 * 2);
+                            if constexpr (!mcast)
+                                tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                            else
+                                tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
+                                               ci[j].w);
+                        }
+                    }
+                } else if (t_issue) {
                     int4 ci;
                     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                                  : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)

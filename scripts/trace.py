@@ -59,7 +59,7 @@ t0 = t[:, 0].min()
 rel = (t - t0) / 1000.0
 names = ["entry", "setup", "dep_wait", "first_full", "last_mma", "accum", "epi_done", "exit"]
 names += [f"full[{k}]" for k in range(8)] + [f"issue[{k}]" for k in range(8)] + ["partial_ok", "recv_ok",
-          "sum_done", "tile_bar", "stores_issued"]
+          "sum_done", "tile_bar", "stores_issued", "mma_done[0]", "mma_done[1]", "mma_done[2]"]
 print(f"{args.workload} K={K} {args.opts} chain={args.chain}: {len(t)} CTAs, span {rel[:, 7].max():.2f} us, "
       f"dep_wait(min)->exit(max) {rel[:, 7].max() - rel[t[:, 2] > 0, 2].min():.2f} us")
 for e, nm in enumerate(names):
