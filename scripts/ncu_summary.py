@@ -20,7 +20,12 @@ KEYS = {
     "dram__bytes_write.sum": "dram_write",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_util_pct",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_util_elapsed_pct",
-    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    # GB100's raw page names the DRAM throughput gpu__dram_throughput (the
+    # dram__throughput alias of older chips is absent)
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct_legacy",
+    "lts__t_sector_hit_rate.pct": "l2_hit_rate_pct",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
     "lts__throughput.avg.pct_of_peak_sustained_elapsed": "l2_throughput_pct",
     "lts__t_bytes.sum": "l2_bytes",
     "launch__grid_size": "grid",
@@ -34,7 +39,10 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1
 
 
 def summarise(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # a raw page exported on the GPU box (ncu -i rep --page raw --csv)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
@@ -55,6 +63,13 @@ def summarise(rep):
                     x *= UNIT.get(u, 1)  # -> us
                 d[name] = x
         d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
+        if d.get("duration"):
+            # achieved DRAM GB/s under ncu (cold, serialised launch) and its
+            # fraction of the measured copy bandwidth (MEASURED_PEAKS.json)
+            d["dram_gbs"] = d["dram_bytes_per_launch"] / (d["duration"] * 1e-6) / 1e9
+            pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+            if os.path.exists(pk):
+                d["dram_frac_of_measured_peak"] = d["dram_gbs"] / json.load(open(pk))["hbm_gbs"]
         res.append(d)
     return res
 
@@ -63,8 +78,9 @@ def main():
     tag = sys.argv[1]
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     allp = json.load(open(path)) if os.path.exists(path) else {}
-    lines = [f"# ncu summary ({tag})", "", "| workload | kernel | us (ncu, cold) | DRAM MB | tensor pipe % | L2 % | DRAM % | grid | cluster |",
-             "|---|---|---|---|---|---|---|---|---|"]
+    lines = [f"# ncu summary ({tag})", "", "| workload | kernel | us (ncu, cold) | DRAM MB | DRAM GB/s (frac of measured) | "
+             "tensor pipe % | L2 % | L2 hit % | DRAM % | grid | cluster |",
+             "|---|---|---|---|---|---|---|---|---|---|---|"]
     for arg in sys.argv[2:]:
         wl, rep = arg.split("=", 1)
         res = summarise(rep)
@@ -74,8 +90,10 @@ def main():
         d["source"] = f"ncu --set full --clock-control none, {os.path.basename(rep)} ({tag})"
         allp[wl] = d
         lines.append(f"| {wl} | {d['kernel'][:60]} | {d.get('duration', 0):.2f} | {d['dram_bytes_per_launch'] / 1e6:.2f} | "
+                     f"{d.get('dram_gbs', 0):.0f} ({d.get('dram_frac_of_measured_peak', 0):.3f}) | "
                      f"{d.get('tensor_pipe_util_pct', 0):.2f} | {d.get('l2_throughput_pct', 0):.1f} | "
-                     f"{d.get('dram_throughput_pct', 0):.1f} | {int(d.get('grid', 0))} | {int(d.get('cluster', 0))} |")
+                     f"{d.get('l2_hit_rate_pct', 0):.1f} | {d.get('dram_throughput_pct', 0):.1f} | "
+                     f"{int(d.get('grid', 0))} | {int(d.get('cluster', 0))} |")
     json.dump(allp, open(path, "w"), indent=1)
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
