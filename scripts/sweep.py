@@ -82,6 +82,7 @@ def spmm_row(name, M, N, K, V, alpha, steps, dev):
         Cs.append(torch.empty((M, N), dtype=torch.bfloat16, device=dev))
         Cd.append(torch.empty((M, N), dtype=torch.bfloat16, device=dev))
     t_ours = time_steps(lambda i: sb.spmm_execute(mats[i % n], Bs[i % n], out=Cs[i % n]), steps)
+    plan = sb.last_plan()
     t_dense = time_steps(lambda i: torch.mm(Wd[i % n], Bs[i % n], out=Cd[i % n]), steps)
     err = (Cs[0].float() - Cd[0].float()).norm() / Cd[0].float().norm()
     flops = 2.0 * M * N * K
@@ -90,7 +91,7 @@ def spmm_row(name, M, N, K, V, alpha, steps, dev):
             "dense_us": t_dense * 1e3, "tflops_dense_equiv": flops / (t_ours * 1e-3) / 1e12,
             "dense_tflops": flops / (t_dense * 1e-3) / 1e12, "speedup": t_dense / t_ours,
             "hbm_gbs": q / (t_ours * 1e-3) / 1e9, "useful_tflops": flops * alpha / (t_ours * 1e-3) / 1e12,
-            "rel_err_vs_dense_bf16": float(err), "sets": n}
+            "rel_err_vs_dense_bf16": float(err), "sets": n, "plan": plan}
 
 
 def conv_row(name, C, H, Kf, R, pad, Nb, V, alpha, steps, dev):
@@ -117,6 +118,7 @@ def conv_row(name, C, H, Kf, R, pad, Nb, V, alpha, steps, dev):
                                   1, torch.cuda.current_stream().cuda_stream)
         assert st == 0
     t_ours = time_steps(step_ours, steps)
+    plan = sb.last_plan()
     Wcl = [w.contiguous(memory_format=torch.channels_last) for w in Wc]
     t_dense = time_steps(lambda i: torch.nn.functional.conv2d(xc[i % n], Wcl[i % n], padding=pad), steps)
     ref = torch.nn.functional.conv2d(xc[0], Wcl[0], padding=pad).float().permute(1, 2, 3, 0)
@@ -125,7 +127,7 @@ def conv_row(name, C, H, Kf, R, pad, Nb, V, alpha, steps, dev):
     return {"name": name, "C": C, "H": H, "Kf": Kf, "R": R, "Nb": Nb, "V": V, "sparsity": 1 - alpha,
             "us": t_ours * 1e3, "dense_us": t_dense * 1e3, "tflops_dense_equiv": flops / (t_ours * 1e-3) / 1e12,
             "dense_tflops": flops / (t_dense * 1e-3) / 1e12, "speedup": t_dense / t_ours,
-            "rel_err_vs_cudnn_bf16": float(err), "sets": n}
+            "rel_err_vs_cudnn_bf16": float(err), "sets": n, "plan": plan}
 
 
 def main():
@@ -146,12 +148,12 @@ def main():
             continue
         rows.append(conv_row(*cfg, args.steps, dev))
         print(json.dumps(rows[-1]), flush=True)
-    lines = ["| config | Shfl-BW us | dense us (cuBLAS/cuDNN) | dense-eq TFLOP/s | speed-up | rel err vs dense |",
-             "|---|---|---|---|---|---|"]
+    lines = ["| config | Shfl-BW us | dense us (cuBLAS/cuDNN) | dense-eq TFLOP/s | speed-up | rel err vs dense | plan |",
+             "|---|---|---|---|---|---|---|"]
     for r in rows:
         e = r.get("rel_err_vs_dense_bf16", r.get("rel_err_vs_cudnn_bf16"))
         lines.append(f"| {r['name']} | {r['us']:.2f} | {r['dense_us']:.2f} | {r['tflops_dense_equiv']:.0f} | "
-                     f"{r['speedup']:.2f}x | {e:.1e} |")
+                     f"{r['speedup']:.2f}x | {e:.1e} | {r.get('plan', '')} |")
     with open(args.out + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(args.out + ".json", "w") as f:
