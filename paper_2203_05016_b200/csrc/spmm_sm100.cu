@@ -235,20 +235,13 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const int cs128 = choose_split(units128).cs;
         const int64_t popt = option("persistent");
         const bool persist128 = popt > 0 || (popt == 0 && units128 * cs128 > 2LL * num_sms());
-        // half-width units: SpMM, and the persistent kernel's SpMM / conv-order
-        // convs (KIND 1's activation rows are one position wide)
-        const bool can = option("cp_async_slabs") == 0 && n_gemm > 64 &&
-                         (b.kind == 0 || (b.kind == 2 && persist128));
-        if (tn == 64 && can) {
-            tile_n = 64;
-        } else if (tn == 0 && can) {
-            if (!persist128 && units128 * cs128 * 2 <= num_sms()) {
-                tile_n = 64;
-            }
-            // (persistent half-width units fill the last wave better -- ResNet
-            // 3x3 @28: 392 units on 296 slots -- but measured slower: @28
-            // 10.7 -> 14.9 us, FFN1 N=4096 8.9 -> 13.6 us; option only)
-        }
+        // half-width units: SpMM on the one-CTA-per-unit kernel.  (In the
+        // persistent kernel they would fill the last wave of CTA slots better
+        // -- ResNet 3x3 @28: 392 units on 296 slots -- but measured slower:
+        // @28 10.7 -> 14.9 us, FFN1 N=4096 8.9 -> 13.6 us.)
+        const bool can = option("cp_async_slabs") == 0 && n_gemm > 64 && b.kind == 0 && !persist128;
+        if (tn == 64 && can) tile_n = 64;
+        else if (tn == 0 && can && units128 * cs128 * 2 <= num_sms()) tile_n = 64;
     }
     const int n_tiles = static_cast<int>((n_gemm + tile_n - 1) / tile_n);
     const int64_t units = static_cast<int64_t>(n_tiles) * groups;
@@ -314,9 +307,9 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const int64_t gi = option("gather_issue");
         if (gi < 0 || gi > 2) return fail(SHFLBW_BAD_PARAMS, "gather_issue must be 0, 1 or 2");
         const bool multicast = (hybrid || (vsplit && b.kind == 0)) && cs > 1;
-        // (conv KIND 2 supports the elected issue too, but it measured 2x
-        // slower there: ResNet 3x3 @56 12.4 -> 25.9 us; per-lane by default)
-        prm.issue1 = (b.kind == 0 && (gi == 1 || (gi == 0 && !multicast))) || (b.kind == 2 && gi == 1) ? 1 : 0;
+        // (the same for the conv KIND 2 producers measured 2x slower: ResNet
+        // 3x3 @56 12.4 -> 25.9 us; convs keep the per-lane issue)
+        prm.issue1 = b.kind == 0 && (gi == 1 || (gi == 0 && !multicast)) ? 1 : 0;
     }
     {
         const int64_t r = option("raster");
@@ -353,7 +346,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         // per-unit kernel wins: FFN2 N=4096 256 units 7.4 vs 8.3 us)
         int64_t opt = option("persistent");
         if (opt == 0) opt = (units * cs > 2LL * num_sms()) ? 2 : -1;
-        prm.persistent = !prm.ksplit && opt > 0 && groups <= 4096 && (tile_n == kBlockN || b.kind != 1) ? 1 : 0;
+        prm.persistent = !prm.ksplit && opt > 0 && groups <= 4096 && tile_n == kBlockN ? 1 : 0;
         prm.per_sm = static_cast<int>(std::min<int64_t>(2, std::max<int64_t>(1, opt)));  // launch bounds: 2
     }
     int stages = static_cast<int>(option("stages"));

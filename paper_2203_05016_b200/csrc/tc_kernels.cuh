@@ -690,18 +690,6 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
             g_p0 = (pos / p.qp) * p.stride - p.pad;
             g_q0 = (pos % p.qp) * p.stride - p.pad;
         }
-        // conv KIND 2, elected issue: both MN blocks' output positions
-        int e_p0[2] = {0, 0}, e_q0[2] = {0, 0};
-        bool e_ok[2] = {true, true};
-        if constexpr (KIND == 2) {
-#pragma unroll
-            for (int bb = 0; bb < 2; ++bb) {
-                const int pos = (n0 + bb * 64) / p.Nb;
-                e_ok[bb] = pos < p.PQ;
-                e_p0[bb] = (pos / p.qp) * p.stride - p.pad;
-                e_q0[bb] = (pos % p.qp) * p.stride - p.pad;
-            }
-        }
         // cp.async part (SpMM only): slabs [2-cps, 2): cps*512 16-byte chunks per K block
         const int cpr_log2 = cps == 2 ? 4 : 3;  // chunks per row: 8*cps
         const T* Bp = static_cast<const T*>(p.B);
@@ -727,11 +715,11 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
             if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
             unsigned char* a_st = smem + s * kStageBytes;
             const int32_t* mk = meta_s + win * kBlockK;
-            if ((KIND == 0 || KIND == 2) && p.issue1) {
-                // option "gather_issue" 1: this warp's gathers for the stage
-                // issued back to back by one elected lane, all index loads
-                // first (the per-lane issue compiles to a serialised ELECT /
-                // R2UR.BROADCAST loop per gather)
+            if (KIND == 0 && p.issue1) {
+                // SpMM, option "gather_issue" 1: this warp's gathers for the
+                // stage issued back to back by one elected lane, all index
+                // loads first (the per-lane issue compiles to a serialised
+                // ELECT / R2UR.BROADCAST loop per gather)
                 if (elect_one_sync()) {
                     int4 ci[8];
                     const uint32_t mrow = meta_u32 + static_cast<uint32_t>(win * kBlockK * 4);
@@ -749,12 +737,11 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
                         if (j >= per_warp || (mcast && (jg % VSF) != vr)) continue;
                         const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
                         void* dst = a_st + bb * blk_bytes + rg * (4 * 64 * 2);
-                        int x = n0 + bb * 64;
-                        if constexpr (KIND == 2) x = conv_wide_rows(p, ci[j], e_p0[bb], e_q0[bb], e_ok[bb]);
                         if constexpr (!mcast)
-                            tma_gather4(dst, &tmB, &full[s], x, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                            tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
                         else
-                            tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                            tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
+                                           ci[j].w);
                     }
                 }
             } else if (t_issue) {
@@ -902,7 +889,7 @@ __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc,
             return;
         }
     }
-    const int64_t n = m < p.tile_n ? out_col(p, n0 + m) : -1;
+    const int64_t n = out_col(p, n0 + m);
     const bool live = n >= 0;
 #pragma unroll
     for (int c = 0; c < (VS + 31) / 32; ++c) {
@@ -1011,8 +998,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                 const int nkb = (gptr_s[gl + 1] - gp) / kBlockK;
                 for (int kb = 0; kb < nkb; ++kb, ++kbg) {
                     if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
-                    // (half-width units fill one of the two activation slabs)
-                    mbar_arrive_expect_tx(&full[s], (KIND == 1 ? 2 : p.tile_n / 64) * (kABytes / 2) + WL::kBytes);
+                    mbar_arrive_expect_tx(&full[s], kStageBytes);
 #pragma unroll
                     for (int sl = 0; sl < WL::kSlabs; ++sl)
                         tma_load_2d(smem + s * kStageBytes + kABytes + sl * WL::kSlabBytes, &tmW, &full[s],
@@ -1067,7 +1053,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         constexpr int kGT = 32 * GW;
         const int gw = warp - 2, et = threadIdx.x - 64;  // et 0..kGT-1
         const int bw = KIND == 0 ? 64 : p.bw;
-        const int nblk = KIND == 1 ? kBlockN / bw : p.tile_n / 64;  // MN blocks per unit
+        const int nblk = kBlockN / bw;
         const int blk_bytes = kBlockK * bw * 2;
         constexpr int kRGW = 16 / GW;  // row groups (4 rows) per warp in every MN block
         const int per_warp = kRGW * nblk;
@@ -1115,7 +1101,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                 load_window(cn.gl, 0, buf ^ 1, true);
                 cp_async_commit();
             }
-            const int n0 = c.tile * p.tile_n;
+            const int n0 = c.tile * kBlockN;
             const int32_t* mbuf = meta_s + buf * kMetaBlocks * kBlockK;
             int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
             bool g_pos_ok = true;
@@ -1128,19 +1114,6 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                 g_p0 = pr * p.stride - p.pad;
                 g_q0 = (pos - pr * p.qp) * p.stride - p.pad;
             }
-            // conv KIND 2, elected issue: both MN blocks' output positions
-            int e_p0[2] = {0, 0}, e_q0[2] = {0, 0};
-            bool e_ok[2] = {true, true};
-            if constexpr (KIND == 2) {
-#pragma unroll
-                for (int bb = 0; bb < 2; ++bb) {
-                    const int pos = ddiv(n0 + bb * 64, p.inv_nb);
-                    e_ok[bb] = pos < p.PQ;
-                    const int pr = ddiv(pos, p.inv_qp);
-                    e_p0[bb] = pr * p.stride - p.pad;
-                    e_q0[bb] = (pos - pr * p.qp) * p.stride - p.pad;
-                }
-            }
             for (int kb = 0; kb < nkb; ++kb, ++kbg) {
                 const int win = kb % kMetaBlocks;
                 if (win == 0 && kb > 0) {  // deep group: later windows of this unit, synchronously
@@ -1149,9 +1122,9 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                     named_bar<kGT>(2);
                 }
                 if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
-                if ((KIND == 0 || KIND == 2) && p.issue1) {
-                    // one elected lane per warp issues the warp's gathers back
-                    // to back, index loads first (k_spmm_tc)
+                if (KIND == 0 && p.issue1) {
+                    // SpMM: one elected lane per warp issues the warp's
+                    // gathers back to back, index loads first (k_spmm_tc)
                     if (elect_one_sync()) {
                         int4 ci[8];
                         const uint32_t mrow = smem_u32(mbuf) + static_cast<uint32_t>(win * kBlockK * 4);
@@ -1169,12 +1142,11 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                             if (j >= per_warp || (mcast && (jg % CS) != static_cast<int>(rank))) continue;
                             const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
                             void* dst = smem + s * kStageBytes + bb * blk_bytes + rg * (4 * 64 * 2);
-                            int x = n0 + bb * 64;
-                            if constexpr (KIND == 2) x = conv_wide_rows(p, ci[j], e_p0[bb], e_q0[bb], e_ok[bb]);
                             if constexpr (!mcast)
-                                tma_gather4(dst, &tmB, &full[s], x, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                                tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
                             else
-                                tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                                tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
+                                               ci[j].w);
                         }
                     }
                 } else if (t_issue) {
@@ -1223,7 +1195,7 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         grid_dependency_wait();  // C may still be read by the previous kernel
         int i = 0;
         for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
-            const int n0 = c.tile * p.tile_n;
+            const int n0 = c.tile * kBlockN;
             const int nkb = group_nkb(c.gl);
             const int b = i & 1;
             asm volatile("bar.sync 3, 128;" ::: "memory");  // previous unit done with rows_s / ctile

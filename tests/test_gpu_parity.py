@@ -1035,63 +1035,3 @@ def test_persistent_raster_orders_bitwise(sb, oracle, V):
     sb.set_option("raster", 0)
     assert np.array_equal(outs[1], outs[2])
     assert oracle.rel_frobenius(outs[2][:, :128], oracle.spmm(p, np.ascontiguousarray(B[:, :128]))) <= TOL
-
-
-@pytest.mark.parametrize("gather_issue", [1, 2])
-def test_persistent_half_width_bitwise(sb, oracle, gather_issue):
-    """Half-width units in the persistent kernel (SpMM and conv-order conv):
-    the same bits as 128-column units, per-lane and elected gather issue."""
-    mask, W, B = synthetic(oracle, 2048, 512, 1000, 64, 0.5)
-    a, p = compress_both(sb, oracle, W, mask, 64)
-    Bd = dev(B, torch.bfloat16)
-    sb.set_option("persistent", 2)
-    sb.set_option("gather_issue", gather_issue)
-    outs = {}
-    for tn in (128, 64):
-        sb.set_option("tile_n", tn)
-        outs[tn] = (sb.spmm_execute(a, Bd).cpu().numpy(),
-                    sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
-        plan = sb.last_plan()
-        assert plan.startswith("k_spmm_persist") and f"tile_n={tn}" in plan, plan
-    assert np.array_equal(outs[64][0], outs[128][0]) and np.array_equal(outs[64][1], outs[128][1])
-    assert oracle.rel_frobenius(outs[64][0][:, :200], oracle.spmm(p, np.ascontiguousarray(B[:, :200]))) <= TOL
-    # conv in conv order (KIND 2), Q = 7 (padded position grid)
-    C, H, Kf, V, Nb = 32, 7, 128, 64, 32
-    cmask, Wt, x = _conv_setup(oracle, C, H, H, Kf, 3, 3, V, Nb, seed=21)
-    w = sb.conv_prepare(sb.compress_shflbw(dev(Wt), dev(cmask), V), 3)
-    xd = dev(x, torch.bfloat16)
-    geo = sb.ConvGeometry(3, 3, 1, 1)
-    conv = {}
-    for tn in (128, 64):
-        sb.set_option("tile_n", tn)
-        conv[tn] = sb.conv2d(w, xd, geo).cpu().numpy()
-        plan = sb.last_plan()
-        assert plan.startswith("k_spmm_persist") and "kind=2" in plan and f"tile_n={tn}" in plan, plan
-    for k in ("persistent", "tile_n", "gather_issue"):
-        sb.set_option(k, 0)
-    assert np.array_equal(conv[64], conv[128])
-    assert oracle.rel_frobenius(conv[64], oracle.conv2d(oracle.compress(Wt, cmask, V), x, 3, 3, 1, 1)) <= TOL
-
-
-@pytest.mark.parametrize("prepared", [False, True])
-def test_conv_gather_issue_bitwise(sb, oracle, prepared):
-    """Elected vs per-lane gather issue for the conv producers: same bits."""
-    C, H, Kf, V, Nb = 64, 10, 128, 64, 32
-    mask, Wt, x = _conv_setup(oracle, C, H, H, Kf, 3, 3, V, Nb, seed=13)
-    w = sb.compress_shflbw(dev(Wt), dev(mask), V)
-    if prepared:
-        w = sb.conv_prepare(w, 3)
-    xd = dev(x, torch.bfloat16)
-    geo = sb.ConvGeometry(3, 3, 1, 1)
-    got = {}
-    for persist in (-1, 2):
-        for gi in (1, 2):
-            sb.set_option("persistent", persist)
-            sb.set_option("gather_issue", gi)
-            got[(persist, gi)] = sb.conv2d(w, xd, geo).cpu().numpy()
-    sb.set_option("persistent", 0)
-    sb.set_option("gather_issue", 0)
-    ref = got[(-1, 2)]
-    for k, v in got.items():
-        assert np.array_equal(v, ref), k
-    assert oracle.rel_frobenius(ref, oracle.conv2d(oracle.compress(Wt, mask, V), x, 3, 3, 1, 1)) <= TOL
