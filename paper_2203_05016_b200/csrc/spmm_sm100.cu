@@ -232,9 +232,11 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const int64_t tn = option("tile_n");
         if (tn != 0 && tn != 64 && tn != 128) return fail(SHFLBW_BAD_PARAMS, "tile_n must be 0, 64 or 128");
         const int64_t units128 = (n_gemm + kBlockN - 1) / kBlockN * groups;
-        const int cs128 = choose_split(units128).cs;
+        const Split sp128 = choose_split(units128);
+        const int cs128 = sp128.cs;
         const int64_t popt = option("persistent");
-        const bool persist128 = popt > 0 || (popt == 0 && units128 * cs128 > 2LL * num_sms());
+        const bool ksplit128 = sp128.hybrid || (cs128 > 1 && !sp128.vsplit);  // K splits never run persistent
+        const bool persist128 = !ksplit128 && (popt > 0 || (popt == 0 && units128 * cs128 > 2LL * num_sms()));
         // half-width units: SpMM on the one-CTA-per-unit kernel.  (In the
         // persistent kernel they would fill the last wave of CTA slots better
         // -- ResNet 3x3 @28: 392 units on 296 slots -- but measured slower:
