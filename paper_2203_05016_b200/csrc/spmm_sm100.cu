@@ -358,7 +358,8 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         // as many stages as its share of shared memory holds (>= 2), with the
         // staged output tile dropped when it would cost a stage.
         const int64_t budget = 232448 / prm.per_sm - 1024;
-        const int64_t tile = static_cast<int64_t>(vs) * kBlockN * (c.dtype == SHFLBW_F32 ? 4 : 2);
+        const int out_esz = c.dtype == SHFLBW_F32 ? 4 : 2;
+        const int64_t tile = static_cast<int64_t>(tc::persist_tile_rows(vs, out_esz)) * kBlockN * out_esz;
         const int64_t fixed = 1024 + 2 * kMetaBlocks * kBlockK * 4 + 4 * 128 + 4 * (groups + 2) + 512;
         const int64_t stage = kABytes + static_cast<int64_t>(kBlockK) * vs * 2;
         const int64_t with_tile = (budget - fixed - tile) / stage, without = (budget - fixed) / stage;

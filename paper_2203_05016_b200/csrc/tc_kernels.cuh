@@ -873,19 +873,33 @@ struct UnitCursor {
 };
 
 
+// Rows of the persistent kernel's staged output tile: 16-bit outputs are
+// staged and stored 32 rows at a time (an 8 KB tile instead of VS x 128 x 2:
+// the freed shared memory buys a fourth pipeline stage at 2 CTAs per SM).
+__host__ __device__ constexpr int persist_tile_rows(int vs, int out_esz) {
+    return (out_esz == 2 && vs % 32 == 0) ? 32 : vs;
+}
+
 template <class OT, int VS>
 __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc, int nkb, int m, int q, int lane,
                                               int n0, const int32_t* rows_s, unsigned char* ctile,
                                               uint64_t* acc_empty) {
     if constexpr (sizeof(OT) == 2 && VS % 32 == 0) {
         if (p.bulk_out) {
-            stage_tile_stmatrix<OT, VS>(t_acc, nkb, q, lane, ctile);
-            // accumulator drained: the MMA warp may start the next unit in it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty);
-            asm volatile("bar.sync 3, 128;" ::: "memory");
-            store_tile_rows<OT, VS, false, true>(p, ctile, rows_s, q, lane, n0);
+            // 32 output rows at a time through an 8 KB staged tile
+#pragma unroll
+            for (int c0 = 0; c0 < VS; c0 += 32) {
+                if (c0 > 0) asm volatile("bar.sync 3, 128;" ::: "memory");  // previous rows stored
+                stage_tile_stmatrix<OT, 32>(t_acc + c0, nkb, q, lane, ctile);
+                if (c0 + 32 >= VS) {
+                    // accumulator drained: the MMA warp may start the next unit in it
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(acc_empty);
+                }
+                asm volatile("bar.sync 3, 128;" ::: "memory");
+                store_tile_rows<OT, 32, false, true>(p, ctile, rows_s + c0, q, lane, n0);
+            }
             return;
         }
     }
@@ -943,7 +957,8 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
     const bool tmaj = p.raster == 2;  // column-tile-major unit order
     const int out_esz = p.c_dtype == SHFLBW_F32 ? 4 : 2;
     unsigned char* ctile = smem + stages * kStageBytes;  // [VS][128] out (staged stores only)
-    int32_t* meta_s = reinterpret_cast<int32_t*>(ctile + (p.bulk_out ? VS * kBlockN * out_esz : 0));  // [2][kMetaBlocks][64]
+    int32_t* meta_s = reinterpret_cast<int32_t*>(  // [2][kMetaBlocks][64]
+        ctile + (p.bulk_out ? persist_tile_rows(VS, out_esz) * kBlockN * out_esz : 0));
     int32_t* rows_s = meta_s + 2 * kMetaBlocks * kBlockK;                              // VS
     int32_t* gptr_s = rows_s + (VS < 4 ? 4 : VS);                                      // ngroups + 1
     uint64_t* full = reinterpret_cast<uint64_t*>(gptr_s + ((ngroups + 2) & ~1));
@@ -1285,7 +1300,9 @@ int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParam
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
     const size_t out_esz = prm.c_dtype == SHFLBW_F32 ? 4 : 2;
     const size_t smem = static_cast<size_t>(prm.stages) * kStage +
-                        (prm.bulk_out ? static_cast<size_t>(VS) * kBlockN * out_esz : 0) + 1024 +
+                        (prm.bulk_out ? static_cast<size_t>(persist_tile_rows(VS, static_cast<int>(out_esz))) *
+                                            kBlockN * out_esz
+                                      : 0) + 1024 +
                         2 * kMetaBlocks * kBlockK * 4 + (VS < 4 ? 4 : VS) * 4 + ((groups + 2) & ~1) * 4 +
                         (2 * prm.stages + 5) * 8 + 16;
     auto kern = k_spmm_persist<DT, VS, CS, KIND, GW>;
