@@ -84,6 +84,15 @@ typedef struct shflbw_cu_matrix {
  * bits 8..15 hold the filter width S it was prepared for */
 #define SHFLBW_CONV_ORDER 2
 #define SHFLBW_CONV_ORDER_S(reserved) (((reserved) >> 8) & 0xff)
+/* shflbw_cu_matrix.reserved bit: built by shflbw_cu_compress_async and not yet
+ * finalized -- total_cols / max_group_cols hold the allocation bounds
+ * (G * roundup(K, 64) / roundup(K, 64)); every kernel reads the exact group
+ * sizes from the device, so the matrix is usable as is */
+#define SHFLBW_SIZE_BOUND 4
+/* shflbw_cu_matrix.reserved bit: the buffers were allocated from the bound
+ * (shflbw_cu_compress_async); a later compress_async of the same shape into
+ * this matrix reuses them */
+#define SHFLBW_BOUND_ALLOC 8
 
 /* ---- library ---------------------------------------------------------- */
 const char* shflbw_cu_last_error(void);
@@ -142,6 +151,26 @@ int shflbw_cu_compress(const void* dense, int32_t dense_dtype, const uint8_t* ma
                        int32_t M, int32_t K, int32_t V, int32_t value_dtype,
                        shflbw_cu_matrix* out, uint32_t* fail_row,
                        shflbw_stream_t stream);
+
+/* The converter without a host synchronisation (graph-capturable, stream
+ * ordered like every kernel): *out is allocated from the bound
+ * G * roundup(K, 64) columns and built on `stream`; status [dev] int32[4]
+ * receives {status code, fail_row, total columns, widest group}.  A
+ * non-conformant mask, a mask byte > 1 or an (astronomically unlikely) row
+ * hash collision is reported there instead of being returned (the pipeline
+ * stays in bounds).  The matrix may be used by SpMM / conv calls enqueued
+ * after it; shflbw_cu_matrix_finalize (one synchronisation, e.g. outside a
+ * captured graph) returns the status code -- NONCONFORMANT_MASK with
+ * *fail_row, BAD_PARAMS, CUDA_ERROR -- and sets the exact total_cols /
+ * max_group_cols.  Results equal shflbw_cu_compress's.  If *out already holds
+ * a bound-allocated matrix of the same M, K, V and value dtype (from an
+ * earlier compress_async), its buffers are reused: a captured graph then
+ * converts into the same memory on every replay. */
+int shflbw_cu_compress_async(const void* dense, int32_t dense_dtype, const uint8_t* mask,
+                             int32_t M, int32_t K, int32_t V, int32_t value_dtype,
+                             shflbw_cu_matrix* out, int32_t* status, shflbw_stream_t stream);
+int shflbw_cu_matrix_finalize(shflbw_cu_matrix* m, const int32_t* status, uint32_t* fail_row,
+                              shflbw_stream_t stream);
 
 void shflbw_cu_matrix_free(shflbw_cu_matrix* m);
 

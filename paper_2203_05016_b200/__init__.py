@@ -10,15 +10,15 @@ from .shflbw import (BadGeometry, BadMagic, BadParams, ConvGeometry, CorruptPayl
                      ShapeMismatch, UnsupportedVersion, smx1_dump, smx1_dumps, smx1_load, smx1_loads,
                      PruneConfig, PruneResult, importance_scores, kept_score, kmeans_row_grouping,
                      prune_shflbw, prune_unstructured, prune_vectorwise,
-                     ShflBWMatrix, TileConfig, compress_shflbw, conv2d, conv_output_size, conv_prepare,
-                     decompress, fold_input_permutation, last_plan, launch_count, set_option, spmm_execute, spmm_groups, spmm_groups_peers,
+                     ShflBWMatrix, TileConfig, compress_shflbw, compress_shflbw_async, conv2d, conv_output_size, conv_prepare,
+                     decompress, finalize, fold_input_permutation, last_plan, launch_count, set_option, spmm_execute, spmm_groups, spmm_groups_peers,
                      unpermute_rows, upload, validate_pattern)
 
 __all__ = ["BadGeometry", "BadMagic", "BadParams", "ConvGeometry", "CorruptPayload", "Error", "NonConformantMask",
            "ShapeMismatch", "UnsupportedVersion", "smx1_dump", "smx1_dumps", "smx1_load", "smx1_loads",
            "PruneConfig", "PruneResult", "importance_scores", "kept_score", "kmeans_row_grouping",
            "prune_shflbw", "prune_unstructured", "prune_vectorwise",
-           "ShflBWMatrix", "TileConfig", "compress_shflbw", "conv2d", "conv_output_size", "conv_prepare",
-           "decompress",
+           "ShflBWMatrix", "TileConfig", "compress_shflbw", "compress_shflbw_async", "conv2d", "conv_output_size", "conv_prepare",
+           "decompress", "finalize",
            "fold_input_permutation", "last_plan", "launch_count", "set_option", "spmm_execute", "spmm_groups", "spmm_groups_peers",
            "unpermute_rows", "upload", "validate_pattern"]

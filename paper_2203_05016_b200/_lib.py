@@ -49,6 +49,9 @@ SIGNATURES = {
     "shflbw_cu_compress": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                      C.c_int32, C.POINTER(CuMatrix), C.POINTER(C.c_uint32), C.c_void_p]),
     "shflbw_cu_matrix_free": (None, [C.POINTER(CuMatrix)]),
+    "shflbw_cu_compress_async": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                           C.c_int32, C.POINTER(CuMatrix), C.c_void_p, C.c_void_p]),
+    "shflbw_cu_matrix_finalize": (C.c_int, [C.POINTER(CuMatrix), C.c_void_p, C.POINTER(C.c_uint32), C.c_void_p]),
     "shflbw_cu_matrix_upload": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(CuMatrix),
                                           C.c_void_p]),

@@ -164,6 +164,20 @@ int shflbw_cu_compress(const void* dense, int32_t dense_dtype, const uint8_t* ma
                          reinterpret_cast<cudaStream_t>(stream));
 }
 
+int shflbw_cu_compress_async(const void* dense, int32_t dense_dtype, const uint8_t* mask, int32_t M, int32_t K,
+                             int32_t V, int32_t value_dtype, shflbw_cu_matrix* out, int32_t* status,
+                             shflbw_stream_t stream) {
+    if (!out || !status) return fail(SHFLBW_BAD_PARAMS, "null output matrix or status");
+    return compress_async_impl(dense, dense_dtype, mask, M, K, V, value_dtype, out, status,
+                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+int shflbw_cu_matrix_finalize(shflbw_cu_matrix* m, const int32_t* status, uint32_t* fail_row,
+                              shflbw_stream_t stream) {
+    if (!m || !status) return fail(SHFLBW_BAD_PARAMS, "null matrix or status");
+    return finalize_impl(m, status, fail_row, reinterpret_cast<cudaStream_t>(stream));
+}
+
 void shflbw_cu_matrix_free(shflbw_cu_matrix* m) { free_matrix(m); }
 
 int shflbw_cu_matrix_upload(int32_t M, int32_t K, int32_t V, const uint32_t* row_indices,

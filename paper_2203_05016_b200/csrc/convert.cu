@@ -91,6 +91,62 @@ __global__ void k_pack_rows(const uint8_t* __restrict__ mask, int M, int K, int 
     }
 }
 
+// Same, 16 mask bytes per lane load (K % 16 == 0, 16-byte aligned mask): a
+// warp covers 512 columns per load; lane l's 16 bytes become bits
+// 15..0 of its pattern, four consecutive lanes' patterns one 64-bit word
+// (column 0 = MSB, as k_pack_rows).
+__global__ void k_pack_rows16(const uint8_t* __restrict__ mask, int M, int K, int W, uint64_t seed,
+                              uint64_t* __restrict__ words, int* __restrict__ popc, uint64_t* __restrict__ keys,
+                              uint32_t* __restrict__ vals, uint32_t* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (r >= M) return;
+    const uint4* row = reinterpret_cast<const uint4*>(mask + static_cast<int64_t>(r) * K);
+    const int nchunk = K / 16;
+    uint64_t h = 0;
+    int pc = 0;
+    bool bad = false;
+    for (int c0 = 0; c0 < nchunk; c0 += 32) {
+        const int c = c0 + lane;
+        uint32_t pat = 0;
+        if (c < nchunk) {
+            const uint4 q = row[c];
+            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t byte = (w4[i] >> (8 * b)) & 0xffu;
+                    bad |= byte > 1;
+                    pat |= (byte != 0 ? 1u : 0u) << (15 - (i * 4 + b));
+                }
+            }
+        }
+        const uint32_t p1 = __shfl_down_sync(0xffffffffu, pat, 1);
+        const uint32_t p2 = __shfl_down_sync(0xffffffffu, pat, 2);
+        const uint32_t p3 = __shfl_down_sync(0xffffffffu, pat, 3);
+        const int w = (c0 + lane) / 4;  // word of lanes 4q..4q+3
+        if ((lane & 3) == 0 && w < W) {
+            const uint64_t word = (static_cast<uint64_t>(pat) << 48) | (static_cast<uint64_t>(p1) << 32) |
+                                  (static_cast<uint64_t>(p2) << 16) | p3;
+            words[static_cast<int64_t>(r) * W + w] = word;
+            pc += __popcll(word);
+            h += word_hash(word, w, seed);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        h += __shfl_xor_sync(0xffffffffu, h, o);
+        pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags[0], 1u);
+    if (lane == 0) {
+        popc[r] = pc;
+        keys[r] = h;
+        vals[r] = static_cast<uint32_t>(r);
+    }
+}
+
 // Re-hash with another seed (collision retry): one warp per row.
 __global__ void k_hash_rows(const uint64_t* __restrict__ words, int M, int W, uint64_t seed,
                             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
@@ -129,9 +185,12 @@ __global__ void __launch_bounds__(1024) k_sort_small(uint64_t* __restrict__ keys
     __syncthreads();
     for (int kk = 2; kk <= P; kk <<= 1) {
         for (int j = kk >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
+            // pair t of the P / 2 compare-exchanges of this step: i = lower
+            // index (bit j clear), ixj = i + j -- no idle half of the threads
+            for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+                const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+                const int ixj = i | j;
+                {
                     const bool up = (i & kk) == 0;
                     const uint64_t ka = k[i], kb = k[ixj];
                     const uint32_t pa = pos[i], pb = pos[ixj];
@@ -141,9 +200,9 @@ __global__ void __launch_bounds__(1024) k_sort_small(uint64_t* __restrict__ keys
                         k[ixj] = ka;
                         pos[i] = pb;
                         pos[ixj] = pa;
-                        const uint32_t t = v[i];
+                        const uint32_t tv = v[i];
                         v[i] = v[ixj];
-                        v[ixj] = t;
+                        v[ixj] = tv;
                     }
                 }
             }
@@ -358,6 +417,9 @@ __global__ void k_assign(const uint32_t* __restrict__ srows, const int* __restri
     const int slot = rank[i] % V;
     const int lead_row = static_cast<int>(srows[i - slot]);
     const int g = gid_by_row[lead_row];
+    // a non-conformant mask has more than M / V leaders: the asynchronous
+    // converter runs on anyway (its status reports the failure), in bounds
+    if (g >= M / V) return;
     row_indices[static_cast<int64_t>(g) * V + slot] = static_cast<int32_t>(srows[i]);
     if (slot == 0) {
         const int n = popc[lead_row];
@@ -594,6 +656,19 @@ __global__ void k_convert_2d(const void* __restrict__ src, int sdt, int64_t ld_s
             store_from_f32(dst, ddt, r * ld_dst + c, load_as_f32(src, sdt, r * ld_src + c));
 }
 
+// asynchronous converter status: [0] status code, [1] fail_row, [2] total
+// columns (group_ptr[G]), [3] widest group (padded)
+__global__ void k_status(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ fail_row,
+                         const int32_t* __restrict__ total, const int* __restrict__ maxp,
+                         int32_t* __restrict__ status) {
+    const int code = flags[0] ? SHFLBW_BAD_PARAMS
+                              : (flags[1] ? SHFLBW_CUDA_ERROR : (flags[2] ? SHFLBW_NONCONFORMANT_MASK : SHFLBW_OK));
+    status[0] = code;
+    status[1] = code == SHFLBW_NONCONFORMANT_MASK ? static_cast<int32_t>(*fail_row) : 0;
+    status[2] = *total;
+    status[3] = *maxp;
+}
+
 // ---- host helpers ------------------------------------------------------------
 
 }  // namespace
@@ -708,6 +783,18 @@ int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_
 
 namespace {
 
+int launch_pack_rows(const uint8_t* mask, int M, int K, int W, uint64_t seed, uint64_t* words, int* popc,
+                     uint64_t* keys, uint32_t* vals, uint32_t* flags, cudaStream_t s) {
+    if (K > 0 && K % 16 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0) {
+        k_pack_rows16<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, W, seed, words, popc, keys, vals, flags);
+        SBW_LAUNCHED("k_pack_rows16");
+    } else {
+        k_pack_rows<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, W, seed, words, popc, keys, vals, flags);
+        SBW_LAUNCHED("k_pack_rows");
+    }
+    return SHFLBW_OK;
+}
+
 // Steps 1-4 shared by validate and compress.
 struct ClassPlan {
     DevBuf words, popc, keys, vals, keys2, vals2, rank, lead, fail_head, flags;
@@ -733,10 +820,9 @@ int plan_classes(const uint8_t* mask, int M, int K, int V, ClassPlan& p, uint32_
         const uint64_t seed = 0x5ca1ab1e00000000ULL + attempt;
         SBW_CUDA(cudaMemsetAsync(p.flags.p, 0, sizeof(uint32_t) * 4, s));
         if (attempt == 0) {
-            k_pack_rows<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, p.W, seed, p.words.as<uint64_t>(),
-                                                       p.popc.as<int>(), p.keys.as<uint64_t>(),
-                                                       p.vals.as<uint32_t>(), p.flags.as<uint32_t>());
-            SBW_LAUNCHED("k_pack_rows");
+            if (int st = launch_pack_rows(mask, M, K, p.W, seed, p.words.as<uint64_t>(), p.popc.as<int>(),
+                                          p.keys.as<uint64_t>(), p.vals.as<uint32_t>(), p.flags.as<uint32_t>(), s))
+                return st;
             if (K == 0) {  // no columns: every row is the empty support
                 SBW_CUDA(cudaMemsetAsync(p.popc.p, 0, sizeof(int) * M, s));
                 k_hash_rows<<<grid_for(M, 8), 256, 0, s>>>(p.words.as<uint64_t>(), M, p.W, seed,
@@ -930,6 +1016,143 @@ int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M
     // the matrix is complete on return (SpMM prologues read it before their
     // programmatic-launch wait, see the "pdl" option)
     SBW_CUDA(cudaStreamSynchronize(s));
+    return SHFLBW_OK;
+}
+
+// The converter without a host synchronisation (graph-capturable): the
+// output is allocated from the bound G * roundup(K, 64) columns, hash
+// collisions / bad mask bytes / non-conformance and the sizes are written to
+// status[4] on the device, and the rest of the pipeline runs regardless (in
+// bounds).  shflbw_cu_matrix_finalize reads the status back.
+int compress_async_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M, int K, int V,
+                        int value_dtype, shflbw_cu_matrix* out, int32_t* status, cudaStream_t s) {
+    if (int st = check_dtype16(value_dtype)) return st;
+    if (dense_dtype < SHFLBW_F32 || dense_dtype > SHFLBW_F16) return fail(SHFLBW_BAD_PARAMS, "dense dtype");
+    if (V <= 0 || M < 0 || K < 0 || M % V != 0) return fail(SHFLBW_BAD_PARAMS, "V must divide M");
+    const int G = M / V;
+    const int64_t kpad = (static_cast<int64_t>(K) + SHFLBW_K_TILE - 1) / SHFLBW_K_TILE * SHFLBW_K_TILE;
+    const int64_t bound = static_cast<int64_t>(G) * kpad;
+    if (bound > 0x7fffffffLL) return fail(SHFLBW_UNSUPPORTED, "compress_async: G * roundup(K, 64) exceeds 2^31");
+    // reuse a bound-sized matrix of the same shape (e.g. converting into the
+    // same buffers on every replay of a captured graph), else allocate one
+    const bool reuse = out->owns && out->row_indices && (out->reserved & SHFLBW_BOUND_ALLOC) && out->rows == M &&
+                       out->cols == K && out->v == V && out->dtype == value_dtype;
+    auto cleanup = [&](int st) {
+        if (st && !reuse) free_matrix(out);
+        return st;
+    };
+    if (!reuse) {
+        if (int st = alloc_meta(out, M, K, V, value_dtype, s)) return st;
+        if (int st = alloc_data(out, bound, s)) return cleanup(st);
+    }
+    out->total_cols = bound;
+    out->max_group_cols = static_cast<int32_t>(kpad);
+    out->reserved = SHFLBW_SIZE_BOUND | SHFLBW_BOUND_ALLOC;
+    DevBuf flags, fr, maxp;
+    SBW_CUDA(flags.alloc(sizeof(uint32_t) * 4, s));
+    SBW_CUDA(fr.alloc(sizeof(uint32_t), s));
+    SBW_CUDA(maxp.alloc(sizeof(int), s));
+    SBW_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(uint32_t) * 4, s));
+    SBW_CUDA(cudaMemsetAsync(fr.p, 0, sizeof(uint32_t), s));
+    SBW_CUDA(cudaMemsetAsync(maxp.p, 0, sizeof(int), s));
+    if (M == 0) {
+        SBW_CUDA(cudaMemsetAsync(out->group_ptr, 0, sizeof(int32_t), s));
+        k_status<<<1, 1, 0, s>>>(flags.as<uint32_t>(), fr.as<uint32_t>(), out->group_ptr, maxp.as<int>(), status);
+        SBW_LAUNCHED("k_status");
+        return SHFLBW_OK;
+    }
+    ClassPlan p;
+    p.W = K > 0 ? (K + 63) / 64 : 1;
+    const int64_t MW = static_cast<int64_t>(M) * p.W;
+    SBW_CUDA(p.words.alloc(sizeof(uint64_t) * MW, s));
+    SBW_CUDA(p.popc.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.keys.alloc(sizeof(uint64_t) * M, s));
+    SBW_CUDA(p.vals.alloc(sizeof(uint32_t) * M, s));
+    SBW_CUDA(p.keys2.alloc(sizeof(uint64_t) * M, s));
+    SBW_CUDA(p.vals2.alloc(sizeof(uint32_t) * M, s));
+    SBW_CUDA(p.rank.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.lead.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.fail_head.alloc(sizeof(int) * M, s));
+    if (K == 0) SBW_CUDA(cudaMemsetAsync(p.words.p, 0, sizeof(uint64_t) * MW, s));
+    const uint64_t seed = 0x5ca1ab1e00000000ULL;
+    if (int st = launch_pack_rows(mask, M, K, p.W, seed, p.words.as<uint64_t>(), p.popc.as<int>(),
+                                  p.keys.as<uint64_t>(), p.vals.as<uint32_t>(), flags.as<uint32_t>(), s))
+        return cleanup(st);
+    if (K == 0) {
+        SBW_CUDA(cudaMemsetAsync(p.popc.p, 0, sizeof(int) * M, s));
+        k_hash_rows<<<grid_for(M, 8), 256, 0, s>>>(p.words.as<uint64_t>(), M, p.W, seed, p.keys.as<uint64_t>(),
+                                                   p.vals.as<uint32_t>());
+        SBW_LAUNCHED("k_hash_rows");
+    }
+    int st = radix_sort_pairs(p.keys.as<uint64_t>(), p.vals.as<uint32_t>(), p.keys2.as<uint64_t>(),
+                              p.vals2.as<uint32_t>(), M, s);
+    if (st) return cleanup(st);
+    k_runs<<<grid_for(M, 256), 256, 0, s>>>(p.keys.as<uint64_t>(), p.vals.as<uint32_t>(), p.words.as<uint64_t>(), M,
+                                            p.W, V, p.rank.as<int>(), p.lead.as<int>(), p.fail_head.as<int>(),
+                                            flags.as<uint32_t>());
+    SBW_LAUNCHED("k_runs");
+    k_fail_argmin<<<1, 1024, 0, s>>>(p.fail_head.as<int>(), p.vals.as<uint32_t>(), p.words.as<uint64_t>(), M, p.W,
+                                     fr.as<uint32_t>());
+    SBW_LAUNCHED("k_fail_argmin");
+    DevBuf gid, leader, padded;
+    SBW_CUDA(gid.alloc(sizeof(int) * M, s));
+    SBW_CUDA(leader.alloc(sizeof(int) * G, s));
+    SBW_CUDA(padded.alloc(sizeof(int) * G, s));
+    // every slot defined even when a non-conformant mask leaves some unassigned
+    SBW_CUDA(cudaMemsetAsync(out->row_indices, 0, sizeof(int32_t) * M, s));
+    SBW_CUDA(cudaMemsetAsync(out->group_ncols, 0, sizeof(int32_t) * G, s));
+    SBW_CUDA(cudaMemsetAsync(leader.p, 0, sizeof(int) * G, s));
+    SBW_CUDA(cudaMemsetAsync(padded.p, 0, sizeof(int) * G, s));
+    if ((st = scan_exclusive(p.lead.as<int>(), gid.as<int>(), M, nullptr, s))) return cleanup(st);
+    k_assign<<<grid_for(M, 256), 256, 0, s>>>(p.vals.as<uint32_t>(), p.rank.as<int>(), gid.as<int>(), p.popc.as<int>(),
+                                              M, V, SHFLBW_K_TILE, out->row_indices, leader.as<int32_t>(),
+                                              out->group_ncols, padded.as<int>());
+    SBW_LAUNCHED("k_assign");
+    if ((st = scan_exclusive(padded.as<int>(), out->group_ptr, G, out->group_ptr + G, s))) return cleanup(st);
+    k_max<<<1, 256, 0, s>>>(padded.as<int>(), G, maxp.as<int>());
+    SBW_LAUNCHED("k_max");
+    if (G > 0) {
+        k_pack_cols<<<G, 128, 0, s>>>(p.words.as<uint64_t>(), p.W, leader.as<int32_t>(), out->group_ptr,
+                                      out->group_ncols, out->col_idx);
+        SBW_LAUNCHED("k_pack_cols");
+        const int jc = V <= 1024 ? 64 : 8;
+        const size_t smem = static_cast<size_t>(jc) * V * dtype_bytes(value_dtype);
+        const dim3 grid(static_cast<unsigned>((kpad + jc - 1) / jc), G);
+        if (grid.x > 0) {
+            cudaError_t ce = cudaSuccess;
+            by_dtype(value_dtype, [&]<int DT>() {
+                if (smem > 48 * 1024)
+                    ce = cudaFuncSetAttribute(k_pack_values<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem));
+                k_pack_values<DT><<<grid, 256, smem, s>>>(dense, dense_dtype, K, V, jc, out->row_indices,
+                                                          out->group_ptr, out->group_ncols, out->col_idx,
+                                                          out->values);
+            });
+            if (ce != cudaSuccess) return cleanup(cuda_fail(ce, "cudaFuncSetAttribute"));
+            SBW_LAUNCHED("k_pack_values");
+        }
+    }
+    k_status<<<1, 1, 0, s>>>(flags.as<uint32_t>(), fr.as<uint32_t>(), out->group_ptr + G, maxp.as<int>(), status);
+    SBW_LAUNCHED("k_status");
+    return SHFLBW_OK;
+}
+
+int finalize_impl(shflbw_cu_matrix* m, const int32_t* status, uint32_t* fail_row, cudaStream_t s) {
+    int32_t h[4] = {0, 0, 0, 0};
+    SBW_CUDA(cudaMemcpyAsync(h, status, sizeof(h), cudaMemcpyDeviceToHost, s));
+    SBW_CUDA(cudaStreamSynchronize(s));
+    if (fail_row) *fail_row = static_cast<uint32_t>(h[1]);
+    switch (h[0]) {
+        case SHFLBW_OK: break;
+        case SHFLBW_BAD_PARAMS: return fail(SHFLBW_BAD_PARAMS, "SparsityMask: entries must be 0 or 1");
+        case SHFLBW_NONCONFORMANT_MASK:
+            return fail(SHFLBW_NONCONFORMANT_MASK,
+                        "compress_shflbw: support class size is not a multiple of V (row " + std::to_string(h[1]) + ")");
+        default: return fail(SHFLBW_CUDA_ERROR, "compress_async: row-hash collision (retry with shflbw_cu_compress)");
+    }
+    m->total_cols = h[2];
+    m->max_group_cols = h[3];
+    m->reserved &= ~SHFLBW_SIZE_BOUND;
     return SHFLBW_OK;
 }
 

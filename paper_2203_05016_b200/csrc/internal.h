@@ -14,6 +14,9 @@ int validate_impl(const uint8_t* mask, int M, int K, int V, int32_t* pass, uint3
                   cudaStream_t s);
 int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M, int K, int V,
                   int value_dtype, shflbw_cu_matrix* out, uint32_t* fail_row, cudaStream_t s);
+int compress_async_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M, int K, int V,
+                        int value_dtype, shflbw_cu_matrix* out, int32_t* status, cudaStream_t s);
+int finalize_impl(shflbw_cu_matrix* m, const int32_t* status, uint32_t* fail_row, cudaStream_t s);
 int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t* group_ncols,
                 const uint32_t* cols, const float* values, int value_dtype, shflbw_cu_matrix* out,
                 cudaStream_t s);

@@ -232,6 +232,37 @@ def compress_shflbw(dense: torch.Tensor, mask: torch.Tensor, v: int,
     return ShflBWMatrix(cm)
 
 
+def compress_shflbw_async(dense: torch.Tensor, mask: torch.Tensor, v: int,
+                          dtype: torch.dtype = torch.bfloat16, out: "ShflBWMatrix | None" = None,
+                          status: torch.Tensor | None = None):
+    """The converter without a host synchronisation (shflbw_cu_compress_async,
+    graph-capturable): -> (matrix, status) with status a device int32[4]
+    {code, fail_row, total columns, widest group}.  The matrix is usable by
+    SpMM / conv work enqueued after it; finalize(matrix, status) raises the
+    reference's exception for a bad mask and sets the exact sizes."""
+    if not (isinstance(dense, torch.Tensor) and dense.is_cuda and dense.dim() == 2):
+        raise BadParams("dense must be a 2-D CUDA tensor")
+    mask = _dev_u8(mask)
+    if tuple(dense.shape) != tuple(mask.shape):
+        raise ShapeMismatch("compress_shflbw: dense and mask shapes differ")
+    dense = dense.contiguous()
+    M, K = mask.shape
+    if status is None:
+        status = torch.zeros(4, dtype=torch.int32, device=dense.device)
+    m = out if out is not None else ShflBWMatrix(L.CuMatrix())
+    _check(_lib().shflbw_cu_compress_async(dense.data_ptr(), _dt(dense.dtype), mask.data_ptr(), M, K, v, _dt(dtype),
+                                           m.ptr, status.data_ptr(), _stream()))
+    m._keep = (dense, mask)  # inputs must outlive the enqueued conversion
+    return m, status
+
+
+def finalize(a: ShflBWMatrix, status: torch.Tensor) -> None:
+    """Read an asynchronous conversion's status (one synchronisation): raises
+    NonConformantMask "(row N)" / BadParams / Error, else fixes the sizes."""
+    fr = C.c_uint32(0)
+    _check(_lib().shflbw_cu_matrix_finalize(a.ptr, status.data_ptr(), C.byref(fr), _stream()))
+
+
 def upload(M: int, K: int, V: int, row_indices, group_ncols, cols, values,
            dtype: torch.dtype = torch.bfloat16) -> ShflBWMatrix:
     """A host (reference-layout) ShflBWMatrix -> device."""

@@ -35,6 +35,47 @@ for name, M, K, V in (("ns", 2048, 2048, 64), ("lf", 16384, 4096, 64), ("ffn1", 
     print(json.dumps({"shape": name, "M": M, "K": K, "wall_ms_median": round(walls[5], 3),
                       "event_ms_median": round(gpus[5], 3), "wall_ms_min": round(walls[0], 3)}), flush=True)
 
+# asynchronous converter (no host sync): enqueue wall time and device time,
+# converting into the same bound-sized matrix (the captured-graph use)
+for name, M, K, V in (("ns", 2048, 2048, 64), ("lf", 16384, 4096, 64), ("ffn1", 2048, 512, 64)):
+    mask = torch.from_numpy(bench.synth_mask(M, K, V, K // 4, 1234)).to(dev)
+    W = bench.uniform16(torch, (M, K), 100, dev)
+    a, st = sb.compress_shflbw_async(W, mask, V)
+    for _ in range(3):
+        sb.compress_shflbw_async(W, mask, V, out=a, status=st)
+    torch.cuda.synchronize()
+    enq, gpus = [], []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        t = time.perf_counter()
+        sb.compress_shflbw_async(W, mask, V, out=a, status=st)
+        enq.append((time.perf_counter() - t) * 1e3)
+        e1.record()
+        torch.cuda.synchronize()
+        gpus.append(e0.elapsed_time(e1))
+    # the same pipeline as one CUDA graph replay
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        sb.compress_shflbw_async(W, mask, V, out=a, status=st)
+    g.replay()
+    torch.cuda.synchronize()
+    gr = []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        gr.append(e0.elapsed_time(e1))
+    sb.finalize(a, st)
+    enq.sort(), gpus.sort(), gr.sort()
+    print(json.dumps({"async_shape": name, "M": M, "K": K, "enqueue_ms_median": round(enq[5], 3),
+                      "event_ms_median": round(gpus[5], 3), "graph_replay_ms_median": round(gr[5], 3)}),
+          flush=True)
+
 # allocation check: repeated compress + free must not grow device usage
 mask = torch.from_numpy(bench.synth_mask(2048, 2048, 64, 512, 1234)).to(dev)
 W = bench.uniform16(torch, (2048, 2048), 100, dev)

@@ -1035,3 +1035,84 @@ def test_persistent_raster_orders_bitwise(sb, oracle, V):
     sb.set_option("raster", 0)
     assert np.array_equal(outs[1], outs[2])
     assert oracle.rel_frobenius(outs[2][:, :128], oracle.spmm(p, np.ascontiguousarray(B[:, :128]))) <= TOL
+
+
+# ------------------------------------------------- asynchronous converter (round 2)
+
+@pytest.mark.parametrize("M,K,V,alpha", [(2048, 2048, 64, 0.25), (4096, 1024, 32, 0.25), (8192, 1024, 128, 0.1),
+                                         (16384, 4096, 64, 0.25), (96, 40, 8, 0.5)])
+def test_compress_async_equals_sync(sb, oracle, M, K, V, alpha):
+    """shflbw_cu_compress_async (no host sync, bound-sized output) + finalize
+    gives the synchronous converter's layout bit for bit, and the SpMM on the
+    matrix before finalize is within tolerance of the oracle."""
+    cpg = int(np.floor(alpha * K + 0.5))
+    mask = oracle.random_shflbw_mask(M, K, V, cpg, oracle.rng(99))
+    W = oracle.round16(oracle.random_dense(M, K, 3))
+    Wd, md = dev(W), dev(mask)
+    a_sync = sb.compress_shflbw(Wd, md, V)
+    a, status = sb.compress_shflbw_async(Wd, md, V)
+    N = 136
+    B = oracle.round16(oracle.random_dense(K, N, 4))
+    Bd = dev(B, torch.bfloat16)
+    early = sb.spmm_execute(a, Bd).cpu().numpy()  # bound sizes, not finalized yet
+    sb.finalize(a, status)
+    st = status.cpu().numpy()
+    assert st[0] == 0 and st[2] == a_sync.total_cols
+    gp, ci, vv = a.raw()
+    gq, cq, vq = a_sync.raw()
+    assert np.array_equal(gp, gq) and np.array_equal(ci, cq) and np.array_equal(vv, vq)
+    ri, gn, cols, vals = a.to_host()
+    rj, gm, colsj, valsj = a_sync.to_host()
+    assert np.array_equal(ri, rj) and np.array_equal(gn, gm)
+    if M * K <= (1 << 24):
+        want = oracle.spmm(oracle.compress(W, mask, V), B)
+        assert oracle.rel_frobenius(early, want) <= TOL
+    assert np.array_equal(sb.spmm_execute(a, Bd).cpu().numpy(), sb.spmm_execute(a_sync, Bd).cpu().numpy())
+
+
+def test_compress_async_reports_errors(sb, oracle):
+    """Non-conformant masks and mask bytes > 1 are reported through the
+    device status and raised by finalize (the reference's classes and
+    fail_row)."""
+    M, K, V = 512, 96, 8
+    mask = oracle.random_shflbw_mask(M, K, V, 24, oracle.rng(5))
+    mask[7, 3] ^= 1
+    want = oracle.validate(mask, V)
+    a, status = sb.compress_shflbw_async(torch.zeros(M, K, device="cuda"), dev(mask), V)
+    with pytest.raises(sb.NonConformantMask, match=rf"\(row {want[1]}\)"):
+        sb.finalize(a, status)
+    bad = mask.copy()
+    bad[0, 0] = 2
+    a, status = sb.compress_shflbw_async(torch.zeros(M, K, device="cuda"), dev(bad), V)
+    with pytest.raises(sb.BadParams):
+        sb.finalize(a, status)
+
+
+def test_compress_async_graph_capture(sb, oracle):
+    """compress_async + SpMM captured in one CUDA graph: replay after the
+    weights change gives the freshly converted product (no host sync inside)."""
+    M, K, N, V = 2048, 1024, 256, 64
+    mask = oracle.random_shflbw_mask(M, K, V, K // 4, oracle.rng(17))
+    md = dev(mask)
+    W = torch.empty((M, K), dtype=torch.bfloat16, device="cuda")
+    B = dev(oracle.round16(oracle.random_dense(K, N, 5)), torch.bfloat16)
+    out = torch.empty((M, N), dtype=torch.float32, device="cuda")
+    W.copy_(dev(oracle.round16(oracle.random_dense(M, K, 6)), torch.bfloat16))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # the bound-sized matrix + warm-up, outside capture
+        a, status = sb.compress_shflbw_async(W, md, V)
+        sb.spmm_execute(a, B, out=out)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):  # converts into a's buffers on every replay
+        sb.compress_shflbw_async(W, md, V, out=a, status=status)
+        sb.spmm_execute(a, B, out=out)
+    for seed in (7, 8):
+        Wn = oracle.round16(oracle.random_dense(M, K, seed))
+        W.copy_(dev(Wn, torch.bfloat16))
+        g.replay()
+        torch.cuda.synchronize()
+        want = oracle.spmm(oracle.compress(Wn, mask, V), oracle.round16(oracle.random_dense(K, N, 5)))
+        assert oracle.rel_frobenius(out.cpu().numpy(), want) <= TOL
+        assert status.cpu().numpy()[0] == 0
