@@ -93,6 +93,10 @@ typedef struct shflbw_cu_matrix {
  * (shflbw_cu_compress_async); a later compress_async of the same shape into
  * this matrix reuses them */
 #define SHFLBW_BOUND_ALLOC 8
+/* shflbw_cu_matrix.reserved bit: some K block is one contiguous run of 64
+ * columns (block-wise patterns; set by shflbw_cu_compress / _upload): the
+ * SpMM loads such blocks as TMA 2D tiles instead of row gathers */
+#define SHFLBW_CONTIG_BLOCKS 16
 
 /* ---- library ---------------------------------------------------------- */
 const char* shflbw_cu_last_error(void);

@@ -656,6 +656,20 @@ __global__ void k_convert_2d(const void* __restrict__ src, int sdt, int64_t ld_s
             store_from_f32(dst, ddt, r * ld_dst + c, load_as_f32(src, sdt, r * ld_src + c));
 }
 
+// *flag |= 1 if any K block of any group is one contiguous run of 64 columns
+// (block-wise patterns: the SpMM then loads those blocks as TMA 2D tiles)
+__global__ void k_contig_blocks(const int32_t* __restrict__ group_ptr, const int32_t* __restrict__ col_idx,
+                                uint32_t* __restrict__ flag) {
+    const int g = blockIdx.x;
+    for (int j = group_ptr[g] + threadIdx.x * SHFLBW_K_TILE; j < group_ptr[g + 1]; j += blockDim.x * SHFLBW_K_TILE) {
+        const int first = col_idx[j], last = col_idx[j + SHFLBW_K_TILE - 1];
+        if (first >= 0 && last - first == SHFLBW_K_TILE - 1) {
+            atomicOr(flag, 1u);
+            return;
+        }
+    }
+}
+
 // asynchronous converter status: [0] status code, [1] fail_row, [2] total
 // columns (group_ptr[G]), [3] widest group (padded)
 __global__ void k_status(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ fail_row,
@@ -1013,9 +1027,20 @@ int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M
             SBW_LAUNCHED("k_pack_values");
         }
     }
+    // contiguous 64-column K blocks anywhere (block-wise masks)?
+    uint32_t contig = 0;
+    if (G > 0 && total_cols > 0) {
+        DevBuf cf;
+        SBW_CUDA(cf.alloc(sizeof(uint32_t), s));
+        SBW_CUDA(cudaMemsetAsync(cf.p, 0, sizeof(uint32_t), s));
+        k_contig_blocks<<<G, 32, 0, s>>>(out->group_ptr, out->col_idx, cf.as<uint32_t>());
+        SBW_LAUNCHED("k_contig_blocks");
+        SBW_CUDA(cudaMemcpyAsync(&contig, cf.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    }
     // the matrix is complete on return (SpMM prologues read it before their
     // programmatic-launch wait, see the "pdl" option)
     SBW_CUDA(cudaStreamSynchronize(s));
+    if (contig) out->reserved |= SHFLBW_CONTIG_BLOCKS;
     return SHFLBW_OK;
 }
 
@@ -1223,6 +1248,18 @@ int upload_impl(int M, int K, int V, const uint32_t* row_indices, const uint32_t
         if (hf[1]) return cleanup(fail(SHFLBW_SHAPE_MISMATCH, "column index exceeds B rows or is not increasing"));
     }
     SBW_CUDA(cudaStreamSynchronize(s));
+    {   // contiguous 64-column K blocks (the device layout's K blocks start at
+        // each group's column 0)
+        int64_t off = 0;
+        for (int g = 0; g < G && !(out->reserved & SHFLBW_CONTIG_BLOCKS); ++g) {
+            for (uint32_t j = 0; j + SHFLBW_K_TILE <= group_ncols[g]; j += SHFLBW_K_TILE)
+                if (cols[off + j + SHFLBW_K_TILE - 1] - cols[off + j] == SHFLBW_K_TILE - 1) {
+                    out->reserved |= SHFLBW_CONTIG_BLOCKS;
+                    break;
+                }
+            off += group_ncols[g];
+        }
+    }
     return SHFLBW_OK;
 }
 
@@ -1293,7 +1330,8 @@ int conv_prepare_impl(const shflbw_cu_matrix* w, int S, shflbw_cu_matrix* out, c
         });
         SBW_LAUNCHED("k_conv_scatter");
     }
-    out->reserved = (w->reserved & ~(SHFLBW_CONV_ORDER | (0xff << 8))) | SHFLBW_CONV_ORDER | (S << 8);
+    out->reserved = (w->reserved & ~(SHFLBW_CONV_ORDER | SHFLBW_CONTIG_BLOCKS | (0xff << 8))) | SHFLBW_CONV_ORDER |
+                    (S << 8);
     SBW_CUDA(cudaStreamSynchronize(s));
     return SHFLBW_OK;
 }

@@ -158,6 +158,6 @@ int shflbw_cu_fold_input_permutation(shflbw_cu_matrix* a, const int32_t* produce
         SBW_CUDA(cudaStreamSynchronize(s));
         if (h) return fail(SHFLBW_BAD_PARAMS, "fold: producer_rows is not a permutation of 0..cols-1");
     }
-    a->reserved |= SHFLBW_FOLDED;
+    a->reserved = (a->reserved | SHFLBW_FOLDED) & ~SHFLBW_CONTIG_BLOCKS;
     return SHFLBW_OK;
 }

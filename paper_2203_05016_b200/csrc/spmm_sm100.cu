@@ -299,6 +299,16 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
     prm.PQ = b.P * qp;
     prm.ksplit = hybrid ? 2 : ((cs > 1 && (!vsplit || conv_ksplit)) ? 1 : 0);
     prm.tile_n = tile_n;
+    // TMA tile loads for contiguous K blocks: matrices that have them
+    // (SHFLBW_CONTIG_BLOCKS); option "tile_loads" -1: gathers only, 1: check
+    // every K block of any matrix
+    {
+        const int64_t tl = option("tile_loads");
+        // (the per-block check "last - first == 63" relies on ascending
+        // columns: not for folded or conv-ordered matrices)
+        const bool ascending = !(a->reserved & (SHFLBW_FOLDED | SHFLBW_CONV_ORDER));
+        prm.tiles = b.kind == 0 && ascending && (tl > 0 || (tl == 0 && (a->reserved & SHFLBW_CONTIG_BLOCKS))) ? 1 : 0;
+    }
     {
         // SpMM gather issue ("gather_issue"): 1 = one elected lane per warp
         // issues the warp's gathers back to back, 2 = each issuing lane its
@@ -398,7 +408,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         if (prm.gw != 4 && prm.gw != 8) return fail(SHFLBW_BAD_PARAMS, "gather_warps must be 4 or 8");
     }
 
-    CUtensorMap tmB, tmW;
+    CUtensorMap tmB, tmW, tmBt;
     int st;
     if (b.kind == 0)
         st = make_map_2d(&tmB, a->dtype, b.ptr, static_cast<uint64_t>(b.N), static_cast<uint64_t>(b.K),
@@ -410,6 +420,14 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         st = make_map_2d(&tmB, a->dtype, b.ptr, static_cast<uint64_t>(b.Nb),
                          static_cast<uint64_t>(b.C) * b.H * b.W, static_cast<uint64_t>(b.Nb) * 2, bw, 1, bw * 2);
     if (st) return st;
+    // block-wise K blocks: B as 64-column x 64-row TMA tiles (SpMM only)
+    if (b.kind == 0 && prm.tiles) {
+        st = make_map_2d(&tmBt, a->dtype, b.ptr, static_cast<uint64_t>(b.N), static_cast<uint64_t>(b.K),
+                         static_cast<uint64_t>(b.ldb) * 2, 64, 64, 128);
+        if (st) return st;
+    } else {
+        tmBt = tmB;
+    }
     const int wbox = vs < 64 ? vs : 64;
     const int64_t wrows = a->total_cols > 0 ? a->total_cols : 1;
     st = make_map_2d(&tmW, a->dtype, a->values, static_cast<uint64_t>(V), static_cast<uint64_t>(wrows),
@@ -428,10 +446,10 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         set_plan(plan);
     }
     if (a->dtype == SHFLBW_BF16)
-        return b.kind == 0 ? tc::dispatch<SHFLBW_BF16, 0>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s)
-                           : tc::dispatch<SHFLBW_BF16, 1>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s);
-    return b.kind == 0 ? tc::dispatch<SHFLBW_F16, 0>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s)
-                       : tc::dispatch<SHFLBW_F16, 1>(vs, cs, b.kind, tmB, tmW, prm, n_tiles, groups, s);
+        return b.kind == 0 ? tc::dispatch<SHFLBW_BF16, 0>(vs, cs, b.kind, tmB, tmW, tmBt, prm, n_tiles, groups, s)
+                           : tc::dispatch<SHFLBW_BF16, 1>(vs, cs, b.kind, tmB, tmW, tmBt, prm, n_tiles, groups, s);
+    return b.kind == 0 ? tc::dispatch<SHFLBW_F16, 0>(vs, cs, b.kind, tmB, tmW, tmBt, prm, n_tiles, groups, s)
+                       : tc::dispatch<SHFLBW_F16, 1>(vs, cs, b.kind, tmB, tmW, tmBt, prm, n_tiles, groups, s);
 }
 
 }  // namespace sbw

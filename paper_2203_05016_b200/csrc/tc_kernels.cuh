@@ -94,6 +94,8 @@ struct TcParams {
     int per_sm;      // persistent: resident CTAs per SM
     int gw;          // gather warps per CTA (4, 8)
     int issue1;      // 1: SpMM gathers issued by one elected lane per warp (option "gather_issue")
+    int tiles;       // 1: SpMM K blocks whose 64 columns are one contiguous run (block-wise
+                     //    patterns) load B with two TMA 2D tiles instead of 32 gather4s
     int raster;      // persistent unit order: 1 group-major, 2 column-tile-major
     int tile_n;      // output columns per unit: 128, or 64 (k_spmm_tc, SpMM only: half-width units)
     int n_extra;     // further output destinations (fused all-gather), staged-store path only
@@ -509,6 +511,7 @@ __device__ __forceinline__ int conv_wide_rows(const TcParams& p, int4& ci, int h
 template <int DT, int VS, int CS, int KIND, int KSPLIT, int GW>
 __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     k_spmm_tc(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
+              const __grid_constant__ CUtensorMap tmBt,
               TcParams p) {
     using WL = WeightLayout<VS>;
     constexpr int kStageBytes = kABytes + WL::kBytes;
@@ -715,7 +718,20 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
             if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
             unsigned char* a_st = smem + s * kStageBytes;
             const int32_t* mk = meta_s + win * kBlockK;
-            if (KIND == 0 && p.issue1) {
+            // block-wise K block: its 64 (ascending) columns are c0..c0+63
+            int c0 = -1;
+            if constexpr (KIND == 0 && !mcast) {
+                if (p.tiles) {
+                    const int first = mk[0], last = mk[kBlockK - 1];
+                    if (first >= 0 && last - first == kBlockK - 1) c0 = first;
+                }
+            }
+            if (c0 >= 0) {
+                // B rows c0..c0+63 of each 64-column slab: one 2D TMA tile per
+                // slab into the same swizzled layout the gathers produce
+                if (gw == 0 && elect_one_sync())
+                    for (int bb = 0; bb < nblk; ++bb) tma_load_2d(a_st + bb * blk_bytes, &tmBt, &full[s], n0 + bb * 64, c0);
+            } else if (KIND == 0 && p.issue1) {
                 // SpMM, option "gather_issue" 1: this warp's gathers for the
                 // stage issued back to back by one elected lane, all index
                 // loads first (the per-lane issue compiles to a serialised
@@ -940,7 +956,8 @@ __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc,
 
 template <int DT, int VS, int CS, int KIND, int GW>
 __global__ void __launch_bounds__(192 + 32 * GW, 2)
-    k_spmm_persist(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW, TcParams p,
+    k_spmm_persist(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
+                   const __grid_constant__ CUtensorMap tmBt, TcParams p,
                    int units, int n_tiles) {
     using WL = WeightLayout<VS>;
     constexpr int kStageBytes = kABytes + WL::kBytes;
@@ -1137,7 +1154,18 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
                     named_bar<kGT>(2);
                 }
                 if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
-                if (KIND == 0 && p.issue1) {
+                int c0 = -1;  // block-wise K block (k_spmm_tc)
+                if constexpr (KIND == 0 && !mcast) {
+                    if (p.tiles) {
+                        const int first = mbuf[win * kBlockK], last = mbuf[win * kBlockK + kBlockK - 1];
+                        if (first >= 0 && last - first == kBlockK - 1) c0 = first;
+                    }
+                }
+                if (c0 >= 0) {
+                    if (gw == 0 && elect_one_sync())
+                        for (int bb = 0; bb < nblk; ++bb)
+                            tma_load_2d(smem + s * kStageBytes + bb * blk_bytes, &tmBt, &full[s], n0 + bb * 64, c0);
+                } else if (KIND == 0 && p.issue1) {
                     // SpMM: one elected lane per warp issues the warp's
                     // gathers back to back, index loads first (k_spmm_tc)
                     if (elect_one_sync()) {
@@ -1261,7 +1289,7 @@ struct SmemCaps {
 };
 
 template <int DT, int VS, int CS, int KIND, int KSPLIT, int GW>
-int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles, int groups,
               cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
     constexpr int KSF = KSPLIT == 1 ? CS : (KSPLIT == 2 ? 2 : 1);
@@ -1288,14 +1316,14 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& pr
     attr[1].val.programmaticStreamSerializationAllowed = option("pdl") ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, prm));
+    SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, tmBt, prm));
     count_launch();
     return SHFLBW_OK;
 }
 
 
 template <int DT, int VS, int CS, int KIND, int GW>
-int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles, int groups,
                    cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
     const size_t out_esz = prm.c_dtype == SHFLBW_F32 ? 4 : 2;
@@ -1331,48 +1359,48 @@ int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParam
     attr[1].val.programmaticStreamSerializationAllowed = option("pdl") ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, prm, units, n_tiles));
+    SBW_CUDA(cudaLaunchKernelEx(&cfg, kern, tmB, tmW, tmBt, prm, units, n_tiles));
     count_launch();
     return SHFLBW_OK;
 }
 
 // gather warps per CTA (prm.gw): 4 or 8
 template <int DT, int VS, int CS, int KIND, int KSPLIT>
-int launch_tc_gw(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+int launch_tc_gw(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles, int groups,
                  cudaStream_t s) {
     // (V = 128 K-split epilogues hold 128 fp32 partials per thread: they would
     // spill at the 2-CTA register budget of 8 gather warps)
     if constexpr (!(VS == 128 && KSPLIT != 0))
-        if (prm.gw == 8) return launch_tc<DT, VS, CS, KIND, KSPLIT, 8>(tmB, tmW, prm, n_tiles, groups, s);
-    return launch_tc<DT, VS, CS, KIND, KSPLIT, 4>(tmB, tmW, prm, n_tiles, groups, s);
+        if (prm.gw == 8) return launch_tc<DT, VS, CS, KIND, KSPLIT, 8>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+    return launch_tc<DT, VS, CS, KIND, KSPLIT, 4>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
 }
 
 template <int DT, int VS, int CS, int KIND>
-int launch_persist_gw(const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles, int groups,
+int launch_persist_gw(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles, int groups,
                       cudaStream_t s) {
-    if (prm.gw >= 8) return launch_persist<DT, VS, CS, KIND, 8>(tmB, tmW, prm, n_tiles, groups, s);
-    return launch_persist<DT, VS, CS, KIND, 4>(tmB, tmW, prm, n_tiles, groups, s);
+    if (prm.gw >= 8) return launch_persist<DT, VS, CS, KIND, 8>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+    return launch_persist<DT, VS, CS, KIND, 4>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
 }
 
 // SpMM variants: V split (CS CTAs, multicast), K split, 2 x 2, persistent
 template <int DT, int VS>
-int dispatch_spmm(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles,
+int dispatch_spmm(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles,
                   int groups, cudaStream_t s) {
     if (prm.persistent) {
         switch (cs) {
-            case 1: return launch_persist_gw<DT, VS, 1, 0>(tmB, tmW, prm, n_tiles, groups, s);
-            case 2: return launch_persist_gw<DT, VS, 2, 0>(tmB, tmW, prm, n_tiles, groups, s);
-            case 4: return launch_persist_gw<DT, VS, 4, 0>(tmB, tmW, prm, n_tiles, groups, s);
+            case 1: return launch_persist_gw<DT, VS, 1, 0>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+            case 2: return launch_persist_gw<DT, VS, 2, 0>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+            case 4: return launch_persist_gw<DT, VS, 4, 0>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
         }
         return SHFLBW_UNSUPPORTED;
     }
     switch (cs * 2 + prm.ksplit) {
-        case 2: case 3: return launch_tc_gw<DT, VS, 1, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 4: return launch_tc_gw<DT, VS, 2, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 5: return launch_tc_gw<DT, VS, 2, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
-        case 8: return launch_tc_gw<DT, VS, 4, 0, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 9: return launch_tc_gw<DT, VS, 4, 0, 1>(tmB, tmW, prm, n_tiles, groups, s);
-        case 10: return launch_tc_gw<DT, VS, 4, 0, 2>(tmB, tmW, prm, n_tiles, groups, s);
+        case 2: case 3: return launch_tc_gw<DT, VS, 1, 0, 0>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        case 4: return launch_tc_gw<DT, VS, 2, 0, 0>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        case 5: return launch_tc_gw<DT, VS, 2, 0, 1>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        case 8: return launch_tc_gw<DT, VS, 4, 0, 0>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        case 9: return launch_tc_gw<DT, VS, 4, 0, 1>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        case 10: return launch_tc_gw<DT, VS, 4, 0, 2>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }
@@ -1381,13 +1409,13 @@ int dispatch_spmm(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const 
 // conv-ordered weight, 128-byte rows): one CTA per unit, K split over 2 or 4
 // CTAs, persistent
 template <int DT, int VS, int KIND>
-int dispatch_conv(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm, int n_tiles,
+int dispatch_conv(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles,
                   int groups, cudaStream_t s) {
-    if (prm.persistent) return launch_persist_gw<DT, VS, 1, KIND>(tmB, tmW, prm, n_tiles, groups, s);
+    if (prm.persistent) return launch_persist_gw<DT, VS, 1, KIND>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
     switch (cs * 2 + prm.ksplit) {
-        case 2: case 3: return launch_tc_gw<DT, VS, 1, KIND, 0>(tmB, tmW, prm, n_tiles, groups, s);
-        case 5: return launch_tc_gw<DT, VS, 2, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
-        case 9: return launch_tc_gw<DT, VS, 4, KIND, 1>(tmB, tmW, prm, n_tiles, groups, s);
+        case 2: case 3: return launch_tc_gw<DT, VS, 1, KIND, 0>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        case 5: return launch_tc_gw<DT, VS, 2, KIND, 1>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        case 9: return launch_tc_gw<DT, VS, 4, KIND, 1>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
     }
     return SHFLBW_UNSUPPORTED;
 }
@@ -1395,12 +1423,12 @@ int dispatch_conv(int cs, const CUtensorMap& tmB, const CUtensorMap& tmW, const 
 // KG 0: SpMM (kind 0), KG 1: conv (kinds 1, 2) -- explicitly instantiated in
 // tc_inst_{bf16,f16}_{spmm,conv}.cu
 template <int DT, int KG>
-int dispatch(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const TcParams& prm,
+int dispatch(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm,
              int n_tiles, int groups, cudaStream_t s) {
     auto one = [&]<int VS>() -> int {
-        if constexpr (KG == 0) return dispatch_spmm<DT, VS>(cs, tmB, tmW, prm, n_tiles, groups, s);
-        else if (kind == 2) return dispatch_conv<DT, VS, 2>(cs, tmB, tmW, prm, n_tiles, groups, s);
-        else return dispatch_conv<DT, VS, 1>(cs, tmB, tmW, prm, n_tiles, groups, s);
+        if constexpr (KG == 0) return dispatch_spmm<DT, VS>(cs, tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        else if (kind == 2) return dispatch_conv<DT, VS, 2>(cs, tmB, tmW, tmBt, prm, n_tiles, groups, s);
+        else return dispatch_conv<DT, VS, 1>(cs, tmB, tmW, tmBt, prm, n_tiles, groups, s);
     };
     switch (vs) {
         case 16: return one.template operator()<16>();
@@ -1412,7 +1440,7 @@ int dispatch(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap
 }
 
 #define SBW_TC_DISPATCH(DT, KG)                                                                          \
-    int dispatch<DT, KG>(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW,      \
+    int dispatch<DT, KG>(int vs, int cs, int kind, const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt,      \
                          const TcParams& prm, int n_tiles, int groups, cudaStream_t s)
 extern template SBW_TC_DISPATCH(SHFLBW_BF16, 0);
 extern template SBW_TC_DISPATCH(SHFLBW_BF16, 1);

@@ -9,8 +9,10 @@ input sets, CUDA graph, CUDA events):
   * VW (vector-wise): the same kernel on a mask whose groups are V
     consecutive rows, so row_indices is the identity (the paper's "row
     shuffling is nearly free" claim, PAPER.md:268, is Shfl-BW / VW ~ 1);
-  * BW (block-wise V x V, the same density) through the library's BSR kernel
-    (torch.sparse_bsr_tensor @ dense, cuSPARSE), where it runs;
+  * BW (block-wise V x V, the same density) through this library: every K
+    block is one contiguous 64-column run, loaded as two TMA 2D tiles (and,
+    for comparison, with the Shfl-BW gathers); and through the library BSR
+    kernel (torch.sparse_bsr_tensor @ dense, cuSPARSE), where it runs;
   * dense cuBLAS bf16 GEMM.
 """
 import argparse
@@ -79,6 +81,17 @@ def main():
             res["shflbw_over_vw"] = res["shflbw_us"] / res["vw_us"]
             res["dense_us"] = sweep.time_steps(lambda i: torch.mm(Ws[i % n], Bs[i % n], out=Cs[i % n]),
                                                args.steps) * 1e3
+            # block-wise V x V through this library: every K block is one
+            # contiguous 64-column run -> two TMA 2D tiles per K block (default)
+            # or, for comparison, the same gathers as Shfl-BW
+            bwm = torch.from_numpy(bw_mask(M, K, V, alpha, 1234)).to(dev)
+            bmats = [sb.compress_shflbw(w, bwm, V) for w in Ws]
+            for tl, key in ((0, "bw_tiles_us"), (-1, "bw_gathers_us")):
+                sb.set_option("tile_loads", tl)
+                res[key] = sweep.time_steps(lambda i: sb.spmm_execute(bmats[i % n], Bs[i % n], out=Cs[i % n]),
+                                            args.steps) * 1e3
+            sb.set_option("tile_loads", 0)
+            res["shflbw_over_bw"] = res["shflbw_us"] / res["bw_tiles_us"]
             try:  # block-wise through the library BSR kernel (cuSPARSE)
                 bm = torch.from_numpy(bw_mask(M, K, V, alpha, 1234)).to(dev).to(torch.bfloat16)
                 bsr = [(w * bm).to_sparse_bsr((V, V)) for w in Ws]
@@ -88,12 +101,14 @@ def main():
                 res["bsr_error"] = f"{type(e).__name__}: {str(e)[:120]}"
             rows.append(res)
             print(json.dumps(res), flush=True)
-    lines = ["| shape | sparsity | Shfl-BW us | VW us | Shfl-BW / VW | BW via cuSPARSE BSR us | dense cuBLAS us |",
-             "|---|---|---|---|---|---|---|"]
+    lines = ["| shape | sparsity | Shfl-BW us | VW us | Shfl-BW / VW | BW us (TMA tiles) | BW us (gathers) | "
+             "Shfl-BW / BW | BW via cuSPARSE BSR us | dense cuBLAS us |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         bsr = f"{r['bsr_us']:.2f}" if r["bsr_us"] else "n/a"
         lines.append(f"| {r['shape']} | {r['sparsity']:.0%} | {r['shflbw_us']:.2f} | {r['vw_us']:.2f} | "
-                     f"{r['shflbw_over_vw']:.3f} | {bsr} | {r['dense_us']:.2f} |")
+                     f"{r['shflbw_over_vw']:.3f} | {r['bw_tiles_us']:.2f} | {r['bw_gathers_us']:.2f} | "
+                     f"{r['shflbw_over_bw']:.3f} | {bsr} | {r['dense_us']:.2f} |")
     with open(args.out + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(args.out + ".json", "w") as f:

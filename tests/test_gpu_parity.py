@@ -1116,3 +1116,42 @@ def test_compress_async_graph_capture(sb, oracle):
         want = oracle.spmm(oracle.compress(Wn, mask, V), oracle.round16(oracle.random_dense(K, N, 5)))
         assert oracle.rel_frobenius(out.cpu().numpy(), want) <= TOL
         assert status.cpu().numpy()[0] == 0
+
+
+# ------------------------------------------- block-wise K blocks: TMA tiles (round 2)
+
+def _bw_mask(M, K, V, keep, seed):
+    rs = np.random.RandomState(seed)
+    blocks = np.zeros((M // V, K // V), np.uint8)
+    for i in range(M // V):
+        blocks[i, rs.permutation(K // V)[:keep]] = 1
+    return np.kron(blocks, np.ones((V, V), np.uint8))
+
+
+@pytest.mark.parametrize("M,N,K,keep,persistent", [(1024, 128, 2048, 8, 0), (512, 4096, 2048, 8, 0),
+                                                   (2048, 1000, 1024, 4, 2), (1024, 200, 1024, 5, -1)])
+def test_blockwise_tile_loads_bitwise(sb, oracle, M, N, K, keep, persistent):
+    """Block-wise V x V masks (V = 64): every K block is one contiguous run of
+    64 columns, loaded as two TMA 2D tiles instead of 32 gather4s -- the same
+    operand bytes in the same layout, so the result is bit-identical to the
+    gather path; a mask mixing runs and scattered columns too."""
+    V = 64
+    mask = _bw_mask(M, K, V, keep, 3)
+    if persistent == -1:  # mix: scatter one group's columns
+        mask[:V] = 0
+        mask[:V, np.random.RandomState(1).choice(K, 96, replace=False)] = 1
+    W = oracle.round16(oracle.random_dense(M, K, 1))
+    B = oracle.round16(oracle.random_dense(K, N, 2))
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    sb.set_option("persistent", persistent if persistent > 0 else 0)
+    outs = {}
+    for tl in ((0 if persistent != -1 else 1), -1):  # auto (matrix flag) / forced check, gathers only
+        sb.set_option("tile_loads", tl)
+        outs[tl] = (sb.spmm_execute(a, Bd).cpu().numpy(),
+                    sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
+    sb.set_option("tile_loads", 0)
+    sb.set_option("persistent", 0)
+    t = 0 if persistent != -1 else 1
+    assert np.array_equal(outs[t][0], outs[-1][0]) and np.array_equal(outs[t][1], outs[-1][1])
+    assert oracle.rel_frobenius(outs[t][0][:, :128], oracle.spmm(p, np.ascontiguousarray(B[:, :128]))) <= TOL
