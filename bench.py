@@ -517,6 +517,36 @@ def sharded_lf(torch, sb, dist, world, rank, dev, steps, barrier):
         out["fused_p2p"] = {"ms_per_step": fms, "value": flops / (fms * 1e-3) / 1e12, "unit": UNIT,
                             "collective": "none: shflbw_cu_spmm_groups_peers stores every row into all ranks' "
                                           "outputs over P2P (CUDA IPC) from the epilogue"}
+        # the same gather through an NVLS multicast address (one multimem.st
+        # per 16 bytes, replicated by the NVSwitch), where the box offers it
+        try:
+            from paper_2203_05016_b200.sharded import MulticastOutputs
+            mouts = MulticastOutputs((M, N), torch.bfloat16)
+            mc = mouts.mc_ptr + mouts.mc_offset if mouts.mc_ptr else 0
+        except Exception as e:  # noqa: BLE001
+            mouts, mc, why = None, 0, f"{type(e).__name__}: {str(e)[:160]}"
+        else:
+            why = "no multicast address (symmetric-memory multicast_ptr == 0)"
+        mc = int(max_over_ranks(torch, dist, 0.0 if mc else 1.0) == 0.0) and mc  # every rank must have one
+        if mc:
+            for _ in range(2):
+                sb.spmm_groups_multicast(a, g0, g1, B, mc, torch.bfloat16, N)
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                sb.spmm_groups_multicast(a, g0, g1, B, mc, torch.bfloat16, N)
+            e1.record()
+            torch.cuda.synchronize()
+            mms = max_over_ranks(torch, dist, e0.elapsed_time(e1) / reps)
+            barrier()
+            out["fused_multicast"] = {"ms_per_step": mms, "value": flops / (mms * 1e-3) / 1e12, "unit": UNIT,
+                                      "collective": "none: shflbw_cu_spmm_groups_multicast, one multimem.st per "
+                                                    "16-byte row chunk through the NVLS multicast address"}
+        else:
+            out["fused_multicast"] = {"unavailable": why}
+        del mouts
     del a, B, C
     torch.cuda.empty_cache()
     return out

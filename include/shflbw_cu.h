@@ -242,6 +242,17 @@ int shflbw_cu_spmm_groups_peers(const shflbw_cu_matrix* a, int32_t g_begin, int3
                                 void* const* C_dst, int32_t n_dst, int32_t c_dtype,
                                 int64_t ldc, shflbw_stream_t stream);
 
+/* The same with the gather through NVLink SHARP (NVLS) multicast: C_mc is a
+ * multicast address bound to every rank's full C (e.g. torch symmetric
+ * memory's multicast_ptr, or cuMulticastCreate + cuMulticastBindMem +
+ * cuMemMap); each finished 16-byte row chunk is ONE multimem.st that the
+ * NVSwitch replicates into all GPUs' outputs (the P2P variant above issues P
+ * stores).  bf16 / f16 output, the tcgen05 path, same ordering contract. */
+int shflbw_cu_spmm_groups_multicast(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_end,
+                                    const void* B, int32_t K_b, int32_t N, int64_t ldb,
+                                    void* C_mc, int32_t c_dtype, int64_t ldc,
+                                    shflbw_stream_t stream);
+
 /* Conv weight layout (cf. a library's one-time filter reorder): *out = a copy
  * of w whose columns are, per group, ordered by filter column s = c % S
  * (ascending c within each s) with every s-run padded to a multiple of 4 by

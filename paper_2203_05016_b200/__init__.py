@@ -11,7 +11,7 @@ from .shflbw import (BadGeometry, BadMagic, BadParams, ConvGeometry, CorruptPayl
                      PruneConfig, PruneResult, importance_scores, kept_score, kmeans_row_grouping,
                      prune_shflbw, prune_unstructured, prune_vectorwise,
                      ShflBWMatrix, TileConfig, compress_shflbw, compress_shflbw_async, conv2d, conv_output_size, conv_prepare,
-                     decompress, finalize, fold_input_permutation, last_plan, launch_count, set_option, spmm_execute, spmm_groups, spmm_groups_peers,
+                     decompress, finalize, fold_input_permutation, last_plan, launch_count, set_option, spmm_execute, spmm_groups, spmm_groups_multicast, spmm_groups_peers,
                      unpermute_rows, upload, validate_pattern)
 
 __all__ = ["BadGeometry", "BadMagic", "BadParams", "ConvGeometry", "CorruptPayload", "Error", "NonConformantMask",
@@ -20,5 +20,5 @@ __all__ = ["BadGeometry", "BadMagic", "BadParams", "ConvGeometry", "CorruptPaylo
            "prune_shflbw", "prune_unstructured", "prune_vectorwise",
            "ShflBWMatrix", "TileConfig", "compress_shflbw", "compress_shflbw_async", "conv2d", "conv_output_size", "conv_prepare",
            "decompress", "finalize",
-           "fold_input_permutation", "last_plan", "launch_count", "set_option", "spmm_execute", "spmm_groups", "spmm_groups_peers",
+           "fold_input_permutation", "last_plan", "launch_count", "set_option", "spmm_execute", "spmm_groups", "spmm_groups_multicast", "spmm_groups_peers",
            "unpermute_rows", "upload", "validate_pattern"]

@@ -65,6 +65,9 @@ SIGNATURES = {
     "shflbw_cu_spmm_groups_peers": (C.c_int, [C.POINTER(CuMatrix), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                               C.c_int32, C.c_int64, C.POINTER(C.c_void_p), C.c_int32, C.c_int32,
                                               C.c_int64, C.c_void_p]),
+    "shflbw_cu_spmm_groups_multicast": (C.c_int, [C.POINTER(CuMatrix), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                                  C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_int64,
+                                                  C.c_void_p]),
     "shflbw_cu_spmm_groups": (C.c_int, [C.POINTER(CuMatrix), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                         C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                         C.c_void_p]),

@@ -76,15 +76,15 @@ int run_spmm(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b
         // (the message names the reason), not a silent CUDA-core fallback
         if (st != SHFLBW_UNSUPPORTED || option("strict")) return st;
     }
-    if (c.n_extra > 0)
-        return fail(SHFLBW_UNSUPPORTED, "spmm with peer destinations: needs the tcgen05 path (bf16/f16 matrix, V in "
-                                        "{16, 32, 64, 128}, 16-byte aligned rows)");
+    if (c.n_extra > 0 || c.multicast)
+        return fail(SHFLBW_UNSUPPORTED, "spmm with peer / multicast destinations: needs the tcgen05 path (bf16/f16 "
+                                        "matrix, V in {16, 32, 64, 128}, 16-byte aligned rows)");
     return spmm_simt(a, g_begin, g_end, b, c, s);
 }
 
 int spmm_groups_impl(const shflbw_cu_matrix* a, int g_begin, int g_end, const void* B, int K_b, int N,
                      int64_t ldb, void* C, int c_dtype, int64_t ldc, int compact, cudaStream_t s,
-                     void* const* extra = nullptr, int n_extra = 0) {
+                     void* const* extra = nullptr, int n_extra = 0, int multicast = 0) {
     if (int st = check_compute_matrix(a)) return st;
     if (int st = check_out_dtype(c_dtype)) return st;
     if (K_b != a->cols) return fail(SHFLBW_SHAPE_MISMATCH, "spmm: A columns != B rows");
@@ -109,6 +109,7 @@ int spmm_groups_impl(const shflbw_cu_matrix* a, int g_begin, int g_end, const vo
         c.extra[d] = extra[d];
     }
     c.n_extra = n_extra;
+    c.multicast = multicast;
     return run_spmm(a, g_begin, g_end, b, c, s);
 }
 
@@ -239,6 +240,15 @@ int shflbw_cu_spmm_groups_peers(const shflbw_cu_matrix* a, int32_t g_begin, int3
     if (c_dtype == SHFLBW_F32) return fail(SHFLBW_UNSUPPORTED, "spmm_groups_peers: 16-bit output only");
     return spmm_groups_impl(a, g_begin, g_end, B, K_b, N, ldb, C_dst[0], c_dtype, ldc, 0,
                             reinterpret_cast<cudaStream_t>(stream), C_dst + 1, n_dst - 1);
+}
+
+int shflbw_cu_spmm_groups_multicast(const shflbw_cu_matrix* a, int32_t g_begin, int32_t g_end, const void* B,
+                                    int32_t K_b, int32_t N, int64_t ldb, void* C_mc, int32_t c_dtype, int64_t ldc,
+                                    shflbw_stream_t stream) {
+    if (c_dtype == SHFLBW_F32) return fail(SHFLBW_UNSUPPORTED, "spmm_groups_multicast: 16-bit output only");
+    if (!C_mc || (reinterpret_cast<uintptr_t>(C_mc) & 15)) return fail(SHFLBW_BAD_PARAMS, "spmm_groups_multicast: null or unaligned address");
+    return spmm_groups_impl(a, g_begin, g_end, B, K_b, N, ldb, C_mc, c_dtype, ldc, 0,
+                            reinterpret_cast<cudaStream_t>(stream), nullptr, 0, 1);
 }
 
 int shflbw_cu_unpermute_rows(const int32_t* row_indices, int32_t M, int32_t N, const void* C_perm,

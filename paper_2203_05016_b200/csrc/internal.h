@@ -63,6 +63,9 @@ struct OutSpec {
     // through P2P mappings: the all-gather fused into the epilogue)
     void* extra[kMaxPeers - 1] = {};
     int n_extra = 0;
+    // 1: ptr is an NVLS multicast address -- every row store is one
+    // multimem.st that lands in all bound GPUs' outputs
+    int multicast = 0;
 };
 
 // spmm_simt.cu: CUDA-core kernel, any V, bit-exact ascending-k order

@@ -346,6 +346,8 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
                 if (reinterpret_cast<uintptr_t>(c.extra[d]) % 16 != 0) return unsup("peer destination not 16-byte aligned");
         }
         prm.n_extra = c.n_extra;
+        prm.mc = c.multicast;
+        if (c.multicast && !prm.bulk_out) return unsup("multicast output needs 16-byte aligned output rows");
         for (int d = 0; d < c.n_extra; ++d) prm.C_extra[d] = c.extra[d];
     }
     // persistent when one wave of CTAs cannot cover the units (option
@@ -374,7 +376,7 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const int64_t stage = kABytes + static_cast<int64_t>(kBlockK) * vs * 2;
         const int64_t with_tile = (budget - fixed - tile) / stage, without = (budget - fixed) / stage;
         if (prm.bulk_out && with_tile < 2) {  // the staged epilogue is worth a stage
-            if (c.n_extra > 0) prm.persistent = 0;  // ... unless it carries the extra destinations
+            if (c.n_extra > 0 || c.multicast) prm.persistent = 0;  // ... unless it carries the extra / multicast stores
             else prm.bulk_out = 0;
         }
         const int64_t fit = prm.bulk_out ? with_tile : without;

@@ -99,6 +99,7 @@ struct TcParams {
     int raster;      // persistent unit order: 1 group-major, 2 column-tile-major
     int tile_n;      // output columns per unit: 128, or 64 (k_spmm_tc, SpMM only: half-width units)
     int n_extra;     // further output destinations (fused all-gather), staged-store path only
+    int mc;          // 1: C is an NVLS multicast address (multimem.st row stores), staged-store path only
     void* C_extra[kMaxPeers - 1];
 };
 
@@ -194,7 +195,8 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
                              : "r"(cb + static_cast<uint32_t>(v * kBlockN * esz + pc * 16)));
                 asm volatile("ld.shared.b32 %0, [%1];" : "=r"(row) : "r"(rbase + static_cast<uint32_t>(v * 4)));
                 const int64_t off = (static_cast<int64_t>(row) * p.ldc + nn) * esz;
-                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + off) = x;
+                if (p.mc) multimem_st16(static_cast<char*>(p.C) + off, x);
+                else *reinterpret_cast<int4*>(static_cast<char*>(p.C) + off) = x;
                 for (int d = 0; d < p.n_extra; ++d) *reinterpret_cast<int4*>(static_cast<char*>(p.C_extra[d]) + off) = x;
             }
         }
@@ -220,9 +222,11 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
 #pragma unroll
         for (int k = 0; k < kIters; ++k) {
             const int v = v0 + k * 4 * kRowsPerInst;
-            if (v < ROWS)
-                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + (static_cast<int64_t>(row[k]) * p.ldc + nn) * esz) =
-                    x[k];
+            if (v < ROWS) {
+                char* dst = static_cast<char*>(p.C) + (static_cast<int64_t>(row[k]) * p.ldc + nn) * esz;
+                if (p.mc) multimem_st16(dst, x[k]);
+                else *reinterpret_cast<int4*>(dst) = x[k];
+            }
         }
         // further destinations (fused all-gather): the same rows again, read
         // back from the staged tile so the common path keeps its registers

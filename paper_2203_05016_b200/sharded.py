@@ -14,6 +14,11 @@ map (-1 for padding rows).
 ``ShardPlan`` is pure host logic (tested with gloo on CPU);
 ``ShardedSpMM`` binds it to the CUDA kernels.
 
+Multicast variant (``ShardedSpMM.full_multicast``, ``MulticastOutputs``):
+the same epilogue stores go once through an NVLS multicast address bound to
+every rank's output (torch symmetric memory), so each row chunk is one
+multimem.st instead of P P2P stores.
+
 Fused all-gather (``ShardedSpMM.full_fused``): every rank holds a full-size
 output buffer; the buffers are shared through CUDA IPC once
 (``PeerOutputs``), and ``shflbw_cu_spmm_groups_peers`` stores each finished
@@ -166,3 +171,44 @@ def _full_fused(self, b: torch.Tensor, outputs: PeerOutputs) -> torch.Tensor:
 
 
 ShardedSpMM.full_fused = _full_fused
+
+
+class MulticastOutputs:
+    """A full-size [M, N] output on every rank in torch symmetric memory, with
+    the NVLS multicast address bound to all ranks' buffers (``mc_ptr``; 0 when
+    the GPUs / driver offer no multicast, e.g. without NVSwitch).  Stores
+    through ``mc_ptr`` land in every rank's ``buf``."""
+
+    def __init__(self, shape, dtype, group=None, device=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.buf = symm_mem.empty(*shape, dtype=dtype, device=dev)
+        self.buf.zero_()
+        self.handle = symm_mem.rendezvous(self.buf, group or dist.group.WORLD)
+        self.mc_ptr = int(getattr(self.handle, "multicast_ptr", 0) or 0)
+        # the multicast address maps the buffer's allocation; this tensor may
+        # sit at an offset inside it
+        self.mc_offset = int(getattr(self.handle, "buffer_offset", 0) or 0) if self.mc_ptr else 0
+
+
+def _full_multicast(self, b: torch.Tensor, outputs: MulticastOutputs) -> torch.Tensor:
+    """This rank's groups, each row stored ONCE through the NVLS multicast
+    address into every rank's full output buffer (one multimem.st per 16
+    bytes, replicated by the switch); returns this rank's buffer once all
+    ranks' kernels are complete."""
+    import torch.distributed as dist
+    if not outputs.mc_ptr:
+        raise RuntimeError("no NVLS multicast address (MulticastOutputs.mc_ptr == 0)")
+    if self.plan.world > 1:
+        torch.cuda.current_stream().synchronize()  # readers of the previous result are done
+        dist.barrier(group=self.group)
+    self.sb.spmm_groups_multicast(self.a, self.g0, self.g1, b, outputs.mc_ptr + outputs.mc_offset,
+                                  outputs.buf.dtype, outputs.buf.stride(0))
+    torch.cuda.current_stream().synchronize()
+    if self.plan.world > 1:
+        dist.barrier(group=self.group)  # all ranks' rows have landed everywhere
+    return outputs.buf
+
+
+ShardedSpMM.full_multicast = _full_multicast

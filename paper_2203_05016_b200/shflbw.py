@@ -513,6 +513,17 @@ def spmm_groups_peers(a: ShflBWMatrix, g_begin: int, g_end: int, b: torch.Tensor
                                               b.stride(0), ptrs, len(outs), _dt(dtype), ldc, _stream()))
 
 
+def spmm_groups_multicast(a: ShflBWMatrix, g_begin: int, g_end: int, b: torch.Tensor, mc_ptr: int,
+                          dtype: torch.dtype, ldc: int) -> None:
+    """One shard's groups with the all-gather through NVLS multicast: every
+    finished row is stored once at its row_indices position through
+    `mc_ptr`, a multicast address bound to all ranks' full outputs
+    (shflbw_cu_spmm_groups_multicast)."""
+    b = _check_b(a, b)
+    _check(_lib().shflbw_cu_spmm_groups_multicast(a.ptr, g_begin, g_end, b.data_ptr(), b.shape[0], b.shape[1],
+                                                  b.stride(0), int(mc_ptr), _dt(dtype), ldc, _stream()))
+
+
 def unpermute_rows(row_indices_ptr: int, c_perm: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
     _check(_lib().shflbw_cu_unpermute_rows(row_indices_ptr, c_perm.shape[0], c_perm.shape[1],
                                            c_perm.data_ptr(), c_perm.stride(0), out.data_ptr(), out.stride(0),

@@ -147,3 +147,58 @@ def test_fused_allgather_two_processes_one_gpu():
     for p in ps:
         p.join(timeout=60)
     assert res == {0: True, 1: True}, res
+
+
+def _multicast_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    try:
+        import paper_2203_05016_b200 as sb
+        from paper_2203_05016_b200.sharded import MulticastOutputs, ShardedSpMM
+        g = torch.Generator().manual_seed(9)
+        M, K, N, V = 1024, 512, 384, 64
+        mask = torch.zeros((M, K), dtype=torch.uint8)
+        for grp in range(M // V):
+            mask[grp * V:(grp + 1) * V, torch.randperm(K, generator=g)[:K // 4]] = 1
+        mask = mask[torch.randperm(M, generator=g)]
+        W = (torch.rand((M, K), generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+        B = (torch.rand((K, N), generator=g) * 2 - 1).to(torch.bfloat16).cuda()
+        a = sb.compress_shflbw(W, mask.cuda(), V)
+        want = sb.spmm_execute(a, B, out_dtype=torch.bfloat16)
+        try:
+            outs = MulticastOutputs((M, N), torch.bfloat16)
+        except Exception as e:  # symmetric memory / multicast unavailable here
+            q.put((rank, f"skip: {e!r}"))
+            return
+        if not outs.mc_ptr:
+            q.put((rank, "skip: no multicast address (multicast_ptr == 0)"))
+            return
+        sh = ShardedSpMM(a, rank, world)
+        got = sh.full_multicast(B, outs)
+        ok = bool(torch.equal(got, want))
+        got2 = sh.full_multicast(B, outs)  # again into the same buffers
+        q.put((rank, ok and bool(torch.equal(got2, want)) and sb.last_plan().startswith("k_spmm")))
+    except Exception as e:
+        q.put((rank, f"error: {e!r}"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_multicast_allgather_one_rank():
+    """The NVLS multicast epilogue (multimem.st through torch symmetric
+    memory's multicast address) with one rank: every row lands in the
+    rank's own buffer exactly as spmm_execute writes it.  Skipped when the
+    box offers no multicast object."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_multicast_worker, args=(0, 1, free_port(), q))
+    p.start()
+    rank, res = q.get(timeout=240)
+    p.join(timeout=60)
+    if isinstance(res, str) and res.startswith("skip"):
+        pytest.skip(res)
+    assert res is True, res
