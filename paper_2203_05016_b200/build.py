@@ -75,6 +75,11 @@ def build(force: bool = False, verbose: bool = True) -> str:
         NVCC_FLAGS.append("-DSBW_TRACE")
         OBJ = os.path.join(PKG, "build_trace")
         LIB = os.path.join(ROOT, "abl", "trace.so")
+    elif os.environ.get("SBW_VARIANT"):  # development A/B build: -D<variant>, abl/<variant>.so
+        v = os.environ["SBW_VARIANT"]
+        NVCC_FLAGS.append(f"-D{v}")
+        OBJ = os.path.join(PKG, f"build_{v}")
+        LIB = os.path.join(ROOT, "abl", f"{v}.so")
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))

@@ -199,11 +199,12 @@ __device__ __forceinline__ void tc_fence_after() {
 // D[tmem] (+)= A[smem desc] * B[smem desc], kind::f16, one CTA.
 // 16-byte store through an NVLS multicast address: one store, replicated by
 // the switch into every GPU bound to the multicast object
+// (no memory clobber: like the plain 16-byte stores it replaces, it must not
+// stop the compiler from starting the next row's shared-memory reads early)
 __device__ __forceinline__ void multimem_st16(void* addr, int4 x) {
     asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr),
                  "f"(__int_as_float(x.x)), "f"(__int_as_float(x.y)), "f"(__int_as_float(x.z)),
-                 "f"(__int_as_float(x.w))
-                 : "memory");
+                 "f"(__int_as_float(x.w)));
 }
 
 // One lane of a converged warp (elect.sync): lets warp-uniform code issue a

@@ -178,6 +178,24 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
     // a 16-byte chunk never spans two positions; chunks past a half-width unit are dead
     const int64_t nn = chunk * (16 / esz) < p.tile_n ? out_col(p, n0 + chunk * (16 / esz)) : -1;
     const int v0 = q * kRowsPerInst + lane / kLanesPerRow;
+    if (!BATCH && p.mc) {  // interleaved, NVLS multicast address
+        if (nn >= 0) {
+            const uint32_t cb = smem_u32(ctile);
+            const uint32_t rbase = smem_u32(rows);
+#pragma unroll 4
+            for (int v = v0; v < ROWS; v += 4 * kRowsPerInst) {
+                int4 x;
+                int32_t row;
+                const int pc = SWZ ? (chunk ^ (v & 7)) : chunk;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w)
+                             : "r"(cb + static_cast<uint32_t>(v * kBlockN * esz + pc * 16)));
+                asm volatile("ld.shared.b32 %0, [%1];" : "=r"(row) : "r"(rbase + static_cast<uint32_t>(v * 4)));
+                multimem_st16(static_cast<char*>(p.C) + (static_cast<int64_t>(row) * p.ldc + nn) * esz, x);
+            }
+        }
+        return;
+    }
     if (!BATCH) {  // interleaved: fewer live registers (the persistent kernel's epilogue warps)
         if (nn >= 0) {
             // explicit ld.shared, volatile so it stays after the bar.sync above
@@ -195,8 +213,7 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
                              : "r"(cb + static_cast<uint32_t>(v * kBlockN * esz + pc * 16)));
                 asm volatile("ld.shared.b32 %0, [%1];" : "=r"(row) : "r"(rbase + static_cast<uint32_t>(v * 4)));
                 const int64_t off = (static_cast<int64_t>(row) * p.ldc + nn) * esz;
-                if (p.mc) multimem_st16(static_cast<char*>(p.C) + off, x);
-                else *reinterpret_cast<int4*>(static_cast<char*>(p.C) + off) = x;
+                *reinterpret_cast<int4*>(static_cast<char*>(p.C) + off) = x;
                 for (int d = 0; d < p.n_extra; ++d) *reinterpret_cast<int4*>(static_cast<char*>(p.C_extra[d]) + off) = x;
             }
         }
@@ -219,13 +236,20 @@ __device__ __forceinline__ void store_tile_rows(const TcParams& p, const unsigne
                 row[k] = rows[v];
             }
         }
+        if (!p.mc) {
 #pragma unroll
-        for (int k = 0; k < kIters; ++k) {
-            const int v = v0 + k * 4 * kRowsPerInst;
-            if (v < ROWS) {
-                char* dst = static_cast<char*>(p.C) + (static_cast<int64_t>(row[k]) * p.ldc + nn) * esz;
-                if (p.mc) multimem_st16(dst, x[k]);
-                else *reinterpret_cast<int4*>(dst) = x[k];
+            for (int k = 0; k < kIters; ++k) {
+                const int v = v0 + k * 4 * kRowsPerInst;
+                if (v < ROWS)
+                    *reinterpret_cast<int4*>(static_cast<char*>(p.C) +
+                                             (static_cast<int64_t>(row[k]) * p.ldc + nn) * esz) = x[k];
+            }
+        } else {  // NVLS multicast address: the same stores as multimem.st
+#pragma unroll
+            for (int k = 0; k < kIters; ++k) {
+                const int v = v0 + k * 4 * kRowsPerInst;
+                if (v < ROWS)
+                    multimem_st16(static_cast<char*>(p.C) + (static_cast<int64_t>(row[k]) * p.ldc + nn) * esz, x[k]);
             }
         }
         // further destinations (fused all-gather): the same rows again, read
@@ -308,7 +332,8 @@ __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row,
         if (p.bulk_out) {
             stage_tile_stmatrix<OT, VS>(t_row, nkb, q, lane, ctile);
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            store_tile_rows<OT, VS, true, true>(p, ctile, rows_s, q, lane, n0);
+            // (VS = 128: the interleaved loop -- 16 staged chunks + rows in registers would spill)
+            store_tile_rows<OT, VS, (VS <= 64), true>(p, ctile, rows_s, q, lane, n0);
             return;
         }
     }
@@ -339,7 +364,8 @@ __device__ __forceinline__ void epilogue_rows(const TcParams& p, uint32_t t_row,
     }
     if (p.bulk_out) {
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        store_tile_rows<OT, VS>(p, ctile, rows_s, q, lane, n0);
+        // batched loads only while they fit in registers (<= 16 chunks per thread)
+        store_tile_rows<OT, VS, (VS * sizeof(OT) <= 128)>(p, ctile, rows_s, q, lane, n0);
     }
 }
 
@@ -709,97 +735,101 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
         const uint32_t meta_u32 = smem_u32(meta_s);
-        int s = 0;
-        uint32_t ph = 0;
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int win = kb % kMetaBlocks;
-            if (win == 0 && kb > 0) {
-                named_bar<kGT>(2);  // all done with the old window
-                stage_meta(kb);
-                named_bar<kGT>(2);
-            }
-            if (kb >= stages) mbar_wait(&empty[s], ph ^ 1);
-            if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
-            unsigned char* a_st = smem + s * kStageBytes;
-            const int32_t* mk = meta_s + win * kBlockK;
-            // block-wise K block: its 64 (ascending) columns are c0..c0+63
-            int c0 = -1;
-            if constexpr (KIND == 0 && !mcast) {
-                if (p.tiles) {
+        // the K loop, instantiated with and without the block-wise tile path
+        // (even an untaken per-block check cost 2-5 % in the gather-bound loop)
+        auto producer_loop = [&]<bool TILES>() {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int win = kb % kMetaBlocks;
+                if (win == 0 && kb > 0) {
+                    named_bar<kGT>(2);  // all done with the old window
+                    stage_meta(kb);
+                    named_bar<kGT>(2);
+                }
+                if (kb >= stages) mbar_wait(&empty[s], ph ^ 1);
+                if (et == 0 && kb < 8) trace_event(p.trace, 16 + kb);
+                unsigned char* a_st = smem + s * kStageBytes;
+                const int32_t* mk = meta_s + win * kBlockK;
+                // block-wise K block: its 64 (ascending) columns are c0..c0+63
+                int c0 = -1;
+                if constexpr (TILES) {
                     const int first = mk[0], last = mk[kBlockK - 1];
                     if (first >= 0 && last - first == kBlockK - 1) c0 = first;
                 }
-            }
-            if (c0 >= 0) {
-                // B rows c0..c0+63 of each 64-column slab: one 2D TMA tile per
-                // slab into the same swizzled layout the gathers produce
-                if (gw == 0 && elect_one_sync())
-                    for (int bb = 0; bb < nblk; ++bb) tma_load_2d(a_st + bb * blk_bytes, &tmBt, &full[s], n0 + bb * 64, c0);
-            } else if (KIND == 0 && p.issue1) {
-                // SpMM, option "gather_issue" 1: this warp's gathers for the
-                // stage issued back to back by one elected lane, all index
-                // loads first (the per-lane issue compiles to a serialised
-                // ELECT / R2UR.BROADCAST loop per gather)
-                if (elect_one_sync()) {
-                    int4 ci[8];
-                    const uint32_t mrow = meta_u32 + static_cast<uint32_t>(win * kBlockK * 4);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int rg = gw * kRGW + j % kRGW;
-                        if (j < per_warp)
-                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                         : "=r"(ci[j].x), "=r"(ci[j].y), "=r"(ci[j].z), "=r"(ci[j].w)
-                                         : "r"(mrow + static_cast<uint32_t>(rg * 16)));
+                if (TILES && c0 >= 0) {
+                    // B rows c0..c0+63 of each 64-column slab: one 2D TMA tile per
+                    // slab into the same swizzled layout the gathers produce
+                    if (gw == 0 && elect_one_sync())
+                        for (int bb = 0; bb < nblk; ++bb) tma_load_2d(a_st + bb * blk_bytes, &tmBt, &full[s], n0 + bb * 64, c0);
+                } else if (KIND == 0 && p.issue1) {
+                    // SpMM, option "gather_issue" 1: this warp's gathers for the
+                    // stage issued back to back by one elected lane, all index
+                    // loads first (the per-lane issue compiles to a serialised
+                    // ELECT / R2UR.BROADCAST loop per gather)
+                    if (elect_one_sync()) {
+                        int4 ci[8];
+                        const uint32_t mrow = meta_u32 + static_cast<uint32_t>(win * kBlockK * 4);
+    #pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int rg = gw * kRGW + j % kRGW;
+                            if (j < per_warp)
+                                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                             : "=r"(ci[j].x), "=r"(ci[j].y), "=r"(ci[j].z), "=r"(ci[j].w)
+                                             : "r"(mrow + static_cast<uint32_t>(rg * 16)));
+                        }
+    #pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int jg = gw * per_warp + j;
+                            if (j >= per_warp || (mcast && (jg % VSF) != vr)) continue;
+                            const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
+                            void* dst = a_st + bb * blk_bytes + rg * (4 * 64 * 2);
+                            if constexpr (!mcast)
+                                tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                            else
+                                tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
+                                               ci[j].w);
+                        }
                     }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int jg = gw * per_warp + j;
-                        if (j >= per_warp || (mcast && (jg % VSF) != vr)) continue;
-                        const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
-                        void* dst = a_st + bb * blk_bytes + rg * (4 * 64 * 2);
-                        if constexpr (!mcast)
-                            tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
-                        else
-                            tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
-                                           ci[j].w);
+                } else if (t_issue) {
+                    int4 ci;  // explicit ld.shared (a generic load would take the slower generic path)
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
+                                 : "r"(meta_u32 + static_cast<uint32_t>((win * kBlockK + g_rg * 4) * 4)));
+                    int x = g_x;
+                    if (KIND == 1) {
+                        ci.x = conv_row_enc(p, ci.x, g_p0, g_q0, g_pos_ok);
+                        ci.y = conv_row_enc(p, ci.y, g_p0, g_q0, g_pos_ok);
+                        ci.z = conv_row_enc(p, ci.z, g_p0, g_q0, g_pos_ok);
+                        ci.w = conv_row_enc(p, ci.w, g_p0, g_q0, g_pos_ok);
+                    } else if (KIND == 2) {
+                        x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
                     }
+                    void* dst = a_st + g_b * blk_bytes + g_rg * (4 * p.bw * 2);
+                    if constexpr (!mcast)
+                        tma_gather4(dst, &tmB, &full[s], x, ci.x, ci.y, ci.z, ci.w);
+                    else
+                        tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci.x, ci.y, ci.z, ci.w);
                 }
-            } else if (t_issue) {
-                int4 ci;  // explicit ld.shared (a generic load would take the slower generic path)
-                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                             : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
-                             : "r"(meta_u32 + static_cast<uint32_t>((win * kBlockK + g_rg * 4) * 4)));
-                int x = g_x;
-                if (KIND == 1) {
-                    ci.x = conv_row_enc(p, ci.x, g_p0, g_q0, g_pos_ok);
-                    ci.y = conv_row_enc(p, ci.y, g_p0, g_q0, g_pos_ok);
-                    ci.z = conv_row_enc(p, ci.z, g_p0, g_q0, g_pos_ok);
-                    ci.w = conv_row_enc(p, ci.w, g_p0, g_q0, g_pos_ok);
-                } else if (KIND == 2) {
-                    x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
+                if (cps > 0) {
+                    const uint32_t a_u32 = smem_u32(a_st);
+                    for (int id = et; id < cps * 512; id += kGT) {
+                        const int r = id >> cpr_log2, c = id & ((1 << cpr_log2) - 1);
+                        const int sl = tma_slabs + (c >> 3), cc = c & 7;
+                        const int col = mk[r];
+                        const int n = n0 + sl * 64 + cc * 8;
+                        const bool ok = col >= 0 && n < p.N;
+                        const T* src = ok ? Bp + static_cast<int64_t>(col) * p.ldb + n : Bp;
+                        cp_async16(a_u32 + sl * (kABytes / 2) + r * 128 + ((cc ^ (r & 7)) << 4), src, ok);
+                    }
+                    cp_async_arrive_noinc(&full[s]);
                 }
-                void* dst = a_st + g_b * blk_bytes + g_rg * (4 * p.bw * 2);
-                if constexpr (!mcast)
-                    tma_gather4(dst, &tmB, &full[s], x, ci.x, ci.y, ci.z, ci.w);
-                else
-                    tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci.x, ci.y, ci.z, ci.w);
+                __syncwarp();
+                if (++s == stages) s = 0, ph ^= 1;
             }
-            if (cps > 0) {
-                const uint32_t a_u32 = smem_u32(a_st);
-                for (int id = et; id < cps * 512; id += kGT) {
-                    const int r = id >> cpr_log2, c = id & ((1 << cpr_log2) - 1);
-                    const int sl = tma_slabs + (c >> 3), cc = c & 7;
-                    const int col = mk[r];
-                    const int n = n0 + sl * 64 + cc * 8;
-                    const bool ok = col >= 0 && n < p.N;
-                    const T* src = ok ? Bp + static_cast<int64_t>(col) * p.ldb + n : Bp;
-                    cp_async16(a_u32 + sl * (kABytes / 2) + r * 128 + ((cc ^ (r & 7)) << 4), src, ok);
-                }
-                cp_async_arrive_noinc(&full[s]);
-            }
-            __syncwarp();
-            if (++s == stages) s = 0, ph ^= 1;
-        }
+        };
+        if (KIND == 0 && !mcast && p.tiles) producer_loop.template operator()<true>();
+        else producer_loop.template operator()<false>();
         if (gw < 4) {  // warps 2-5 run the epilogue; any further gather warps are done
             // output row map for the epilogue, loaded while the MMAs run
             for (int v = et; v < VS; v += 128) {
@@ -1122,112 +1152,115 @@ __global__ void __launch_bounds__(192 + 32 * GW, 2)
         named_bar<kGT>(2);
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
-        int kbg = 0, i = 0, s = 0, buf = 0;
-        uint32_t ph = 0;
-        for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
-            if (et == 0 && i < 8) trace_event(p.trace, 16 + i);  // gathers: unit i starts issuing
-            UnitCursor cn = c;
-            cn.next();
-            const bool more = cn.u < units;
-            const int nkb = group_nkb(c.gl);
-            // the next unit reads the same single window (same group, <= kMetaBlocks
-            // K blocks, e.g. every unit of a one-group conv): keep it, no reload/sync
-            const bool keep = more && cn.gl == c.gl && nkb <= kMetaBlocks;
-            if (more && !keep) {  // the other buffer was released by the bar.sync ending unit i-1
-                load_window(cn.gl, 0, buf ^ 1, true);
-                cp_async_commit();
-            }
-            const int n0 = c.tile * kBlockN;
-            const int32_t* mbuf = meta_s + buf * kMetaBlocks * kBlockK;
-            int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
-            bool g_pos_ok = true;
-            if (KIND == 1 || KIND == 2) {
-                const int base_n = n0 + g_b * p.bw;
-                const int pos = ddiv(base_n, p.inv_nb);
-                g_x = base_n - pos * p.Nb;
-                g_pos_ok = pos < p.PQ;
-                const int pr = ddiv(pos, p.inv_qp);
-                g_p0 = pr * p.stride - p.pad;
-                g_q0 = (pos - pr * p.qp) * p.stride - p.pad;
-            }
-            for (int kb = 0; kb < nkb; ++kb, ++kbg) {
-                const int win = kb % kMetaBlocks;
-                if (win == 0 && kb > 0) {  // deep group: later windows of this unit, synchronously
-                    named_bar<kGT>(2);
-                    load_window(c.gl, kb, buf, false);
-                    named_bar<kGT>(2);
+        // the unit loop with and without the block-wise tile path (k_spmm_tc)
+        auto gather_units = [&]<bool TILES>() {
+            int kbg = 0, i = 0, s = 0, buf = 0;
+            uint32_t ph = 0;
+            for (UnitCursor c(cid, nclusters, n_tiles, ngroups, tmaj); c.u < units; c.next(), ++i) {
+                if (et == 0 && i < 8) trace_event(p.trace, 16 + i);  // gathers: unit i starts issuing
+                UnitCursor cn = c;
+                cn.next();
+                const bool more = cn.u < units;
+                const int nkb = group_nkb(c.gl);
+                // the next unit reads the same single window (same group, <= kMetaBlocks
+                // K blocks, e.g. every unit of a one-group conv): keep it, no reload/sync
+                const bool keep = more && cn.gl == c.gl && nkb <= kMetaBlocks;
+                if (more && !keep) {  // the other buffer was released by the bar.sync ending unit i-1
+                    load_window(cn.gl, 0, buf ^ 1, true);
+                    cp_async_commit();
                 }
-                if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
-                int c0 = -1;  // block-wise K block (k_spmm_tc)
-                if constexpr (KIND == 0 && !mcast) {
-                    if (p.tiles) {
+                const int n0 = c.tile * kBlockN;
+                const int32_t* mbuf = meta_s + buf * kMetaBlocks * kBlockK;
+                int g_x = n0 + g_b * 64, g_p0 = 0, g_q0 = 0;
+                bool g_pos_ok = true;
+                if (KIND == 1 || KIND == 2) {
+                    const int base_n = n0 + g_b * p.bw;
+                    const int pos = ddiv(base_n, p.inv_nb);
+                    g_x = base_n - pos * p.Nb;
+                    g_pos_ok = pos < p.PQ;
+                    const int pr = ddiv(pos, p.inv_qp);
+                    g_p0 = pr * p.stride - p.pad;
+                    g_q0 = (pos - pr * p.qp) * p.stride - p.pad;
+                }
+                for (int kb = 0; kb < nkb; ++kb, ++kbg) {
+                    const int win = kb % kMetaBlocks;
+                    if (win == 0 && kb > 0) {  // deep group: later windows of this unit, synchronously
+                        named_bar<kGT>(2);
+                        load_window(c.gl, kb, buf, false);
+                        named_bar<kGT>(2);
+                    }
+                    if (kbg >= stages) mbar_wait(&empty[s], ph ^ 1);
+                    int c0 = -1;  // block-wise K block (k_spmm_tc)
+                    if constexpr (TILES) {
                         const int first = mbuf[win * kBlockK], last = mbuf[win * kBlockK + kBlockK - 1];
                         if (first >= 0 && last - first == kBlockK - 1) c0 = first;
                     }
-                }
-                if (c0 >= 0) {
-                    if (gw == 0 && elect_one_sync())
-                        for (int bb = 0; bb < nblk; ++bb)
-                            tma_load_2d(smem + s * kStageBytes + bb * blk_bytes, &tmBt, &full[s], n0 + bb * 64, c0);
-                } else if (KIND == 0 && p.issue1) {
-                    // SpMM: one elected lane per warp issues the warp's
-                    // gathers back to back, index loads first (k_spmm_tc)
-                    if (elect_one_sync()) {
-                        int4 ci[8];
-                        const uint32_t mrow = smem_u32(mbuf) + static_cast<uint32_t>(win * kBlockK * 4);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const int rg = gw * kRGW + j % kRGW;
-                            if (j < per_warp)
-                                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                             : "=r"(ci[j].x), "=r"(ci[j].y), "=r"(ci[j].z), "=r"(ci[j].w)
-                                             : "r"(mrow + static_cast<uint32_t>(rg * 16)));
+                    if (TILES && c0 >= 0) {
+                        if (gw == 0 && elect_one_sync())
+                            for (int bb = 0; bb < nblk; ++bb)
+                                tma_load_2d(smem + s * kStageBytes + bb * blk_bytes, &tmBt, &full[s], n0 + bb * 64, c0);
+                    } else if (KIND == 0 && p.issue1) {
+                        // SpMM: one elected lane per warp issues the warp's
+                        // gathers back to back, index loads first (k_spmm_tc)
+                        if (elect_one_sync()) {
+                            int4 ci[8];
+                            const uint32_t mrow = smem_u32(mbuf) + static_cast<uint32_t>(win * kBlockK * 4);
+    #pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const int rg = gw * kRGW + j % kRGW;
+                                if (j < per_warp)
+                                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                                 : "=r"(ci[j].x), "=r"(ci[j].y), "=r"(ci[j].z), "=r"(ci[j].w)
+                                                 : "r"(mrow + static_cast<uint32_t>(rg * 16)));
+                            }
+    #pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                const int jg = gw * per_warp + j;
+                                if (j >= per_warp || (mcast && (jg % CS) != static_cast<int>(rank))) continue;
+                                const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
+                                void* dst = smem + s * kStageBytes + bb * blk_bytes + rg * (4 * 64 * 2);
+                                if constexpr (!mcast)
+                                    tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
+                                else
+                                    tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
+                                                   ci[j].w);
+                            }
                         }
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const int jg = gw * per_warp + j;
-                            if (j >= per_warp || (mcast && (jg % CS) != static_cast<int>(rank))) continue;
-                            const int rg = gw * kRGW + j % kRGW, bb = j / kRGW;
-                            void* dst = smem + s * kStageBytes + bb * blk_bytes + rg * (4 * 64 * 2);
-                            if constexpr (!mcast)
-                                tma_gather4(dst, &tmB, &full[s], n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z, ci[j].w);
-                            else
-                                tma_gather4_mc(dst, &tmB, &full[s], cmask, n0 + bb * 64, ci[j].x, ci[j].y, ci[j].z,
-                                               ci[j].w);
+                    } else if (t_issue) {
+                        int4 ci;
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
+                                     : "r"(smem_u32(mbuf) + static_cast<uint32_t>((win * kBlockK + g_rg * 4) * 4)));
+                        int x = g_x;
+                        if (KIND == 2) x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
+                        if (KIND == 1) {
+                            ci.x = conv_row_enc(p, ci.x, g_p0, g_q0, g_pos_ok);
+                            ci.y = conv_row_enc(p, ci.y, g_p0, g_q0, g_pos_ok);
+                            ci.z = conv_row_enc(p, ci.z, g_p0, g_q0, g_pos_ok);
+                            ci.w = conv_row_enc(p, ci.w, g_p0, g_q0, g_pos_ok);
                         }
+                        void* dst = smem + s * kStageBytes + g_b * blk_bytes + g_rg * (4 * bw * 2);
+                        if constexpr (!mcast)
+                            tma_gather4(dst, &tmB, &full[s], x, ci.x, ci.y, ci.z, ci.w);
+                        else
+                            tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci.x, ci.y, ci.z, ci.w);
                     }
-                } else if (t_issue) {
-                    int4 ci;
-                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
-                                 : "r"(smem_u32(mbuf) + static_cast<uint32_t>((win * kBlockK + g_rg * 4) * 4)));
-                    int x = g_x;
-                    if (KIND == 2) x = conv_wide_rows(p, ci, g_p0, g_q0, g_pos_ok);
-                    if (KIND == 1) {
-                        ci.x = conv_row_enc(p, ci.x, g_p0, g_q0, g_pos_ok);
-                        ci.y = conv_row_enc(p, ci.y, g_p0, g_q0, g_pos_ok);
-                        ci.z = conv_row_enc(p, ci.z, g_p0, g_q0, g_pos_ok);
-                        ci.w = conv_row_enc(p, ci.w, g_p0, g_q0, g_pos_ok);
+                    __syncwarp();
+                    if (++s == stages) s = 0, ph ^= 1;
+                }
+                if (!keep) {
+                    cp_async_wait<0>();
+                    named_bar<kGT>(2);  // next unit's window visible; this buffer free
+                    if (KIND != 0 && more) {
+                        encode_window(cn.gl, buf ^ 1);
+                        named_bar<kGT>(2);
                     }
-                    void* dst = smem + s * kStageBytes + g_b * blk_bytes + g_rg * (4 * bw * 2);
-                    if constexpr (!mcast)
-                        tma_gather4(dst, &tmB, &full[s], x, ci.x, ci.y, ci.z, ci.w);
-                    else
-                        tma_gather4_mc(dst, &tmB, &full[s], cmask, x, ci.x, ci.y, ci.z, ci.w);
+                    buf ^= 1;
                 }
-                __syncwarp();
-                if (++s == stages) s = 0, ph ^= 1;
             }
-            if (!keep) {
-                cp_async_wait<0>();
-                named_bar<kGT>(2);  // next unit's window visible; this buffer free
-                if (KIND != 0 && more) {
-                    encode_window(cn.gl, buf ^ 1);
-                    named_bar<kGT>(2);
-                }
-                buf ^= 1;
-            }
-        }
+        };
+        if (KIND == 0 && !mcast && p.tiles) gather_units.template operator()<true>();
+        else gather_units.template operator()<false>();
     } else {
         // ---------------- epilogue ----------------
         const int q = warp & 3, m = q * 32 + lane, et = threadIdx.x - (64 + 32 * GW);
