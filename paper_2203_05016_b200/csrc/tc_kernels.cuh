@@ -923,11 +923,12 @@ struct UnitCursor {
 };
 
 
-// Rows of the persistent kernel's staged output tile: 16-bit outputs are
-// staged and stored 32 rows at a time (an 8 KB tile instead of VS x 128 x 2:
-// the freed shared memory buys a fourth pipeline stage at 2 CTAs per SM).
+// Rows of the persistent kernel's staged output tile (all VS rows: staging
+// 32 rows at a time saved 8 KB but bought no extra pipeline stage and slowed
+// the epilogue-bound shapes, ResNet 1x1 @56 6.3 -> 6.8 us)
 __host__ __device__ constexpr int persist_tile_rows(int vs, int out_esz) {
-    return (out_esz == 2 && vs % 32 == 0) ? 32 : vs;
+    (void)out_esz;
+    return vs;
 }
 
 template <class OT, int VS>
@@ -936,20 +937,13 @@ __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc,
                                               uint64_t* acc_empty) {
     if constexpr (sizeof(OT) == 2 && VS % 32 == 0) {
         if (p.bulk_out) {
-            // 32 output rows at a time through an 8 KB staged tile
-#pragma unroll
-            for (int c0 = 0; c0 < VS; c0 += 32) {
-                if (c0 > 0) asm volatile("bar.sync 3, 128;" ::: "memory");  // previous rows stored
-                stage_tile_stmatrix<OT, 32>(t_acc + c0, nkb, q, lane, ctile);
-                if (c0 + 32 >= VS) {
-                    // accumulator drained: the MMA warp may start the next unit in it
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(acc_empty);
-                }
-                asm volatile("bar.sync 3, 128;" ::: "memory");
-                store_tile_rows<OT, 32, false, true>(p, ctile, rows_s + c0, q, lane, n0);
-            }
+            stage_tile_stmatrix<OT, VS>(t_acc, nkb, q, lane, ctile);
+            // accumulator drained: the MMA warp may start the next unit in it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty);
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            store_tile_rows<OT, VS, false, true>(p, ctile, rows_s, q, lane, n0);
             return;
         }
     }

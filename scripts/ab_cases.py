@@ -36,6 +36,8 @@ cases = {
     "conv28": lambda: sweep.conv_row("conv28", 128, 28, 128, 3, 1, 32, 64, 0.25, 300, dev),
     "conv14": lambda: sweep.conv_row("conv14", 256, 14, 256, 3, 1, 32, 64, 0.25, 300, dev),
     "conv7": lambda: sweep.conv_row("conv7", 512, 7, 512, 3, 1, 32, 64, 0.25, 300, dev),
+    "c1x1_56": lambda: sweep.conv_row("c1x1_56", 256, 56, 64, 1, 0, 32, 64, 0.25, 300, dev),
+    "c1x1_14": lambda: sweep.conv_row("c1x1_14", 1024, 14, 256, 1, 0, 32, 64, 0.25, 300, dev),
 }
 out = {}
 for k in only:
