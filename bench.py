@@ -190,8 +190,52 @@ class ClockSampler:
 
 def graph_time(torch, step_fn, steps, warmup, soak_s, barrier):
     """Run `steps` steps (step_fn(i) enqueues step i) as CUDA-graph replays.
-    Returns (elapsed_ms over the K timed steps, t0, t1 host stamps)."""
+    Returns (elapsed_ms over the K timed steps, t0, t1 host stamps).
+
+    K <= 1000: ONE graph holds min(W, 32) untimed lead-in steps, a timing
+    event, the K steps and a second event (external events recorded inside
+    the graph), so the K steps are timed back to back on the device with the
+    graph-launch latency and the pipeline fill outside the window (at K = 20
+    those added ~0.4 us per step).  Larger K: replays of 500-step graphs."""
     stream = torch.cuda.Stream()
+    if steps <= 1000:
+        side = torch.cuda.Stream()
+        lead = max(1, min(warmup, 32))
+        with torch.cuda.stream(stream):
+            for i in range(3):  # eager warm-up (module loads, cuBLAS workspaces)
+                step_fn(i)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True, external=True)
+        e1 = torch.cuda.Event(enable_timing=True, external=True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(lead):
+                step_fn(steps + i)  # lead-in: the sets after the timed ones (round-robin)
+            # e0 hangs off the last lead-in step on a side branch, so the timed
+            # chain keeps its kernel-to-kernel (PDL) edge; an event node in the
+            # chain itself added ~4-8 us of dependency latency per window
+            side.wait_stream(stream)
+            e0.record(side)
+            for i in range(steps):
+                step_fn(i)
+            e1.record(stream)
+            stream.wait_stream(side)
+        with torch.cuda.stream(stream):
+            for _ in range(max(1, math.ceil(warmup / (steps + lead)))):
+                g.replay()
+            torch.cuda.synchronize()
+            t_soak = time.perf_counter()
+            while time.perf_counter() - t_soak < soak_s:  # settle clocks
+                g.replay()
+                torch.cuda.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g.replay()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            barrier()
+        return e0.elapsed_time(e1), t0, t1
     per = max(1, min(steps, 500))
     with torch.cuda.stream(stream):
         for i in range(3):  # eager warm-up (module loads, cuBLAS workspaces)
@@ -368,8 +412,7 @@ def run_reference_arm(args, wl, world, rank):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": steps, "warmup": warm, "ms_per_step": el / steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl["desc"], "M": wl["M"], "N": wl["N"], "K": wl["K"], "V": wl["V"],
-                       "sparsity": 1 - wl["alpha"]},
+            "config": workload_config(wl, args.gpus),
             "ms_per_call": el / (steps * reps) * 1e3,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": c.cores, "kind": c.kind, "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -381,6 +424,26 @@ def run_reference_arm(args, wl, world, rank):
 # our arm
 # --------------------------------------------------------------------------
 
+def rotation(wl):
+    """(padded kept columns, bytes of one input set, number of rotating sets)."""
+    M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
+    kpad = (int(round(wl["alpha"] * K)) + 63) // 64 * 64
+    set_bytes = 2 * M * kpad + 4 * (M // V) * kpad + 4 * M + 2 * K * N + 2 * M * N
+    n = 1 if set_bytes > L2_BYTES else min(64, max(2, math.ceil(1.25 * L2_BYTES / set_bytes)))
+    return kpad, set_bytes, n
+
+
+def workload_config(wl, world):
+    """The `config` object, identical on both arms (the driver compares them)."""
+    M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
+    _, set_bytes, nsets = rotation(wl)
+    return {"workload": wl["desc"], "M": M, "N": N, "K": K, "V": V, "sparsity": 1 - wl["alpha"],
+            "kept_cols_per_group": int(round(wl["alpha"] * K)), "groups": M // V,
+            "parallelism": (f"row-group shards x{world}" if wl["sharded"] else f"replicas x{world}"),
+            "l2": (f"GPU arm: {nsets} rotating input sets x {set_bytes / 2**20:.1f} MiB > 126 MB L2"
+                   if nsets > 1 else "GPU arm: inputs larger than L2")}
+
+
 class RotatingSets:
     """`n` independent (matrix, B, C) sets of one workload, enough that their
     total exceeds L2 (or one set if a single set already does)."""
@@ -389,9 +452,7 @@ class RotatingSets:
         M, N, K, V = wl["M"], wl["N"], wl["K"], wl["V"]
         G = M // V
         cpg = int(round(wl["alpha"] * K))
-        self.kpad = (cpg + 63) // 64 * 64
-        self.set_bytes = 2 * M * self.kpad + 4 * G * self.kpad + 4 * M + 2 * K * N + 2 * M * N
-        n = 1 if self.set_bytes > L2_BYTES else min(64, max(2, math.ceil(1.25 * L2_BYTES / self.set_bytes)))
+        self.kpad, self.set_bytes, n = rotation(wl)
         if profile:
             n = min(n, 4)
         self.n = n
@@ -850,12 +911,11 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": wl["desc"], "M": M, "N": N, "K": K, "V": V, "sparsity": 1 - alpha,
-                       "kept_cols_per_group": cpg, "groups": G, "out_dtype": "bf16", "accum": "fp32",
-                       "parallelism": (f"row-group shards x{world}" if wl["sharded"] else f"replicas x{world}"),
-                       "l2": (f"{nsets} rotating input sets x {set_bytes / 2**20:.1f} MiB > 126 MB L2"
-                              if nsets > 1 else "inputs larger than L2"),
-                       "timing": "CUDA graph replays, CUDA events on the launching stream, max over ranks"},
+            "config": workload_config(wl, world),
+            "out_dtype": "bf16", "accum": "fp32",
+            "timing": ("CUDA graph; CUDA events on the launching stream around exactly the K steps "
+                       "(recorded inside the graph after min(W, 32) lead-in steps when K <= 1000), "
+                       "max over ranks"),
             "plan": plan,
             "speedup_vs_cublas": (value / world / cub["tflops"]) if cub else None,
             "speedup_vs_cublaslt_best": (value / world / lt["tflops"]) if lt and "tflops" in lt else None,
