@@ -54,16 +54,52 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     return x;
 }
 
+// per-word term of a row hash (summed over the row's words): a bijection of
+// the word keyed by (seed, word index) -- two 64-bit multiplies, not two full
+// mix64 rounds (the hash was 60 % of k_pack_rows16's instructions); the row
+// sum is finalised with mix64 before it indexes the class table
 __device__ __forceinline__ uint64_t word_hash(uint64_t word, int w, uint64_t seed) {
-    return mix64(word + mix64(seed ^ (0x9E3779B97F4A7C15ULL * static_cast<uint64_t>(w + 1))));
+    uint64_t x = (word ^ seed) + 0x632BE59BD9B4E019ULL * static_cast<uint64_t>(w + 1);
+    x *= 0x9E3779B97F4A7C15ULL;
+    x ^= x >> 32;
+    x *= 0xD6E8FEB86659FD93ULL;
+    return x ^ (x >> 29);
 }
 
 // flags[0]: mask byte > 1, flags[1]: hash collision, flags[2]: failing class,
 // flags[3]: upload range error
+// Class table (hash planner, M <= kPlanMax): open addressing over P = 2^k >=
+// 2M slots; a row's 64-bit hash claims a slot (atomicCAS), the slot keeps the
+// class's smallest row (atomicMin) and its size (atomicAdd from 0xffffffff).
+// The table is reset by one 0xff memset.  Equal rows always share a slot;
+// rows of different classes sharing one are caught by k_class_check.
+struct ClassTable {
+    uint64_t* key = nullptr;
+    uint32_t* minrow = nullptr;
+    uint32_t* cnt = nullptr;
+    uint32_t* slot = nullptr;  // [M] slot of each row
+    uint32_t mask = 0;
+};
+
+__device__ __forceinline__ void table_insert(const ClassTable& t, uint64_t h, uint32_t r) {
+    h = mix64(h);
+    if (h == ~0ull) h = ~1ull;  // ~0 marks an empty slot
+    uint32_t s = static_cast<uint32_t>(h) & t.mask;
+    for (;;) {
+        const unsigned long long prev =
+            atomicCAS(reinterpret_cast<unsigned long long*>(t.key + s), ~0ull, static_cast<unsigned long long>(h));
+        if (prev == ~0ull || prev == h) break;
+        s = (s + 1) & t.mask;
+    }
+    atomicMin(t.minrow + s, r);
+    atomicAdd(t.cnt + s, 1u);
+    t.slot[r] = s;
+}
+
 __global__ void k_pack_rows(const uint8_t* __restrict__ mask, int M, int K, int W,
                             uint64_t seed, uint64_t* __restrict__ words,
                             int* __restrict__ popc, uint64_t* __restrict__ keys,
-                            uint32_t* __restrict__ vals, uint32_t* __restrict__ flags) {
+                            uint32_t* __restrict__ vals, uint32_t* __restrict__ flags, ClassTable tab) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     if (r >= M) return;
@@ -86,8 +122,12 @@ __global__ void k_pack_rows(const uint8_t* __restrict__ mask, int M, int K, int 
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags[0], 1u);
     if (lane == 0) {
         popc[r] = pc;
-        keys[r] = h;
-        vals[r] = static_cast<uint32_t>(r);
+        if (tab.key) {
+            table_insert(tab, h, static_cast<uint32_t>(r));
+        } else {
+            keys[r] = h;
+            vals[r] = static_cast<uint32_t>(r);
+        }
     }
 }
 
@@ -95,9 +135,9 @@ __global__ void k_pack_rows(const uint8_t* __restrict__ mask, int M, int K, int 
 // warp covers 512 columns per load; lane l's 16 bytes become bits
 // 15..0 of its pattern, four consecutive lanes' patterns one 64-bit word
 // (column 0 = MSB, as k_pack_rows).
-__global__ void k_pack_rows16(const uint8_t* __restrict__ mask, int M, int K, int W, uint64_t seed,
+__global__ void __launch_bounds__(256, 8) k_pack_rows16(const uint8_t* __restrict__ mask, int M, int K, int W, uint64_t seed,
                               uint64_t* __restrict__ words, int* __restrict__ popc, uint64_t* __restrict__ keys,
-                              uint32_t* __restrict__ vals, uint32_t* __restrict__ flags) {
+                              uint32_t* __restrict__ vals, uint32_t* __restrict__ flags, ClassTable tab) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     if (r >= M) return;
@@ -106,32 +146,42 @@ __global__ void k_pack_rows16(const uint8_t* __restrict__ mask, int M, int K, in
     uint64_t h = 0;
     int pc = 0;
     bool bad = false;
-    for (int c0 = 0; c0 < nchunk; c0 += 32) {
-        const int c = c0 + lane;
-        uint32_t pat = 0;
-        if (c < nchunk) {
-            const uint4 q = row[c];
-            const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+    // the row's 16-byte chunks are loaded 4 warp-rounds at a time (2 KB per
+    // warp in flight) before they are decoded: the decode and the shuffles
+    // otherwise expose one load latency per 512 columns
+    constexpr int kBatch = 4;
+    for (int cb = 0; cb < nchunk; cb += 32 * kBatch) {
+        uint4 qb[kBatch];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const uint32_t byte = (w4[i] >> (8 * b)) & 0xffu;
-                    bad |= byte > 1;
-                    pat |= (byte != 0 ? 1u : 0u) << (15 - (i * 4 + b));
-                }
-            }
+        for (int b = 0; b < kBatch; ++b) {
+            const int c = cb + 32 * b + lane;
+            qb[b] = c < nchunk ? __ldcs(row + c) : make_uint4(0, 0, 0, 0);
         }
-        const uint32_t p1 = __shfl_down_sync(0xffffffffu, pat, 1);
-        const uint32_t p2 = __shfl_down_sync(0xffffffffu, pat, 2);
-        const uint32_t p3 = __shfl_down_sync(0xffffffffu, pat, 3);
-        const int w = (c0 + lane) / 4;  // word of lanes 4q..4q+3
-        if ((lane & 3) == 0 && w < W) {
-            const uint64_t word = (static_cast<uint64_t>(pat) << 48) | (static_cast<uint64_t>(p1) << 32) |
-                                  (static_cast<uint64_t>(p2) << 16) | p3;
-            words[static_cast<int64_t>(r) * W + w] = word;
-            pc += __popcll(word);
-            h += word_hash(word, w, seed);
+#pragma unroll
+        for (int b = 0; b < kBatch; ++b) {
+            const int c0 = cb + 32 * b;
+            if (c0 >= nchunk) break;
+            const uint4 q = qb[b];
+            // bytes are 0/1 (anything else is flagged and the mask rejected):
+            // (x & 0x01010101) * 0x08040201 gathers the 4 bytes' low bits into
+            // bits 27..24, first byte (lowest column) highest
+            bad |= ((q.x | q.y | q.z | q.w) & 0xFEFEFEFEu) != 0;
+            const uint32_t n0 = ((q.x & 0x01010101u) * 0x08040201u) >> 24;
+            const uint32_t n1 = ((q.y & 0x01010101u) * 0x08040201u) >> 24;
+            const uint32_t n2 = ((q.z & 0x01010101u) * 0x08040201u) >> 24;
+            const uint32_t n3 = ((q.w & 0x01010101u) * 0x08040201u) >> 24;
+            const uint32_t pat = (n0 << 12) | (n1 << 8) | (n2 << 4) | n3;
+            const uint32_t p1 = __shfl_down_sync(0xffffffffu, pat, 1);
+            const uint32_t p2 = __shfl_down_sync(0xffffffffu, pat, 2);
+            const uint32_t p3 = __shfl_down_sync(0xffffffffu, pat, 3);
+            const int w = (c0 + lane) / 4;  // word of lanes 4q..4q+3
+            if ((lane & 3) == 0 && w < W) {
+                const uint64_t word = (static_cast<uint64_t>(pat) << 48) | (static_cast<uint64_t>(p1) << 32) |
+                                      (static_cast<uint64_t>(p2) << 16) | p3;
+                words[static_cast<int64_t>(r) * W + w] = word;
+                pc += __popcll(word);
+                h += word_hash(word, w, seed);
+            }
         }
     }
 #pragma unroll
@@ -142,8 +192,12 @@ __global__ void k_pack_rows16(const uint8_t* __restrict__ mask, int M, int K, in
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags[0], 1u);
     if (lane == 0) {
         popc[r] = pc;
-        keys[r] = h;
-        vals[r] = static_cast<uint32_t>(r);
+        if (tab.key) {
+            table_insert(tab, h, static_cast<uint32_t>(r));
+        } else {
+            keys[r] = h;
+            vals[r] = static_cast<uint32_t>(r);
+        }
     }
 }
 
@@ -683,6 +737,471 @@ __global__ void k_status(const uint32_t* __restrict__ flags, const uint32_t* __r
     status[3] = *maxp;
 }
 
+// ---- hash planner (M <= kPlanMax): class check, one-CTA plan, fused pack ----
+
+// K2: one warp per row.  rep = the class's smallest row (the table slot's
+// atomicMin); a row whose words differ from its representative's shares a
+// slot with another class (a 64-bit hash collision): flags[1].
+__global__ void k_class_check(const uint64_t* __restrict__ words, int M, int W, ClassTable tab,
+                              uint32_t* __restrict__ rep_out, uint32_t* __restrict__ csize_out,
+                              uint32_t* __restrict__ flags) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (r >= M) return;
+    const uint32_t sl = tab.slot[r];
+    const uint32_t rep = tab.minrow[sl];
+    if (rep != static_cast<uint32_t>(r)) {
+        bool diff = false;
+        const uint64_t* a = words + static_cast<int64_t>(r) * W;
+        const uint64_t* b = words + static_cast<int64_t>(rep) * W;
+        for (int w = lane; w < W; w += 32) diff |= a[w] != b[w];
+        if (__any_sync(0xffffffffu, diff) && lane == 0) atomicOr(&flags[1], 1u);
+    }
+    if (lane == 0) {
+        rep_out[r] = rep;
+        csize_out[r] = tab.cnt[sl] + 1u;
+    }
+}
+
+constexpr int kPlanThreads = 1024;
+constexpr int kPlanMax = 32768;                      // rows: 16-bit row ids in shared memory
+
+// exclusive scan of one int per thread over a 1024-thread block; *total =
+// the block sum (every thread).  `tmp` holds 33 ints.
+__device__ __forceinline__ int block_scan_1024(int x, int* tmp, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) tmp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int v = tmp[lane];
+        int wi = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        tmp[lane] = wi - v;  // exclusive warp offsets
+        if (lane == 31) tmp[32] = wi;
+    }
+    __syncthreads();
+    const int r = tmp[warp] + incl - x;
+    *total = tmp[32];
+    __syncthreads();
+    return r;
+}
+
+// lanes whose `nb`-bit digit d equals this lane's (and whose `valid` agrees):
+// ballots per bit instead of MATCH.ANY, which in k_plan stalled every warp for
+// ~40 SM cycles per call (60 % of the large-FFN plan time)
+__device__ __forceinline__ unsigned match_digit(uint32_t d, int nb, bool valid) {
+    const unsigned vb = __ballot_sync(0xffffffffu, valid);
+    unsigned m = valid ? vb : ~vb;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        if (b < nb) {
+            const bool bit = (d >> b) & 1u;
+            const unsigned bal = __ballot_sync(0xffffffffu, bit);
+            m &= bit ? bal : ~bal;
+        }
+    }
+    return m;
+}
+
+__device__ __noinline__ bool row_less(const uint64_t* words, int W, int a, int b) {  // -1 = none
+    if (b < 0) return a >= 0;
+    if (a < 0) return false;
+    const uint64_t* x = words + static_cast<int64_t>(a) * W;
+    const uint64_t* y = words + static_cast<int64_t>(b) * W;
+    for (int w = 0; w < W; ++w)
+        if (x[w] != y[w]) return x[w] < y[w];
+    return a < b;
+}
+
+// K3, one CTA: (1) stable LSD sort of the rows by representative in shared
+// memory (8-bit digits, per-warp digit counts, match_any ranks) -- classes
+// become runs of ascending rows, like the reference's std::map buckets
+// (src/formats.cpp:40-46); (2) rank = position - position of the run's
+// representative; leaders = ranks that are multiples of V; (3) exclusive scan
+// of the leader flags in row order = group number by first row (the
+// reference's group order, src/formats.cpp:160-170); (4) failing classes
+// (size % V != 0): lexicographically smallest one's smallest row
+// (src/formats.cpp:113-125); (5) row_indices / leaders / n_g; (6) group_ptr
+// = exclusive scan of roundup(n_g, ktile), widest group; status.
+// row_indices == nullptr: validation only (status alone).
+__global__ void __launch_bounds__(kPlanThreads, 1)
+    k_plan(const uint32_t* __restrict__ rep_by_row, const uint32_t* __restrict__ csize, const int* __restrict__ popc,
+           const uint64_t* __restrict__ words, int M, int W, int V, int ktile, const uint32_t* __restrict__ flags,
+           int32_t* __restrict__ row_indices, int32_t* __restrict__ group_leader, int32_t* __restrict__ group_ncols,
+           int32_t* __restrict__ group_ptr, int32_t* __restrict__ status) {
+    extern __shared__ __align__(16) unsigned char sm_plan[];
+    const int Mp = (M + 7) & ~7;
+    uint16_t* rep = reinterpret_cast<uint16_t*>(sm_plan);  // rep by row, later rank by sorted position
+    uint16_t* bufa = rep + Mp;
+    uint16_t* bufb = bufa + Mp;
+    uint16_t* wcnt = bufb + Mp;  // [32 warps][256 digits]
+    __shared__ int tmp[33];
+    __shared__ int best_s[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = M / V;
+    // representatives: 16-byte loads, all in flight
+    if ((M & 3) == 0) {
+        const uint4* r4 = reinterpret_cast<const uint4*>(rep_by_row);
+#pragma unroll 1
+        for (int i4 = tid; i4 < M / 4; i4 += 4 * kPlanThreads) {
+            uint4 q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i4 + u * kPlanThreads < M / 4) q[u] = r4[i4 + u * kPlanThreads];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = 4 * (i4 + u * kPlanThreads);
+                if (i < M) {
+                    rep[i] = static_cast<uint16_t>(q[u].x);
+                    rep[i + 1] = static_cast<uint16_t>(q[u].y);
+                    rep[i + 2] = static_cast<uint16_t>(q[u].z);
+                    rep[i + 3] = static_cast<uint16_t>(q[u].w);
+                }
+            }
+        }
+    } else {
+        for (int i = tid; i < M; i += kPlanThreads) rep[i] = static_cast<uint16_t>(rep_by_row[i]);
+    }
+    for (int i = tid; i < M; i += kPlanThreads) bufa[i] = static_cast<uint16_t>(i);
+    __syncthreads();
+    // (1) sort
+    const int bits = M > 1 ? 32 - __clz(M - 1) : 0;
+    const int CH = (((M + 31) >> 5) + 31) & ~31;  // positions per warp (whole rounds)
+    const int p0 = warp * CH, p1 = min(p0 + CH, M);
+    const unsigned lt = (1u << lane) - 1u;
+    uint16_t* src = bufa;
+    uint16_t* dst = bufb;
+    for (int sh = 0; sh < bits; sh += 8) {
+        const int nb = min(8, bits - sh);
+        for (int i = tid; i < 32 * 256; i += kPlanThreads) wcnt[i] = 0;
+        __syncthreads();
+        for (int base = p0; base < p1; base += 32) {
+            const int i = base + lane;
+            const bool valid = i < p1;
+            const uint32_t d = valid ? (rep[src[i]] >> sh) & 255u : 0u;
+            const unsigned peers = match_digit(d, nb, valid);
+            if (valid && (peers & lt) == 0) wcnt[warp * 256 + d] += static_cast<uint16_t>(__popc(peers));
+        }
+        __syncthreads();
+        {   // digit-major exclusive offsets: (digit, warp)
+            int tot = 0;
+            if (tid < 256)
+                for (int w = 0; w < 32; ++w) tot += wcnt[w * 256 + tid];
+            int all;
+            int run = block_scan_1024(tid < 256 ? tot : 0, tmp, &all);
+            if (tid < 256)
+                for (int w = 0; w < 32; ++w) {
+                    const int c = wcnt[w * 256 + tid];
+                    wcnt[w * 256 + tid] = static_cast<uint16_t>(run);
+                    run += c;
+                }
+        }
+        __syncthreads();
+        for (int base = p0; base < p1; base += 32) {
+            const int i = base + lane;
+            const bool valid = i < p1;
+            const uint16_t row = valid ? src[i] : 0;
+            const uint32_t d = valid ? (rep[row] >> sh) & 255u : 0u;
+            const unsigned peers = match_digit(d, nb, valid);
+            if (valid) dst[wcnt[warp * 256 + d] + __popc(peers & lt)] = row;
+            __syncwarp();
+            if (valid && (peers & lt) == 0) wcnt[warp * 256 + d] += static_cast<uint16_t>(__popc(peers));
+            __syncwarp();
+        }
+        __syncthreads();
+        uint16_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    // (2) ranks.  Positions are split into thread-contiguous ranges; a run
+    // (class) starts where the row is its own representative; rank = position
+    // - run start (an exclusive max-scan carries the start across threads).
+    // Loops are not unrolled: a one-CTA kernel pays every instruction-cache
+    // miss (fully unrolled, 45 % of the samples were no_instruction stalls).
+    const int PT = (M + kPlanThreads - 1) / kPlanThreads;
+    const int q0 = min(tid * PT, M), q1 = min(q0 + PT, M);
+    int best = -1, last = -1;
+    bool anyfail = false;
+#pragma unroll 1
+    for (int i = q0; i < q1; ++i) {
+        const int row = src[i];
+        if (rep[row] == row) {
+            last = i;
+            if (csize[row] % static_cast<uint32_t>(V) != 0) {
+                anyfail = true;
+                if (row_less(words, W, row, best)) best = row;
+            }
+        }
+    }
+    {
+        int carry = last;  // inclusive max over threads <= tid, then shifted
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, carry, o);
+            if (lane >= o) carry = max(carry, t);
+        }
+        if (lane == 31) tmp[warp] = carry;
+        __syncthreads();
+        if (warp == 0) {
+            int wv = tmp[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, wv, o);
+                if (lane >= o) wv = max(wv, t);
+            }
+            tmp[lane] = wv;
+        }
+        __syncthreads();
+        int excl = __shfl_up_sync(0xffffffffu, carry, 1);
+        if (lane == 0) excl = -1;
+        if (warp > 0) excl = max(excl, tmp[warp - 1]);
+        int cur = excl;
+#pragma unroll 1
+        for (int i = q0; i < q1; ++i) {
+            const int row = src[i];
+            if (rep[row] == row) cur = i;
+            dst[i] = static_cast<uint16_t>(i - cur);  // rank by sorted position
+        }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int i = q0; i < q1; ++i) rep[src[i]] = (dst[i] % V) == 0 ? 1 : 0;  // leader flags by row
+    anyfail = __syncthreads_or(anyfail);
+    if (anyfail) {  // (4) lexicographic argmin over the failing classes' representatives
+#pragma unroll 1
+        for (int o = 16; o; o >>= 1) {
+            const int other = __shfl_down_sync(0xffffffffu, best, o);
+            if (lane < o && row_less(words, W, other, best)) best = other;
+        }
+        if (lane == 0) best_s[warp] = best;
+        __syncthreads();
+        if (warp == 0) {
+            best = best_s[lane];
+#pragma unroll 1
+            for (int o = 16; o; o >>= 1) {
+                const int other = __shfl_down_sync(0xffffffffu, best, o);
+                if (lane < o && row_less(words, W, other, best)) best = other;
+            }
+            if (lane == 0) best_s[0] = best;
+        }
+        __syncthreads();
+        best = best_s[0];
+    }
+    // (3) group number of each leader row: exclusive scan in row order
+    int nlead;
+    {
+        int cnt = 0;
+#pragma unroll 1
+        for (int r = q0; r < q1; ++r) cnt += rep[r];
+        int run = block_scan_1024(cnt, tmp, &nlead);
+#pragma unroll 1
+        for (int r = q0; r < q1; ++r) {
+            const int f = rep[r];
+            rep[r] = static_cast<uint16_t>(run);
+            run += f;
+        }
+    }
+    __syncthreads();
+    int code = flags[0] ? SHFLBW_BAD_PARAMS
+                        : (flags[1] ? SHFLBW_CUDA_ERROR : (anyfail ? SHFLBW_NONCONFORMANT_MASK : SHFLBW_OK));
+    if (!row_indices) {
+        if (tid == 0) {
+            status[0] = code;
+            status[1] = anyfail ? best : 0;
+            status[2] = status[3] = 0;
+        }
+        return;
+    }
+    if (nlead != G) {  // non-conformant: every output slot defined
+        for (int i = tid; i < M; i += kPlanThreads) row_indices[i] = 0;
+        for (int g = tid; g < G; g += kPlanThreads) group_leader[g] = group_ncols[g] = 0;
+        __syncthreads();
+    }
+    // (5) assignment
+#pragma unroll 1
+    for (int i = q0; i < q1; ++i) {
+        const int slot = dst[i] % V;
+        const int lead_row = src[i - slot];
+        const int g = rep[lead_row];
+        if (g < G) {
+            row_indices[static_cast<int64_t>(g) * V + slot] = src[i];
+            if (slot == 0) {
+                group_leader[g] = lead_row;
+                group_ncols[g] = popc[lead_row];
+            }
+        }
+    }
+    __syncthreads();
+    // (6) group_ptr, widest group
+    const int PG = (G + kPlanThreads - 1) / kPlanThreads;
+    const int g0 = min(tid * PG, G), g1 = min(g0 + PG, G);
+    int sum = 0, mx = 0;
+    for (int g = g0; g < g1; ++g) {
+        const int pd = (group_ncols[g] + ktile - 1) / ktile * ktile;
+        sum += pd;
+        mx = max(mx, pd);
+    }
+    int total;
+    int run = block_scan_1024(sum, tmp, &total);
+    for (int g = g0; g < g1; ++g) {
+        group_ptr[g] = run;
+        run += (group_ncols[g] + ktile - 1) / ktile * ktile;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) best_s[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+        int m = 0;
+        for (int w = 0; w < 32; ++w) m = max(m, best_s[w]);
+        group_ptr[G] = total;
+        status[0] = code;
+        status[1] = anyfail ? best : 0;
+        status[2] = total;
+        status[3] = m;
+    }
+}
+
+// K4: one CTA per (group, 64-column K block): the block's column list from
+// the leader row's words (prefix popcount, replaces k_pack_cols), the group's
+// V rows gathered at those columns (independent loads, 16 per thread in
+// flight), rounded to the value type and transposed through a bank-padded
+// shared tile, written as one contiguous V x 64 slab.  Also flags block-wise
+// K blocks (64 consecutive columns) in *contig.
+template <int DT, int DIN>
+__global__ void __launch_bounds__(256, 8) k_pack_group(const void* __restrict__ dense, int K, int V, int W,
+                                                    const uint64_t* __restrict__ words,
+                                                    const int32_t* __restrict__ group_leader,
+                                                    const int32_t* __restrict__ group_ptr,
+                                                    const int32_t* __restrict__ group_ncols,
+                                                    const int32_t* __restrict__ row_indices,
+                                                    int32_t* __restrict__ col_idx, void* __restrict__ values,
+                                                    uint32_t* __restrict__ contig) {
+    using T = typename Elem<DT>::T;
+    using TI = typename Elem<DIN>::T;
+    constexpr int JC = SHFLBW_K_TILE;
+    constexpr int kWCap = 1024;  // leader words held as prefix counts (K <= 65536)
+    extern __shared__ __align__(16) unsigned char sm_pack[];
+    __shared__ int cols_s[JC];
+    __shared__ int tmp[8];
+    __shared__ int wpre[kWCap];
+    const int SV = sizeof(T) == 2 ? V + 2 : V + 1;  // odd bank stride between columns
+    T* stage = reinterpret_cast<T*>(sm_pack);       // [JC][SV]
+    int* rows_s = reinterpret_cast<int*>(sm_pack + ((static_cast<size_t>(JC) * SV * sizeof(T) + 15) & ~size_t(15)));
+    const int g = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gp = group_ptr[g];
+    const int padded = group_ptr[g + 1] - gp;
+    const int j0 = blockIdx.x * JC;
+    if (j0 >= padded) return;
+    const int ng = group_ncols[g];
+    const int nvalid = max(0, min(JC, ng - j0));
+    for (int v = tid; v < V; v += 256) rows_s[v] = row_indices[static_cast<int64_t>(g) * V + v];
+    if (nvalid > 0) {
+        // exclusive prefix popcount of the leader row's words, then thread t
+        // < nvalid selects set bit j0 + t: binary search over the prefix, then
+        // the bit inside the word (column 0 = MSB)
+        const uint64_t* lw = words + static_cast<int64_t>(group_leader[g]) * W;
+        const int wpt = (W + 255) / 256;
+        const int w0 = min(tid * wpt, W), w1 = min(w0 + wpt, W);
+        int cnt = 0;
+        for (int w = w0; w < w1; ++w) cnt += __popcll(lw[w]);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) tmp[warp] = incl;
+        __syncthreads();
+        int r = incl - cnt;
+        for (int w = 0; w < warp; ++w) r += tmp[w];
+        if (W <= kWCap) {
+            for (int w = w0; w < w1; ++w) {
+                wpre[w] = r;
+                r += __popcll(lw[w]);
+            }
+            __syncthreads();
+            if (tid < nvalid) {
+                const int target = j0 + tid;
+                int lo = 0, hi = W - 1;  // last word whose prefix <= target
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (wpre[mid] <= target) lo = mid;
+                    else hi = mid - 1;
+                }
+                const uint64_t x = lw[lo];
+                int n = target - wpre[lo];
+                const uint32_t xh = static_cast<uint32_t>(x >> 32), xl = static_cast<uint32_t>(x);
+                const int ph = __popc(xh);
+                const int b = n < ph ? static_cast<int>(__fns(__brev(xh), 0, n + 1))
+                                     : 32 + static_cast<int>(__fns(__brev(xl), 0, n - ph + 1));
+                cols_s[tid] = lo * 64 + b;
+            }
+        } else if (r < j0 + nvalid && r + cnt > j0) {
+            for (int w = w0; w < w1 && r < j0 + nvalid; ++w) {
+                uint64_t x = lw[w];
+                const int pc = __popcll(x);
+                if (r + pc <= j0) {
+                    r += pc;
+                    continue;
+                }
+                while (x && r < j0 + nvalid) {
+                    const int b = __clzll(x);
+                    if (r >= j0) cols_s[r - j0] = w * 64 + b;
+                    ++r;
+                    x &= ~(0x8000000000000000ULL >> b);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (tid < JC) col_idx[gp + j0 + tid] = tid < nvalid ? cols_s[tid] : SHFLBW_PAD_COLUMN;
+    if (contig && tid == 0 && nvalid == JC && cols_s[JC - 1] - cols_s[0] == JC - 1) atomicOr(contig, 1u);
+    // gather: thread = (column jj = tid % 64, rows v = tid / 64 + 4u): a warp
+    // reads 32 kept columns of one row; all of a thread's loads in flight
+    const TI* src = static_cast<const TI*>(dense);
+    const int jj = tid & (JC - 1), vq = tid >> 6;
+    const bool live = jj < nvalid;
+    const int col = live ? cols_s[jj] : 0;
+    for (int v0 = 0; v0 < V; v0 += 32) {
+        float x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int v = v0 + 4 * u + vq;
+            x[u] = 0.0f;
+            if (live && v < V) x[u] = Elem<DIN>::to_f(src[static_cast<int64_t>(rows_s[v]) * K + col]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int v = v0 + 4 * u + vq;
+            if (v < V) stage[jj * SV + v] = Elem<DT>::from_f(x[u]);
+        }
+    }
+    __syncthreads();
+    // contiguous V x 64 slab: values[(gp + j0 + jj) * V + v]
+    const int total = V * JC;
+    T* out = static_cast<T*>(values) + static_cast<int64_t>(gp + j0) * V;
+    if (sizeof(T) == 2 && (V & 1) == 0) {
+        uint32_t* out2 = reinterpret_cast<uint32_t*>(out);
+        for (int e = tid; e < total / 2; e += 256) {
+            const int jj = (2 * e) / V, v = (2 * e) % V;
+            out2[e] = *reinterpret_cast<const uint32_t*>(stage + jj * SV + v);
+        }
+    } else {
+        for (int e = tid; e < total; e += 256) out[e] = stage[(e / V) * SV + e % V];
+    }
+}
+
 // ---- host helpers ------------------------------------------------------------
 
 }  // namespace
@@ -797,14 +1316,125 @@ int radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_
 
 namespace {
 
+// run `f.template operator()<DT>()` for the matrix value dtype
+template <class F>
+void by_dtype(int dt, F&& f) {
+    if (dt == SHFLBW_BF16) f.template operator()<SHFLBW_BF16>();
+    else if (dt == SHFLBW_F16) f.template operator()<SHFLBW_F16>();
+    else f.template operator()<SHFLBW_F32>();
+}
+
 int launch_pack_rows(const uint8_t* mask, int M, int K, int W, uint64_t seed, uint64_t* words, int* popc,
-                     uint64_t* keys, uint32_t* vals, uint32_t* flags, cudaStream_t s) {
+                     uint64_t* keys, uint32_t* vals, uint32_t* flags, cudaStream_t s,
+                     const ClassTable& tab = ClassTable{}) {
     if (K > 0 && K % 16 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0) {
-        k_pack_rows16<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, W, seed, words, popc, keys, vals, flags);
+        k_pack_rows16<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, W, seed, words, popc, keys, vals, flags, tab);
         SBW_LAUNCHED("k_pack_rows16");
     } else {
-        k_pack_rows<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, W, seed, words, popc, keys, vals, flags);
+        k_pack_rows<<<grid_for(M, 8), 256, 0, s>>>(mask, M, K, W, seed, words, popc, keys, vals, flags, tab);
         SBW_LAUNCHED("k_pack_rows");
+    }
+    return SHFLBW_OK;
+}
+
+// ---- hash planner host side (M <= kPlanMax) ---------------------------------
+// K1 k_pack_rows(+table insert) -> K2 k_class_check -> K3 k_plan (one CTA)
+// -> K4 k_pack_group: four launches and two memsets for any M up to 32768
+// (the sort-based pipeline: 12-30 launches).  Option "converter_legacy"
+// forces the sort-based pipeline (kept for M > kPlanMax).
+bool use_planner(int M, int V) {
+    return M >= 1 && M <= kPlanMax && V >= 1 && option("converter_legacy") == 0;
+}
+
+struct HashPlan {
+    DevBuf words, popc, table, rep, csize, flags, leader;
+    ClassTable tab;
+    int W = 1;
+    size_t table_bytes = 0;
+};
+
+int hash_plan_alloc(HashPlan& p, int M, int K, int V, cudaStream_t s) {
+    p.W = K > 0 ? (K + 63) / 64 : 1;
+    uint32_t P = 64;
+    while (P < 2u * static_cast<uint32_t>(M)) P <<= 1;
+    p.table_bytes = static_cast<size_t>(P) * 16;
+    SBW_CUDA(p.words.alloc(sizeof(uint64_t) * static_cast<size_t>(M) * p.W, s));
+    SBW_CUDA(p.popc.alloc(sizeof(int) * M, s));
+    SBW_CUDA(p.table.alloc(p.table_bytes + sizeof(uint32_t) * M, s));
+    SBW_CUDA(p.rep.alloc(sizeof(uint32_t) * M, s));
+    SBW_CUDA(p.csize.alloc(sizeof(uint32_t) * M, s));
+    SBW_CUDA(p.flags.alloc(sizeof(uint32_t) * 4, s));
+    SBW_CUDA(p.leader.alloc(sizeof(int32_t) * (M / V + 1), s));
+    p.tab.key = p.table.as<uint64_t>();
+    p.tab.minrow = reinterpret_cast<uint32_t*>(p.tab.key + P);
+    p.tab.cnt = p.tab.minrow + P;
+    p.tab.slot = p.tab.cnt + P;
+    p.tab.mask = P - 1;
+    return SHFLBW_OK;
+}
+
+// K1-K3; status[4] (device) = {code, fail_row, total columns, widest group}.
+// row_indices == nullptr: validation only.
+int hash_plan_run(HashPlan& p, const uint8_t* mask, int M, int K, int V, uint64_t seed, int32_t* row_indices,
+                  int32_t* group_ncols, int32_t* group_ptr, int32_t* status, cudaStream_t s) {
+    SBW_CUDA(cudaMemsetAsync(p.table.p, 0xff, p.table_bytes, s));
+    SBW_CUDA(cudaMemsetAsync(p.flags.p, 0, sizeof(uint32_t) * 4, s));
+    if (int st = launch_pack_rows(mask, M, K, p.W, seed, p.words.as<uint64_t>(), p.popc.as<int>(), nullptr, nullptr,
+                                  p.flags.as<uint32_t>(), s, p.tab))
+        return st;
+    k_class_check<<<grid_for(M, 8), 256, 0, s>>>(p.words.as<uint64_t>(), M, p.W, p.tab, p.rep.as<uint32_t>(),
+                                                 p.csize.as<uint32_t>(), p.flags.as<uint32_t>());
+    SBW_LAUNCHED("k_class_check");
+    const size_t smem = static_cast<size_t>((M + 7) & ~7) * 6 + 32 * 256 * 2;
+    if (smem > 48 * 1024)  // per call: the attribute is per device
+        SBW_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    k_plan<<<1, kPlanThreads, smem, s>>>(p.rep.as<uint32_t>(), p.csize.as<uint32_t>(), p.popc.as<int>(),
+                                         p.words.as<uint64_t>(), M, p.W, V, SHFLBW_K_TILE, p.flags.as<uint32_t>(),
+                                         row_indices, p.leader.as<int32_t>(), group_ncols, group_ptr, status);
+    SBW_LAUNCHED("k_plan");
+    return SHFLBW_OK;
+}
+
+// K4 (V <= 128; wider groups: k_pack_cols + k_pack_values + k_contig_blocks)
+int launch_pack(const void* dense, int dense_dtype, int K, int V, int G, int64_t max_padded, int W,
+                const uint64_t* words, const int32_t* leader, shflbw_cu_matrix* out, uint32_t* contig,
+                cudaStream_t s) {
+    if (G <= 0 || max_padded <= 0) return SHFLBW_OK;
+    const dim3 grid(static_cast<unsigned>((max_padded + SHFLBW_K_TILE - 1) / SHFLBW_K_TILE), G);
+    if (V <= 128) {
+        const int esz = dtype_bytes(out->dtype);
+        const int SV = esz == 2 ? V + 2 : V + 1;
+        const size_t smem = ((static_cast<size_t>(SHFLBW_K_TILE) * SV * esz + 15) & ~size_t(15)) + 4 * V;
+        by_dtype(out->dtype, [&]<int DT>() {
+            auto go = [&](auto kern) {
+                kern<<<grid, 256, smem, s>>>(dense, K, V, W, words, leader, out->group_ptr, out->group_ncols,
+                                             out->row_indices, out->col_idx, out->values, contig);
+            };
+            if (dense_dtype == SHFLBW_BF16) go(k_pack_group<DT, SHFLBW_BF16>);
+            else if (dense_dtype == SHFLBW_F16) go(k_pack_group<DT, SHFLBW_F16>);
+            else go(k_pack_group<DT, SHFLBW_F32>);
+        });
+        SBW_LAUNCHED("k_pack_group");
+        return SHFLBW_OK;
+    }
+    k_pack_cols<<<G, 128, 0, s>>>(words, W, leader, out->group_ptr, out->group_ncols, out->col_idx);
+    SBW_LAUNCHED("k_pack_cols");
+    const int jc = V <= 1024 ? 64 : 8;
+    const size_t smem = static_cast<size_t>(jc) * V * dtype_bytes(out->dtype);
+    const dim3 g2(static_cast<unsigned>((max_padded + jc - 1) / jc), G);
+    cudaError_t ce = cudaSuccess;
+    by_dtype(out->dtype, [&]<int DT>() {
+        if (smem > 48 * 1024)
+            ce = cudaFuncSetAttribute(k_pack_values<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem));
+        k_pack_values<DT><<<g2, 256, smem, s>>>(dense, dense_dtype, K, V, jc, out->row_indices, out->group_ptr,
+                                                 out->group_ncols, out->col_idx, out->values);
+    });
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaFuncSetAttribute");
+    SBW_LAUNCHED("k_pack_values");
+    if (contig) {
+        k_contig_blocks<<<G, 32, 0, s>>>(out->group_ptr, out->col_idx, contig);
+        SBW_LAUNCHED("k_contig_blocks");
     }
     return SHFLBW_OK;
 }
@@ -881,14 +1511,6 @@ int check_dtype16(int dt) {
     return SHFLBW_OK;
 }
 
-// run `f.template operator()<DT>()` for the matrix value dtype
-template <class F>
-void by_dtype(int dt, F&& f) {
-    if (dt == SHFLBW_BF16) f.template operator()<SHFLBW_BF16>();
-    else if (dt == SHFLBW_F16) f.template operator()<SHFLBW_F16>();
-    else f.template operator()<SHFLBW_F32>();
-}
-
 // allocate meta (row_indices, group_ptr, group_ncols) in one block
 int alloc_meta(shflbw_cu_matrix* out, int M, int K, int V, int dtype, cudaStream_t s) {
     const int G = M / V;
@@ -945,6 +1567,28 @@ int validate_impl(const uint8_t* mask, int M, int K, int V, int32_t* pass, uint3
     *pass = 1;
     *fail_row = 0;
     if (M == 0) return SHFLBW_OK;
+    if (use_planner(M, V)) {
+        HashPlan hp;
+        DevBuf st;
+        if (int e = hash_plan_alloc(hp, M, K, V, s)) return e;
+        SBW_CUDA(st.alloc(sizeof(int32_t) * 4, s));
+        int32_t h[4] = {0, 0, 0, 0};
+        for (int attempt = 0; attempt < 4; ++attempt) {
+            if (int e = hash_plan_run(hp, mask, M, K, V, 0x5ca1ab1e00000000ULL + attempt, nullptr, nullptr, nullptr,
+                                      st.as<int32_t>(), s))
+                return e;
+            SBW_CUDA(cudaMemcpyAsync(h, st.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+            SBW_CUDA(cudaStreamSynchronize(s));
+            if (h[0] != SHFLBW_CUDA_ERROR) break;
+        }
+        if (h[0] == SHFLBW_BAD_PARAMS) return fail(SHFLBW_BAD_PARAMS, "SparsityMask: entries must be 0 or 1");
+        if (h[0] == SHFLBW_CUDA_ERROR) return fail(SHFLBW_CUDA_ERROR, "compress: unresolvable row-hash collisions");
+        if (h[0] == SHFLBW_NONCONFORMANT_MASK) {
+            *pass = 0;
+            *fail_row = static_cast<uint32_t>(h[1]);
+        }
+        return SHFLBW_OK;
+    }
     ClassPlan p;
     uint32_t hf[4];
     int st = plan_classes(mask, M, K, V, p, hf, s);
@@ -971,6 +1615,44 @@ int compress_impl(const void* dense, int dense_dtype, const uint8_t* mask, int M
     if (M == 0) {
         SBW_CUDA(cudaMemsetAsync(out->group_ptr, 0, sizeof(int32_t), s));
         return cleanup(alloc_data(out, 0, s));
+    }
+    if (use_planner(M, V)) {
+        HashPlan hp;
+        DevBuf stb, cf;
+        if (int e = hash_plan_alloc(hp, M, K, V, s)) return cleanup(e);
+        SBW_CUDA(stb.alloc(sizeof(int32_t) * 4, s));
+        SBW_CUDA(cf.alloc(sizeof(uint32_t), s));
+        int32_t h[4] = {0, 0, 0, 0};
+        for (int attempt = 0; attempt < 4; ++attempt) {
+            if (int e = hash_plan_run(hp, mask, M, K, V, 0x5ca1ab1e00000000ULL + attempt, out->row_indices,
+                                      out->group_ncols, out->group_ptr, stb.as<int32_t>(), s))
+                return cleanup(e);
+            SBW_CUDA(cudaMemcpyAsync(h, stb.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+            SBW_CUDA(cudaStreamSynchronize(s));
+            if (h[0] != SHFLBW_CUDA_ERROR) break;
+        }
+        if (h[0] == SHFLBW_BAD_PARAMS) return cleanup(fail(SHFLBW_BAD_PARAMS, "SparsityMask: entries must be 0 or 1"));
+        if (h[0] == SHFLBW_CUDA_ERROR)
+            return cleanup(fail(SHFLBW_CUDA_ERROR, "compress: unresolvable row-hash collisions"));
+        if (h[0] == SHFLBW_NONCONFORMANT_MASK) {
+            if (fail_row) *fail_row = static_cast<uint32_t>(h[1]);
+            return cleanup(fail(SHFLBW_NONCONFORMANT_MASK,
+                                "compress_shflbw: support class size is not a multiple of V (row " +
+                                    std::to_string(h[1]) + ")"));
+        }
+        out->max_group_cols = h[3];
+        if (int e = alloc_data(out, h[2], s)) return cleanup(e);
+        SBW_CUDA(cudaMemsetAsync(cf.p, 0, sizeof(uint32_t), s));
+        if (int e = launch_pack(dense, dense_dtype, K, V, G, h[3], hp.W, hp.words.as<uint64_t>(),
+                                hp.leader.as<int32_t>(), out, cf.as<uint32_t>(), s))
+            return cleanup(e);
+        uint32_t contig = 0;
+        SBW_CUDA(cudaMemcpyAsync(&contig, cf.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        // the matrix is complete on return (SpMM prologues read it before their
+        // programmatic-launch wait, see the "pdl" option)
+        SBW_CUDA(cudaStreamSynchronize(s));
+        if (contig) out->reserved |= SHFLBW_CONTIG_BLOCKS;
+        return SHFLBW_OK;
     }
     ClassPlan p;
     uint32_t hf[4];
@@ -1073,6 +1755,17 @@ int compress_async_impl(const void* dense, int dense_dtype, const uint8_t* mask,
     out->total_cols = bound;
     out->max_group_cols = static_cast<int32_t>(kpad);
     out->reserved = SHFLBW_SIZE_BOUND | SHFLBW_BOUND_ALLOC;
+    if (M > 0 && use_planner(M, V)) {
+        HashPlan hp;
+        if (int e = hash_plan_alloc(hp, M, K, V, s)) return cleanup(e);
+        if (int e = hash_plan_run(hp, mask, M, K, V, 0x5ca1ab1e00000000ULL, out->row_indices, out->group_ncols,
+                                  out->group_ptr, status, s))
+            return cleanup(e);
+        if (int e = launch_pack(dense, dense_dtype, K, V, G, kpad, hp.W, hp.words.as<uint64_t>(),
+                                hp.leader.as<int32_t>(), out, nullptr, s))
+            return cleanup(e);
+        return SHFLBW_OK;
+    }
     DevBuf flags, fr, maxp;
     SBW_CUDA(flags.alloc(sizeof(uint32_t) * 4, s));
     SBW_CUDA(fr.alloc(sizeof(uint32_t), s));
