@@ -123,7 +123,12 @@ int shflbw_cu_version(void);
  * instead of running the CUDA-core kernel), "raster" (persistent unit order:
  * 0 = auto, 1 = group-major, 2 = column-tile-major), "tile_n" (output columns
  * per unit: 0 = auto, 128, or 64 = half-width units for grids that would
- * leave SMs idle).  All variants give results
+ * leave SMs idle), "gather_issue" (0 = auto, 1 = one elected lane per
+ * warp issues its gathers, 2 = every issuing lane), "tile_loads" (0 = auto:
+ * block-wise K blocks of matrices flagged SHFLBW_CONTIG_BLOCKS as 2D TMA
+ * tiles, -1 = gathers only, 1 = check every K block),
+ * "converter_legacy" (1: the converter's sort-based class grouping instead
+ * of the class table + one-CTA planner; the same output).  All variants give results
  * within the same tolerance; V split, cp.async, gather warps and persistent
  * are bit-identical to the default.
  * Unknown key: BAD_PARAMS. */

@@ -5,26 +5,32 @@
 //
 // The reference groups rows by exact mask-row equality with a std::map keyed
 // by the whole row (src/formats.cpp:40-46), cuts each class into V-row chunks
-// of ascending rows and orders the chunks by first row.  Here:
+// of ascending rows and orders the chunks by first row.  Here (M <= 28672):
 //
-//   1. k_pack_rows   one warp per row: the mask row becomes 64-bit words with
+//   K1 k_pack_rows   one warp per row: the mask row becomes 64-bit words with
 //                    column 0 as the MSB of word 0 (so unsigned word order is
-//                    the reference's lexicographic byte order), plus popcount
-//                    and a 64-bit hash; bytes > 1 are flagged (SparsityMask's
-//                    constructor rejects them, src/matrix.cpp:24-31).
-//   2. radix sort    stable LSD sort of (hash, row) pairs: equal rows become
-//                    runs, rows ascending inside a run.
-//   3. k_runs        run bounds by binary search; adjacent rows of a run are
-//                    compared word by word -- a hash collision is detected
+//                    the reference's lexicographic byte order), popcount and
+//                    a 64-bit hash; bytes > 1 are flagged (SparsityMask's
+//                    constructor rejects them, src/matrix.cpp:24-31).  The
+//                    hash claims a slot of an open-addressing class table;
+//                    the slot keeps the class's smallest row and its size.
+//   K2 k_class_check every row against its class representative (smallest
+//                    row) word by word -- a hash collision is detected
 //                    exactly and the host retries with another seed, so the
 //                    grouping is exact, not probabilistic.
-//   4. groups        leaders = run positions whose rank is a multiple of V; an
-//                    exclusive scan over rows numbers them by first row, which
-//                    is the reference's group order.
-//   5. packing       per group: column list = set bits of the leader row,
-//                    padded with kPadColumn to a multiple of SHFLBW_K_TILE;
-//                    values gathered, rounded to bf16/fp16 (RNE) and written
-//                    column-major (V contiguous) through a shared-memory tile.
+//   K3 k_plan        one CTA: rows ordered by (representative, row) -- a
+//                    shared-memory LSD sort for M <= 4096, per-1024-row chunk
+//                    ranks (k_chunk_rank, k_chunk_prefix) above; rank in
+//                    class, leaders = ranks that are multiples of V, group
+//                    number = exclusive scan of the leaders in row order (the
+//                    reference's group order), row_indices, n_g, group_ptr.
+//   K4 k_pack_group  per (group, 64-column block): the column list from the
+//                    leader's words, values gathered, rounded to bf16/fp16
+//                    (RNE) and written column-major (V contiguous).
+//
+// Larger M (and option "converter_legacy"): the sort-based pipeline -- a
+// stable radix sort of (hash, row) pairs makes equal rows runs (k_runs checks
+// adjacent rows exactly), then k_assign / k_pack_cols / k_pack_values.
 //
 // A failing class is reported like the reference: the lexicographically
 // smallest failing support class (word-wise argmin over run heads) gives its
@@ -764,7 +770,8 @@ __global__ void k_class_check(const uint64_t* __restrict__ words, int M, int W, 
 }
 
 constexpr int kPlanThreads = 1024;
-constexpr int kPlanMax = 32768;                      // rows: 16-bit row ids in shared memory
+constexpr int kPlanMax = 28672;                      // rows: four 16-bit arrays of M in shared memory
+constexpr int kPlanSmall = 4096;                     // above: chunked ranks (k_chunk_rank) instead of the CTA sort
 
 // exclusive scan of one int per thread over a 1024-thread block; *total =
 // the block sum (every thread).  `tmp` holds 33 ints.
@@ -823,64 +830,90 @@ __device__ __noinline__ bool row_less(const uint64_t* words, int W, int a, int b
     return a < b;
 }
 
-// K3, one CTA: (1) stable LSD sort of the rows by representative in shared
-// memory (8-bit digits, per-warp digit counts, match_any ranks) -- classes
-// become runs of ascending rows, like the reference's std::map buckets
-// (src/formats.cpp:40-46); (2) rank = position - position of the run's
-// representative; leaders = ranks that are multiples of V; (3) exclusive scan
-// of the leader flags in row order = group number by first row (the
-// reference's group order, src/formats.cpp:160-170); (4) failing classes
-// (size % V != 0): lexicographically smallest one's smallest row
-// (src/formats.cpp:113-125); (5) row_indices / leaders / n_g; (6) group_ptr
-// = exclusive scan of roundup(n_g, ktile), widest group; status.
-// row_indices == nullptr: validation only (status alone).
-__global__ void __launch_bounds__(kPlanThreads, 1)
-    k_plan(const uint32_t* __restrict__ rep_by_row, const uint32_t* __restrict__ csize, const int* __restrict__ popc,
-           const uint64_t* __restrict__ words, int M, int W, int V, int ktile, const uint32_t* __restrict__ flags,
-           int32_t* __restrict__ row_indices, int32_t* __restrict__ group_leader, int32_t* __restrict__ group_ncols,
-           int32_t* __restrict__ group_ptr, int32_t* __restrict__ status) {
-    extern __shared__ __align__(16) unsigned char sm_plan[];
-    const int Mp = (M + 7) & ~7;
-    uint16_t* rep = reinterpret_cast<uint16_t*>(sm_plan);  // rep by row, later rank by sorted position
-    uint16_t* bufa = rep + Mp;
-    uint16_t* bufb = bufa + Mp;
-    uint16_t* wcnt = bufb + Mp;  // [32 warps][256 digits]
-    __shared__ int tmp[33];
-    __shared__ int best_s[32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int G = M / V;
-    // representatives: 16-byte loads, all in flight
-    if ((M & 3) == 0) {
-        const uint4* r4 = reinterpret_cast<const uint4*>(rep_by_row);
+// dst[i] = src[i] (u32 -> u16), i < n, by a 1024-thread block: 16-byte loads,
+// four per thread in flight
+__device__ __forceinline__ void load_u16(const uint32_t* __restrict__ src, int n, uint16_t* dst) {
+    const int tid = threadIdx.x;
+    if ((n & 3) == 0) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll 1
-        for (int i4 = tid; i4 < M / 4; i4 += 4 * kPlanThreads) {
+        for (int i4 = tid; i4 < n / 4; i4 += 4 * kPlanThreads) {
             uint4 q[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (i4 + u * kPlanThreads < M / 4) q[u] = r4[i4 + u * kPlanThreads];
+                if (i4 + u * kPlanThreads < n / 4) q[u] = s4[i4 + u * kPlanThreads];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int i = 4 * (i4 + u * kPlanThreads);
-                if (i < M) {
-                    rep[i] = static_cast<uint16_t>(q[u].x);
-                    rep[i + 1] = static_cast<uint16_t>(q[u].y);
-                    rep[i + 2] = static_cast<uint16_t>(q[u].z);
-                    rep[i + 3] = static_cast<uint16_t>(q[u].w);
+                if (i < n) {
+                    dst[i] = static_cast<uint16_t>(q[u].x);
+                    dst[i + 1] = static_cast<uint16_t>(q[u].y);
+                    dst[i + 2] = static_cast<uint16_t>(q[u].z);
+                    dst[i + 3] = static_cast<uint16_t>(q[u].w);
                 }
             }
         }
     } else {
-        for (int i = tid; i < M; i += kPlanThreads) rep[i] = static_cast<uint16_t>(rep_by_row[i]);
+        for (int i = tid; i < n; i += kPlanThreads) dst[i] = static_cast<uint16_t>(src[i]);
     }
-    for (int i = tid; i < M; i += kPlanThreads) bufa[i] = static_cast<uint16_t>(i);
+}
+
+// Exclusive scan over i < n of val(i) in index order, out(i, prefix) per i;
+// each warp walks one contiguous segment 32 consecutive indices at a time
+// (thread-contiguous ranges put the lanes of a warp 2*PT bytes apart in a
+// 16-bit array: 8-way bank conflicts at PT = 16).  Returns the total.
+template <class Val, class Out>
+__device__ __forceinline__ int block_scan_rows(int n, Val val, Out out, int* tmp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int S = (((n + 31) >> 5) + 31) & ~31;
+    const int b0 = warp * S, b1 = min(b0 + S, n);
+    int sum = 0;
+    for (int i = b0 + lane; i < b1; i += 32) sum += val(i);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) tmp[warp] = sum;
     __syncthreads();
-    // (1) sort
-    const int bits = M > 1 ? 32 - __clz(M - 1) : 0;
-    const int CH = (((M + 31) >> 5) + 31) & ~31;  // positions per warp (whole rounds)
-    const int p0 = warp * CH, p1 = min(p0 + CH, M);
+    if (warp == 0) {
+        const int v = tmp[lane];
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        tmp[lane] = incl - v;
+        if (lane == 31) tmp[32] = incl;
+    }
+    __syncthreads();
+    int carry = tmp[warp];
+    for (int base = b0; base < b1; base += 32) {
+        const int i = base + lane;
+        const int v = i < b1 ? val(i) : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (i < b1) out(i, carry + incl - v);
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const int total = tmp[32];
+    __syncthreads();
+    return total;
+}
+
+// Stable LSD sort (8-bit digits) of the n element ids in `a` by key[id]
+// (16-bit), per-warp digit counts and ballot ranks; 1024 threads; returns the
+// buffer (a or b) holding the sorted ids.
+__device__ __forceinline__ uint16_t* block_sort16(const uint16_t* key, uint16_t* a, uint16_t* b, int n, int bits,
+                                                  uint16_t* wcnt, int* tmp) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int CH = (((n + 31) >> 5) + 31) & ~31;  // positions per warp (whole rounds)
+    const int p0 = warp * CH, p1 = min(p0 + CH, n);
     const unsigned lt = (1u << lane) - 1u;
-    uint16_t* src = bufa;
-    uint16_t* dst = bufb;
+    uint16_t* src = a;
+    uint16_t* dst = b;
     for (int sh = 0; sh < bits; sh += 8) {
         const int nb = min(8, bits - sh);
         for (int i = tid; i < 32 * 256; i += kPlanThreads) wcnt[i] = 0;
@@ -888,7 +921,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
         for (int base = p0; base < p1; base += 32) {
             const int i = base + lane;
             const bool valid = i < p1;
-            const uint32_t d = valid ? (rep[src[i]] >> sh) & 255u : 0u;
+            const uint32_t d = valid ? (key[src[i]] >> sh) & 255u : 0u;
             const unsigned peers = match_digit(d, nb, valid);
             if (valid && (peers & lt) == 0) wcnt[warp * 256 + d] += static_cast<uint16_t>(__popc(peers));
         }
@@ -911,7 +944,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
             const int i = base + lane;
             const bool valid = i < p1;
             const uint16_t row = valid ? src[i] : 0;
-            const uint32_t d = valid ? (rep[row] >> sh) & 255u : 0u;
+            const uint32_t d = valid ? (key[row] >> sh) & 255u : 0u;
             const unsigned peers = match_digit(d, nb, valid);
             if (valid) dst[wcnt[warp * 256 + d] + __popc(peers & lt)] = row;
             __syncwarp();
@@ -923,27 +956,137 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
         src = dst;
         dst = t;
     }
-    // (2) ranks.  Positions are split into thread-contiguous ranges; a run
-    // (class) starts where the row is its own representative; rank = position
-    // - run start (an exclusive max-scan carries the start across threads).
+    return src;
+}
+
+// K3a (M > kPlanSmall): one CTA per 1024-row chunk sorts its rows by
+// representative; rank of each row among its class's rows in the chunk, and
+// the class's row count in the chunk: cnt[chunk][rep] (zero elsewhere).
+__global__ void __launch_bounds__(kPlanThreads, 1)
+    k_chunk_rank(const uint32_t* __restrict__ rep_by_row, int M, uint16_t* __restrict__ local_rank,
+                 uint16_t* __restrict__ cnt) {
+    __shared__ uint16_t key[kPlanThreads], a[kPlanThreads], b[kPlanThreads];
+    __shared__ uint16_t wcnt[32 * 256];
+    __shared__ int tmp[33];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int r0 = blockIdx.x * kPlanThreads;
+    const int n = min(kPlanThreads, M - r0);
+    uint16_t* crow = cnt + static_cast<int64_t>(blockIdx.x) * M;
+    for (int i = tid; i < M; i += kPlanThreads) crow[i] = 0;
+    if (tid < n) key[tid] = static_cast<uint16_t>(rep_by_row[r0 + tid]);
+    a[tid] = static_cast<uint16_t>(tid);
+    __syncthreads();
+    const uint16_t* srt = block_sort16(key, a, b, n, 32 - __clz(M - 1), wcnt, tmp);
+    const int i = tid;
+    int k = -1, head = -1;
+    if (i < n) {
+        k = key[srt[i]];
+        if (i == 0 || key[srt[i - 1]] != k) head = i;
+    }
+    int start = head;  // inclusive max-scan: the run's first position
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, start, o);
+        if (lane >= o) start = max(start, t);
+    }
+    if (lane == 31) tmp[warp] = start;
+    __syncthreads();
+    if (warp == 0) {
+        int wv = tmp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wv, o);
+            if (lane >= o) wv = max(wv, t);
+        }
+        tmp[lane] = wv;
+    }
+    __syncthreads();
+    if (warp > 0) start = max(start, tmp[warp - 1]);
+    if (i < n) {
+        local_rank[r0 + srt[i]] = static_cast<uint16_t>(i - start);
+        if (i == n - 1 || key[srt[i + 1]] != k) crow[k] = static_cast<uint16_t>(i - start + 1);
+    }
+}
+
+// K3b: exclusive prefix of each class's per-chunk counts over the chunks
+// (in place), one thread per representative
+__global__ void k_chunk_prefix(const uint32_t* __restrict__ rep_by_row, int M, int nchunks,
+                               uint16_t* __restrict__ cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= M || rep_by_row[r] != static_cast<uint32_t>(r)) return;
+    int run = 0;
+    for (int c0 = 0; c0 < nchunks; c0 += 8) {
+        uint16_t t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = c0 + u < nchunks ? cnt[static_cast<int64_t>(c0 + u) * M + r] : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (c0 + u < nchunks) {
+                cnt[static_cast<int64_t>(c0 + u) * M + r] = static_cast<uint16_t>(run);
+                run += t[u];
+            }
+    }
+}
+
+// K3, one CTA: (1) stable LSD sort of the rows by representative in shared
+// memory (8-bit digits, per-warp digit counts, match_any ranks) -- classes
+// become runs of ascending rows, like the reference's std::map buckets
+// (src/formats.cpp:40-46); (2) rank = position - position of the run's
+// representative; leaders = ranks that are multiples of V; (3) exclusive scan
+// of the leader flags in row order = group number by first row (the
+// reference's group order, src/formats.cpp:160-170); (4) failing classes
+// (size % V != 0): lexicographically smallest one's smallest row
+// (src/formats.cpp:113-125); (5) row_indices / leaders / n_g; (6) group_ptr
+// = exclusive scan of roundup(n_g, ktile), widest group; status.
+// row_indices == nullptr: validation only (status alone).
+__global__ void __launch_bounds__(kPlanThreads, 1)
+    k_plan(const uint32_t* __restrict__ rep_by_row, const uint32_t* __restrict__ csize, const int* __restrict__ popc,
+           const uint64_t* __restrict__ words, int M, int W, int V, int ktile, const uint32_t* __restrict__ flags,
+           int32_t* __restrict__ row_indices, int32_t* __restrict__ group_leader, int32_t* __restrict__ group_ncols,
+           int32_t* __restrict__ group_ptr, int32_t* __restrict__ status, const uint16_t* __restrict__ local_rank,
+           const uint16_t* __restrict__ chunk_pref) {
+    extern __shared__ __align__(16) unsigned char sm_plan[];
+    const int Mp = (M + 7) & ~7;
+    uint16_t* rep = reinterpret_cast<uint16_t*>(sm_plan);  // rep by row, later rank by sorted position
+    uint16_t* bufa = rep + Mp;
+    uint16_t* bufb = bufa + Mp;
+    uint16_t* wcnt = bufb + Mp;  // [32 warps][256 digits]
+    __shared__ int tmp[33];
+    __shared__ int best_s[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = M / V;
+    load_u16(rep_by_row, M, rep);  // representatives
+    for (int i = tid; i < M; i += kPlanThreads) bufa[i] = static_cast<uint16_t>(i);
+    __syncthreads();
+    // (1) rows by representative: sorted here (M <= kPlanSmall), else placed
+    // from the per-chunk ranks of k_chunk_rank + k_chunk_prefix.
+    // (2) rank of each sorted position within its class (dst).
     // Loops are not unrolled: a one-CTA kernel pays every instruction-cache
     // miss (fully unrolled, 45 % of the samples were no_instruction stalls).
     const int PT = (M + kPlanThreads - 1) / kPlanThreads;
     const int q0 = min(tid * PT, M), q1 = min(q0 + PT, M);
-    int best = -1, last = -1;
+    int best = -1;
     bool anyfail = false;
+    uint16_t* src;
+    uint16_t* dst;
+    if (!local_rank) {
+        src = block_sort16(rep, bufa, bufb, M, M > 1 ? 32 - __clz(M - 1) : 0, wcnt, tmp);
+        dst = src == bufa ? bufb : bufa;
+        // a run (class) starts where the row is its own representative; rank
+        // = position - run start (an exclusive max-scan carries the start
+        // across the thread-contiguous ranges)
+        int last = -1;
 #pragma unroll 1
-    for (int i = q0; i < q1; ++i) {
-        const int row = src[i];
-        if (rep[row] == row) {
-            last = i;
-            if (csize[row] % static_cast<uint32_t>(V) != 0) {
-                anyfail = true;
-                if (row_less(words, W, row, best)) best = row;
+        for (int i = q0; i < q1; ++i) {
+            const int row = src[i];
+            if (rep[row] == row) {
+                last = i;
+                if (csize[row] % static_cast<uint32_t>(V) != 0) {
+                    anyfail = true;
+                    if (row_less(words, W, row, best)) best = row;
+                }
             }
         }
-    }
-    {
         int carry = last;  // inclusive max over threads <= tid, then shifted
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -970,12 +1113,56 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
         for (int i = q0; i < q1; ++i) {
             const int row = src[i];
             if (rep[row] == row) cur = i;
-            dst[i] = static_cast<uint16_t>(i - cur);  // rank by sorted position
+            dst[i] = static_cast<uint16_t>(i - cur);
         }
+    } else {
+        // class segments in representative order: exclusive scan over rows of
+        // (row is a representative) * class size (csize staged in bufa);
+        // failing classes found on the way
+        uint16_t* rank_pos = bufb + Mp;  // the 4th array (no digit counters here)
+        load_u16(csize, M, bufa);
+        __syncthreads();
+        for (int r = tid; r < M; r += kPlanThreads)
+            if (rep[r] == r && bufa[r] % V != 0) {
+                anyfail = true;
+                if (row_less(words, W, r, best)) best = r;
+            }
+        block_scan_rows(
+            M, [&](int r) { return rep[r] == r ? static_cast<int>(bufa[r]) : 0; },
+            [&](int r, int x) {
+                if (rep[r] == r) bufb[r] = static_cast<uint16_t>(x);
+            },
+            tmp);
+        // sorted position = segment start + rank (earlier chunks + this chunk)
+#pragma unroll 1
+        for (int r0 = tid; r0 < M; r0 += 16 * kPlanThreads) {
+            int rk[16], rp[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int r = r0 + u * kPlanThreads;
+                rk[u] = rp[u] = 0;
+                if (r < M) {
+                    rp[u] = rep[r];
+                    rk[u] = chunk_pref[static_cast<int64_t>(r >> 10) * M + rp[u]] + local_rank[r];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int r = r0 + u * kPlanThreads;
+                if (r < M) {
+                    const int pos = bufb[rp[u]] + rk[u];
+                    bufa[pos] = static_cast<uint16_t>(r);
+                    rank_pos[pos] = static_cast<uint16_t>(rk[u]);
+                }
+            }
+        }
+        src = bufa;
+        dst = rank_pos;
     }
     __syncthreads();
-#pragma unroll 1
-    for (int i = q0; i < q1; ++i) rep[src[i]] = (dst[i] % V) == 0 ? 1 : 0;  // leader flags by row
+    const bool vpow2 = (V & (V - 1)) == 0;
+    auto modV = [&](int x) { return vpow2 ? (x & (V - 1)) : x % V; };
+    for (int i = tid; i < M; i += kPlanThreads) rep[src[i]] = modV(dst[i]) == 0 ? 1 : 0;  // leader flags by row
     anyfail = __syncthreads_or(anyfail);
     if (anyfail) {  // (4) lexicographic argmin over the failing classes' representatives
 #pragma unroll 1
@@ -998,20 +1185,9 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
         best = best_s[0];
     }
     // (3) group number of each leader row: exclusive scan in row order
-    int nlead;
-    {
-        int cnt = 0;
-#pragma unroll 1
-        for (int r = q0; r < q1; ++r) cnt += rep[r];
-        int run = block_scan_1024(cnt, tmp, &nlead);
-#pragma unroll 1
-        for (int r = q0; r < q1; ++r) {
-            const int f = rep[r];
-            rep[r] = static_cast<uint16_t>(run);
-            run += f;
-        }
-    }
-    __syncthreads();
+    const int nlead = block_scan_rows(
+        M, [&](int r) { return static_cast<int>(rep[r]); },
+        [&](int r, int x) { rep[r] = static_cast<uint16_t>(x); }, tmp);
     int code = flags[0] ? SHFLBW_BAD_PARAMS
                         : (flags[1] ? SHFLBW_CUDA_ERROR : (anyfail ? SHFLBW_NONCONFORMANT_MASK : SHFLBW_OK));
     if (!row_indices) {
@@ -1022,22 +1198,30 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
         }
         return;
     }
+    // n_g is also kept in shared memory (free by now: the digit counters, or
+    // the segment starts) when it fits, so (6) does not re-read it through L2
+    int* ncs = local_rank ? reinterpret_cast<int*>(bufb) : reinterpret_cast<int*>(wcnt);
+    const bool ncs_ok = G <= (local_rank ? Mp / 2 : 32 * 256 / 2);
     if (nlead != G) {  // non-conformant: every output slot defined
         for (int i = tid; i < M; i += kPlanThreads) row_indices[i] = 0;
-        for (int g = tid; g < G; g += kPlanThreads) group_leader[g] = group_ncols[g] = 0;
+        for (int g = tid; g < G; g += kPlanThreads) {
+            group_leader[g] = group_ncols[g] = 0;
+            if (ncs_ok) ncs[g] = 0;
+        }
         __syncthreads();
     }
     // (5) assignment
-#pragma unroll 1
-    for (int i = q0; i < q1; ++i) {
-        const int slot = dst[i] % V;
+    for (int i = tid; i < M; i += kPlanThreads) {
+        const int slot = modV(dst[i]);
         const int lead_row = src[i - slot];
         const int g = rep[lead_row];
         if (g < G) {
             row_indices[static_cast<int64_t>(g) * V + slot] = src[i];
             if (slot == 0) {
+                const int n = popc[lead_row];
                 group_leader[g] = lead_row;
-                group_ncols[g] = popc[lead_row];
+                group_ncols[g] = n;
+                if (ncs_ok) ncs[g] = n;
             }
         }
     }
@@ -1047,7 +1231,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
     const int g0 = min(tid * PG, G), g1 = min(g0 + PG, G);
     int sum = 0, mx = 0;
     for (int g = g0; g < g1; ++g) {
-        const int pd = (group_ncols[g] + ktile - 1) / ktile * ktile;
+        const int pd = ((ncs_ok ? ncs[g] : group_ncols[g]) + ktile - 1) / ktile * ktile;
         sum += pd;
         mx = max(mx, pd);
     }
@@ -1055,7 +1239,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
     int run = block_scan_1024(sum, tmp, &total);
     for (int g = g0; g < g1; ++g) {
         group_ptr[g] = run;
-        run += (group_ncols[g] + ktile - 1) / ktile * ktile;
+        run += ((ncs_ok ? ncs[g] : group_ncols[g]) + ktile - 1) / ktile * ktile;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -1338,16 +1522,16 @@ int launch_pack_rows(const uint8_t* mask, int M, int K, int W, uint64_t seed, ui
 }
 
 // ---- hash planner host side (M <= kPlanMax) ---------------------------------
-// K1 k_pack_rows(+table insert) -> K2 k_class_check -> K3 k_plan (one CTA)
-// -> K4 k_pack_group: four launches and two memsets for any M up to 32768
-// (the sort-based pipeline: 12-30 launches).  Option "converter_legacy"
+// K1 k_pack_rows(+table insert) -> K2 k_class_check -> [k_chunk_rank ->
+// k_chunk_prefix, M > 4096] -> K3 k_plan (one CTA) -> K4 k_pack_group: four
+// (six) launches and two memsets (the sort-based pipeline: 12-30 launches).  Option "converter_legacy"
 // forces the sort-based pipeline (kept for M > kPlanMax).
 bool use_planner(int M, int V) {
     return M >= 1 && M <= kPlanMax && V >= 1 && option("converter_legacy") == 0;
 }
 
 struct HashPlan {
-    DevBuf words, popc, table, rep, csize, flags, leader;
+    DevBuf words, popc, table, rep, csize, flags, leader, chunks;
     ClassTable tab;
     int W = 1;
     size_t table_bytes = 0;
@@ -1365,6 +1549,10 @@ int hash_plan_alloc(HashPlan& p, int M, int K, int V, cudaStream_t s) {
     SBW_CUDA(p.csize.alloc(sizeof(uint32_t) * M, s));
     SBW_CUDA(p.flags.alloc(sizeof(uint32_t) * 4, s));
     SBW_CUDA(p.leader.alloc(sizeof(int32_t) * (M / V + 1), s));
+    if (M > kPlanSmall) {  // local ranks [M] + per-chunk class counts [chunks][M]
+        const size_t nchunks = (M + kPlanThreads - 1) / kPlanThreads;
+        SBW_CUDA(p.chunks.alloc(sizeof(uint16_t) * (((M + 127) & ~127) + nchunks * M), s));
+    }
     p.tab.key = p.table.as<uint64_t>();
     p.tab.minrow = reinterpret_cast<uint32_t*>(p.tab.key + P);
     p.tab.cnt = p.tab.minrow + P;
@@ -1385,12 +1573,24 @@ int hash_plan_run(HashPlan& p, const uint8_t* mask, int M, int K, int V, uint64_
     k_class_check<<<grid_for(M, 8), 256, 0, s>>>(p.words.as<uint64_t>(), M, p.W, p.tab, p.rep.as<uint32_t>(),
                                                  p.csize.as<uint32_t>(), p.flags.as<uint32_t>());
     SBW_LAUNCHED("k_class_check");
-    const size_t smem = static_cast<size_t>((M + 7) & ~7) * 6 + 32 * 256 * 2;
+    uint16_t* lrank = nullptr;
+    uint16_t* cpref = nullptr;
+    if (M > kPlanSmall) {
+        const int nchunks = (M + kPlanThreads - 1) / kPlanThreads;
+        lrank = p.chunks.as<uint16_t>();
+        cpref = lrank + ((M + 127) & ~127);
+        k_chunk_rank<<<nchunks, kPlanThreads, 0, s>>>(p.rep.as<uint32_t>(), M, lrank, cpref);
+        SBW_LAUNCHED("k_chunk_rank");
+        k_chunk_prefix<<<grid_for(M, 256), 256, 0, s>>>(p.rep.as<uint32_t>(), M, nchunks, cpref);
+        SBW_LAUNCHED("k_chunk_prefix");
+    }
+    const size_t smem = static_cast<size_t>((M + 7) & ~7) * (M > kPlanSmall ? 8 : 6) + (M > kPlanSmall ? 0 : 32 * 256 * 2);
     if (smem > 48 * 1024)  // per call: the attribute is per device
         SBW_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_plan<<<1, kPlanThreads, smem, s>>>(p.rep.as<uint32_t>(), p.csize.as<uint32_t>(), p.popc.as<int>(),
                                          p.words.as<uint64_t>(), M, p.W, V, SHFLBW_K_TILE, p.flags.as<uint32_t>(),
-                                         row_indices, p.leader.as<int32_t>(), group_ncols, group_ptr, status);
+                                         row_indices, p.leader.as<int32_t>(), group_ncols, group_ptr, status, lrank,
+                                         cpref);
     SBW_LAUNCHED("k_plan");
     return SHFLBW_OK;
 }

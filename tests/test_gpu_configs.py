@@ -2,10 +2,12 @@
 the planner actually picks for that shape (asserted with
 shflbw_cu_last_plan), against the oracle.
 
-  * compress_shflbw (src/formats.cpp:140-181) at M > 4096 (the converter's
-    multi-block radix sort): covered by test_gpu_parity.py's full-size digest
-    cases (16384 x 4096 V=64, 8192 x 2048 V=32, 8192 x 1024 V=128, pinned to
-    the compiled reference) plus a non-conformant M = 8192 mask here;
+  * compress_shflbw (src/formats.cpp:140-181) at M > 4096 (the planner's
+    chunked ranks; beyond M = 28672 the sort-based pipeline): covered by
+    test_gpu_parity.py's full-size digest cases (16384 x 4096 V=64, 8192 x
+    2048 V=32, 8192 x 1024 V=128, pinned to the compiled reference) plus a
+    non-conformant M = 8192 mask, planner-vs-sort-pipeline equality and an M
+    = 32768 case here;
   * the large-FFN SpMM (16384 x 4096, N = 8192, 75 %) run at full size with
     the auto plan (persistent kernel), column slices checked against
     oracle.spmm (spmm_execute, src/spmm.cpp:76-146) -- output columns are
@@ -246,3 +248,72 @@ def test_resnet50_b32_conv_auto_plan(sb, oracle, name, C, H, Kf, R, V):
         want = oracle.conv2d(p, np.ascontiguousarray(x[:, :, :, b0:b0 + 2]), R, R, 1, pad)
         for k, o in outs.items():
             assert oracle.rel_frobenius(np.ascontiguousarray(o[:, :, :, b0:b0 + 2]), want) <= TOL, (k, plan)
+
+
+# ------------------------------------------------- converter planner paths
+
+def _packing(a):
+    ri, gn, cols, vals = a.to_host()
+    gp, ci, vv = a.raw()
+    return [ri, gn, cols, vals.view(np.uint32), gp, ci, vv]
+
+
+@pytest.mark.parametrize("M,K,V,cpg", [(2048, 2048, 64, 512),    # one-CTA planner (CTA sort)
+                                       (8192, 1024, 32, 256),    # chunked ranks
+                                       (16384, 512, 64, 128),
+                                       (6144, 96, 3, 40),        # V not a power of two
+                                       (4096, 64, 1, 20),        # V = 1: G = M
+                                       (8192, 64, 1, 20)])
+def test_compress_planner_equals_sort_pipeline(sb, oracle, M, K, V, cpg):
+    """The class-table planner (default) and the sort-based pipeline
+    (option converter_legacy) give bit-identical matrices, equal to the
+    oracle (src/formats.cpp:140-181)."""
+    mask = oracle.random_shflbw_mask(M, K, V, cpg, oracle.rng(M + K + V))
+    W = oracle.round16(oracle.random_dense(M, K, 5))
+    a = sb.compress_shflbw(dev(W), dev(mask), V)
+    sb.set_option("converter_legacy", 1)
+    try:
+        b = sb.compress_shflbw(dev(W), dev(mask), V)
+    finally:
+        sb.set_option("converter_legacy", 0)
+    for x, y in zip(_packing(a), _packing(b)):
+        assert np.array_equal(x, y)
+    p = oracle.compress(W, mask, V)
+    ri, gn, cols, vals = a.to_host()
+    assert np.array_equal(ri, p.row_indices) and np.array_equal(gn, p.group_ncols)
+    assert np.array_equal(cols, p.cols)
+    assert np.array_equal(vals.view(np.uint32), oracle.round16(p.values).view(np.uint32))
+
+
+def test_compress_beyond_planner_m32768(sb, oracle):
+    """M = 32768 > the planner's shared-memory bound: the sort-based
+    pipeline, bit-exact against the oracle."""
+    M, K, V = 32768, 128, 64
+    mask = oracle.random_shflbw_mask(M, K, V, 40, oracle.rng(11))
+    W = oracle.round16(oracle.random_dense(M, K, 6))
+    a = sb.compress_shflbw(dev(W), dev(mask), V)
+    p = oracle.compress(W, mask, V)
+    ri, gn, cols, vals = a.to_host()
+    assert np.array_equal(ri, p.row_indices) and np.array_equal(gn, p.group_ncols)
+    assert np.array_equal(cols, p.cols)
+    assert np.array_equal(vals.view(np.uint32), oracle.round16(p.values).view(np.uint32))
+
+
+@pytest.mark.parametrize("M,K,V", [(2048, 256, 16), (12288, 256, 64)])
+def test_planner_nonconformant_both_paths(sb, oracle, M, K, V):
+    """A broken class: the planner and the sort pipeline report the oracle's
+    fail_row (lexicographically first failing class, smallest row)."""
+    mask = oracle.random_shflbw_mask(M, K, V, 60, oracle.rng(3))
+    rs = np.random.RandomState(M)
+    for _ in range(2):
+        mask[rs.randint(M), rs.randint(K)] ^= 1
+    want = oracle.validate(mask, V)
+    assert not want[0]
+    for legacy in (0, 1):
+        sb.set_option("converter_legacy", legacy)
+        try:
+            assert sb.validate_pattern(dev(mask), "shfl_bw", V) == (False, want[1])
+            with pytest.raises(sb.NonConformantMask, match=rf"\(row {want[1]}\)"):
+                sb.compress_shflbw(torch.zeros(M, K, device="cuda"), dev(mask), V)
+        finally:
+            sb.set_option("converter_legacy", 0)
