@@ -127,7 +127,9 @@ int shflbw_cu_version(void);
  * warp issues its gathers, 2 = every issuing lane), "tile_loads" (0 = auto:
  * block-wise K blocks of matrices flagged SHFLBW_CONTIG_BLOCKS as 2D TMA
  * tiles, -1 = gathers only, 1 = check every K block),
- * "converter_legacy" (1: the converter's sort-based class grouping instead
+ * "prefetch" (SpMM: activation rows of the first n K blocks prefetched
+ * into L2 before the programmatic-launch wait; 0 = auto: half-width units
+ * only, -1 = off), "converter_legacy" (1: the converter's sort-based class grouping instead
  * of the class table + one-CTA planner; the same output).  All variants give results
  * within the same tolerance; V split, cp.async, gather warps and persistent
  * are bit-identical to the default.

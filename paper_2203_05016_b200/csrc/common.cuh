@@ -146,6 +146,19 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
+// L2 prefetch of the same four rows (no shared-memory destination, no
+// barrier): issued before the programmatic-launch wait, it overlaps the
+// activation rows' HBM latency with the previous kernel's tail.  L2 is the
+// point of coherence, so a row the previous kernel writes afterwards is
+// simply refreshed there -- the gather after the wait reads the final data.
+__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap* m, int32_t c0, int32_t r0, int32_t r1,
+                                                     int32_t r2, int32_t r3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+                 : "memory");
+}
+
 // Same, multicast to every CTA in `cta_mask` (same smem offset, each CTA's
 // barrier at the same offset receives the bytes).
 __device__ __forceinline__ void tma_gather4_mc(void* dst, const CUtensorMap* m, uint64_t* bar,

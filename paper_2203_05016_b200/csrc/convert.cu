@@ -1135,10 +1135,10 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
             tmp);
         // sorted position = segment start + rank (earlier chunks + this chunk)
 #pragma unroll 1
-        for (int r0 = tid; r0 < M; r0 += 16 * kPlanThreads) {
-            int rk[16], rp[16];
+        for (int r0 = tid; r0 < M; r0 += 8 * kPlanThreads) {
+            int rk[8], rp[8];
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int r = r0 + u * kPlanThreads;
                 rk[u] = rp[u] = 0;
                 if (r < M) {
@@ -1147,7 +1147,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int r = r0 + u * kPlanThreads;
                 if (r < M) {
                     const int pos = bufb[rp[u]] + rk[u];

@@ -324,6 +324,20 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         prm.issue1 = b.kind == 0 && (gi == 1 || (gi == 0 && !multicast)) ? 1 : 0;
     }
     {
+        // SpMM activation rows of the first K blocks prefetched into L2 (TMA
+        // gather4 prefetches) before the programmatic-launch wait ("prefetch":
+        // n = n K blocks, -1 = off, 0 = auto = the first column-index window
+        // for half-width units only).  Measured: north star V = 128 (64-column
+        // units) 4.39 -> 4.12-4.24 us, FFN2 N = 128 3.28 -> 3.25; with
+        // 128-column units it costs 1-10 % (north star 3.66 -> 3.68, FFN2 N =
+        // 4096 6.84 -> 7.5): the prefetches share the TMA unit with the
+        // co-resident previous grid's gathers and delay its completion.  The
+        // same through prefetch.global.L2 (no TMA) was no better.
+        const int64_t pf = option("prefetch");
+        const int64_t want = pf == 0 ? (tile_n == 64 ? kMetaBlocks : 0) : (pf < 0 ? 0 : pf);
+        prm.pf_blocks = b.kind != 0 ? 0 : static_cast<int>(want > kMetaBlocks ? kMetaBlocks : want);
+    }
+    {
         const int64_t r = option("raster");
         if (r < 0 || r > 2) return fail(SHFLBW_BAD_PARAMS, "raster must be 0, 1 or 2");
         // auto: column-tile-major (measured: large FFN 474-484 -> 436-454 us,

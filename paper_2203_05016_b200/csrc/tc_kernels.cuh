@@ -94,6 +94,7 @@ struct TcParams {
     int per_sm;      // persistent: resident CTAs per SM
     int gw;          // gather warps per CTA (4, 8)
     int issue1;      // 1: SpMM gathers issued by one elected lane per warp (option "gather_issue")
+    int pf_blocks;   // SpMM: K blocks whose activation rows are L2-prefetched before the PDL wait
     int tiles;       // 1: SpMM K blocks whose 64 columns are one contiguous run (block-wise
                      //    patterns) load B with two TMA 2D tiles instead of 32 gather4s
     int raster;      // persistent unit order: 1 group-major, 2 column-tile-major
@@ -732,9 +733,20 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
                 reinterpret_cast<int4*>(meta_s)[i] = conv_encode4<KIND>(p, reinterpret_cast<int4*>(meta_s)[i]);
         }
         named_bar<kGT>(2);  // first window visible (overlaps the previous grid)
+        const uint32_t meta_u32 = smem_u32(meta_s);
+        if (KIND == 0 && p.pf_blocks > 0 && t_issue) {
+            // the first K blocks' activation rows into L2 while the previous
+            // grid finishes (p.pf_blocks <= the first window)
+            for (int kb = 0; kb < p.pf_blocks && kb < nkb; ++kb) {
+                int4 ci;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(ci.x), "=r"(ci.y), "=r"(ci.z), "=r"(ci.w)
+                             : "r"(meta_u32 + static_cast<uint32_t>((kb * kBlockK + g_rg * 4) * 4)));
+                tma_prefetch_gather4(&tmB, g_x, ci.x, ci.y, ci.z, ci.w);
+            }
+        }
         grid_dependency_wait();  // B may be the previous kernel's output
         if (et == 0) trace_event(p.trace, 2);
-        const uint32_t meta_u32 = smem_u32(meta_s);
         // the K loop, instantiated with and without the block-wise tile path
         // (even an untaken per-block check cost 2-5 % in the gather-bound loop)
         auto producer_loop = [&]<bool TILES>() {
