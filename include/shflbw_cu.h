@@ -129,7 +129,9 @@ int shflbw_cu_version(void);
  * tiles, -1 = gathers only, 1 = check every K block),
  * "prefetch" (SpMM: activation rows of the first n K blocks prefetched
  * into L2 before the programmatic-launch wait; 0 = auto: half-width units
- * only, -1 = off), "converter_legacy" (1: the converter's sort-based class grouping instead
+ * only, -1 = off), "pdl_trigger" (where the SpMM releases its successor
+ * under PDL: 1 = at entry, -1 = after the setup, 0 = auto: at entry for
+ * one-K-block CTAs), "converter_legacy" (1: the converter's sort-based class grouping instead
  * of the class table + one-CTA planner; the same output).  All variants give results
  * within the same tolerance; V split, cp.async, gather warps and persistent
  * are bit-identical to the default.

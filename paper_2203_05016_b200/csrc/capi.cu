@@ -13,7 +13,7 @@ namespace {
 thread_local std::string g_error;
 thread_local std::string g_plan;
 thread_local int64_t g_launches = 0;
-std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0}, g_pdl{1}, g_cps{0}, g_trace{0}, g_nobulk{0}, g_split_mode{0}, g_persist{0}, g_gw{0}, g_strict{0}, g_raster{0}, g_tile_n{0}, g_issue{0}, g_tiles{0}, g_conv_legacy{0}, g_prefetch{0};
+std::atomic<int64_t> g_force_simt{0}, g_split{0}, g_stages{0}, g_pdl{1}, g_cps{0}, g_trace{0}, g_nobulk{0}, g_split_mode{0}, g_persist{0}, g_gw{0}, g_strict{0}, g_raster{0}, g_tile_n{0}, g_issue{0}, g_tiles{0}, g_conv_legacy{0}, g_prefetch{0}, g_trigger{0};
 }  // namespace
 
 void set_error(const std::string& msg) { g_error = msg; }
@@ -46,6 +46,7 @@ int64_t option(const char* key) {
     if (!std::strcmp(key, "tile_loads")) return g_tiles.load();
     if (!std::strcmp(key, "converter_legacy")) return g_conv_legacy.load();
     if (!std::strcmp(key, "prefetch")) return g_prefetch.load();
+    if (!std::strcmp(key, "pdl_trigger")) return g_trigger.load();
     return 0;
 }
 
@@ -149,6 +150,7 @@ int shflbw_cu_set_option(const char* key, int64_t value) {
     else if (!std::strcmp(key, "tile_loads")) g_tiles = value;
     else if (!std::strcmp(key, "converter_legacy")) g_conv_legacy = value;
     else if (!std::strcmp(key, "prefetch")) g_prefetch = value;
+    else if (!std::strcmp(key, "pdl_trigger")) g_trigger = value;
     else return fail(SHFLBW_BAD_PARAMS, std::string("unknown option ") + key);
     return SHFLBW_OK;
 }

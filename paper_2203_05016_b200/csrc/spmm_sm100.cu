@@ -336,6 +336,15 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         const int64_t pf = option("prefetch");
         const int64_t want = pf == 0 ? (tile_n == 64 ? kMetaBlocks : 0) : (pf < 0 ? 0 : pf);
         prm.pf_blocks = b.kind != 0 ? 0 : static_cast<int>(want > kMetaBlocks ? kMetaBlocks : want);
+        // PDL trigger ("pdl_trigger": 1 = at kernel entry, -1 = after the
+        // setup, 0 = auto): at entry only for one-K-block CTAs, whose whole
+        // main loop is one gather -- there the successor's earlier prologue
+        // pays (GNMT 95 % 2.97 -> 2.67 us); with longer main loops the early
+        // successor CTAs slow this grid (north star 3.63 -> 3.88, GNMT 90 %
+        // 2.86 -> 3.02, GNMT 50 % 4.57 -> 5.3)
+        const int64_t trg = option("pdl_trigger");
+        const int kb_cta = (kb_grp + ksf - 1) / ksf;
+        prm.trigger_early = trg == 1 || (trg == 0 && kb_cta <= 1) ? 1 : 0;
     }
     {
         const int64_t r = option("raster");

@@ -95,6 +95,7 @@ struct TcParams {
     int gw;          // gather warps per CTA (4, 8)
     int issue1;      // 1: SpMM gathers issued by one elected lane per warp (option "gather_issue")
     int pf_blocks;   // SpMM: K blocks whose activation rows are L2-prefetched before the PDL wait
+    int trigger_early;  // 1: griddepcontrol.launch_dependents at entry instead of after the setup
     int tiles;       // 1: SpMM K blocks whose 64 columns are one contiguous run (block-wise
                      //    patterns) load B with two TMA 2D tiles instead of 32 gather4s
     int raster;      // persistent unit order: 1 group-major, 2 column-tile-major
@@ -589,7 +590,10 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     const int cps = p.cps;
     constexpr int kGT = 32 * GW;      // gather threads
     const int et = threadIdx.x - 64;  // gather thread 0..kGT-1 (epilogue: et < 128)
-    if (threadIdx.x == 0) trace_event(p.trace, 0);
+    if (threadIdx.x == 0) {
+        trace_event(p.trace, 0);
+        if (p.trigger_early) grid_launch_dependents();
+    }
     // first window of column indices (static data): cp.async right at entry,
     // so its latency overlaps the barrier / TMEM / cluster setup
     const int nb0 = nkb < kMetaBlocks ? nkb : kMetaBlocks;
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(64 + 32 * GW, GW > 4 ? 2 : 1)
     tc_fence_after();
     const uint32_t tmem_d = *tmem_slot;
     if (threadIdx.x == 0) {
-        grid_launch_dependents();
+        if (!p.trigger_early) grid_launch_dependents();
         trace_event(p.trace, 1);
     }
 
