@@ -17,6 +17,11 @@ ncu --set full --clock-control none --import-source on -k regex:k_spmm -s 10 -c 
 ncu --set full --clock-control none --import-source on -k regex:k_spmm -s 3 -c 1 -o gpurun_out/prof_lf_$T $P --workload lf > gpurun_out/ncu_lf.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_spmm -s 10 -c 1 -o gpurun_out/prof_ffn_$T $P --workload ffn > gpurun_out/ncu_ffn.log 2>&1
 echo "ncu rc $?"
+# converter: warm timings, launch list, full captures of the large-FFN pack / plan / pack kernels
+python scripts/compress_probe.py > gpurun_out/compress_probe_$T.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_conv_$T.csv python scripts/compress_kernels.py > gpurun_out/ncu_conv_l.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_pack_rows16|k_pack_group|k_plan" -s 6 -c 3 -o gpurun_out/prof_conv_$T python scripts/compress_kernels.py > gpurun_out/ncu_conv.log 2>&1
+echo "ncu conv rc $?"
 # reports -> csv pages (the .ncu-rep files would overflow the 64 MiB return)
 for r in gpurun_out/prof_*_$T.ncu-rep; do
   b=${r%.ncu-rep}

@@ -84,16 +84,17 @@ def main():
     for arg in sys.argv[2:]:
         wl, rep = arg.split("=", 1)
         res = summarise(rep)
-        if not res:
-            continue
-        d = res[0]
-        d["source"] = f"ncu --set full --clock-control none, {os.path.basename(rep)} ({tag})"
-        allp[wl] = d
-        lines.append(f"| {wl} | {d['kernel'][:60]} | {d.get('duration', 0):.2f} | {d['dram_bytes_per_launch'] / 1e6:.2f} | "
-                     f"{d.get('dram_gbs', 0):.0f} ({d.get('dram_frac_of_measured_peak', 0):.3f}) | "
-                     f"{d.get('tensor_pipe_util_pct', 0):.2f} | {d.get('l2_throughput_pct', 0):.1f} | "
-                     f"{d.get('l2_hit_rate_pct', 0):.1f} | {d.get('dram_throughput_pct', 0):.1f} | "
-                     f"{int(d.get('grid', 0))} | {int(d.get('cluster', 0))} |")
+        for d in res:  # several kernels in one capture: workload:kernel
+            key = wl
+            if len(res) > 1:
+                key = wl + ":" + d["kernel"].split("(")[0].replace("sbw::<unnamed>::", "").replace("void ", "").split("<")[0].split("::")[-1]
+            d["source"] = f"ncu --set full --clock-control none, {os.path.basename(rep)} ({tag})"
+            allp[key] = d
+            lines.append(f"| {key} | {d['kernel'][:60]} | {d.get('duration', 0):.2f} | {d['dram_bytes_per_launch'] / 1e6:.2f} | "
+                         f"{d.get('dram_gbs', 0):.0f} ({d.get('dram_frac_of_measured_peak', 0):.3f}) | "
+                         f"{d.get('tensor_pipe_util_pct', 0):.2f} | {d.get('l2_throughput_pct', 0):.1f} | "
+                         f"{d.get('l2_hit_rate_pct', 0):.1f} | {d.get('dram_throughput_pct', 0):.1f} | "
+                         f"{int(d.get('grid', 0))} | {int(d.get('cluster', 0))} |")
     json.dump(allp, open(path, "w"), indent=1)
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
