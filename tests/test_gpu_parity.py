@@ -1037,6 +1037,62 @@ def test_persistent_raster_orders_bitwise(sb, oracle, V):
     assert oracle.rel_frobenius(outs[2][:, :128], oracle.spmm(p, np.ascontiguousarray(B[:, :128]))) <= TOL
 
 
+@pytest.mark.parametrize("M,K,V,alpha", [(2048, 2048, 64, 0.25),   # 2 x 2 cluster, 4 K blocks per CTA
+                                         (4096, 1024, 64, 0.05),   # one K block per CTA
+                                         (2048, 2048, 128, 0.25)])  # half-width units
+def test_prefetch_and_pdl_trigger_bitwise(sb, oracle, M, K, V, alpha):
+    """The L2 prefetch of activation rows before the PDL wait and the PDL
+    trigger position change only timing: identical bits for every setting."""
+    N = 128
+    mask, W, B = synthetic(oracle, M, K, N, V, alpha)
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    outs = []
+    for pf in (-1, 0, 16):
+        for trig in (-1, 1):
+            sb.set_option("prefetch", pf)
+            sb.set_option("pdl_trigger", trig)
+            outs.append(sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy())
+            assert sb.last_plan().startswith("k_spmm_tc"), sb.last_plan()
+    sb.set_option("prefetch", 0)
+    sb.set_option("pdl_trigger", 0)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    assert oracle.rel_frobenius(outs[0], oracle.spmm(p, B)) <= 1e-2  # bf16 output
+
+
+@pytest.mark.parametrize("pf,trig", [(16, 1), (16, -1), (-1, 1), (0, 0)])
+def test_pdl_chain_consumes_predecessor_output(sb, oracle, pf, trig):
+    """Back-to-back SpMMs where each consumes the previous one's output (a
+    layer chain: the true data dependency PDL must honour).  With the
+    activation prefetch issued before the wait and the trigger at entry, the
+    chained results equal the same SpMMs run with a full synchronisation in
+    between."""
+    M = K = 2048
+    N, V = 128, 64
+    mats = []
+    for i in range(3):
+        mask, W, _ = synthetic(oracle, M, K, N, V, 0.25, seed=40 + i)
+        mats.append(sb.compress_shflbw(dev(W), dev(mask), V))
+    B0 = dev(oracle.round16(np.random.RandomState(9).uniform(-1, 1, (K, N)).astype(np.float32)), torch.bfloat16)
+    sb.set_option("prefetch", pf)
+    sb.set_option("pdl_trigger", trig)
+    try:
+        x = B0
+        for a in mats:  # enqueued back to back, no host sync
+            x = sb.spmm_execute(a, x, out_dtype=torch.bfloat16)
+        chained = x.float().cpu().numpy()
+        x = B0
+        for a in mats:
+            x = sb.spmm_execute(a, x, out_dtype=torch.bfloat16)
+            torch.cuda.synchronize()
+        serial = x.float().cpu().numpy()
+    finally:
+        sb.set_option("prefetch", 0)
+        sb.set_option("pdl_trigger", 0)
+    assert np.array_equal(chained, serial)
+
+
 # ------------------------------------------------- asynchronous converter (round 2)
 
 @pytest.mark.parametrize("M,K,V,alpha", [(2048, 2048, 64, 0.25), (4096, 1024, 32, 0.25), (8192, 1024, 128, 0.1),
