@@ -261,7 +261,7 @@ def _packing(a):
 @pytest.mark.parametrize("M,K,V,cpg", [(2048, 2048, 64, 512),    # one-CTA planner (CTA sort)
                                        (8192, 1024, 32, 256),    # chunked ranks
                                        (16384, 512, 64, 128),
-                                       (6144, 96, 3, 40),        # V not a power of two
+                                       (6144, 100, 3, 40),       # V not a power of two, K % 16 != 0
                                        (4096, 64, 1, 20),        # V = 1: G = M
                                        (8192, 64, 1, 20)])
 def test_compress_planner_equals_sort_pipeline(sb, oracle, M, K, V, cpg):
@@ -317,3 +317,25 @@ def test_planner_nonconformant_both_paths(sb, oracle, M, K, V):
                 sb.compress_shflbw(torch.zeros(M, K, device="cuda"), dev(mask), V)
         finally:
             sb.set_option("converter_legacy", 0)
+
+
+@pytest.mark.parametrize("M,K,V", [(2048, 300, 64), (8192, 256, 256), (1024, 64, 16)])
+@pytest.mark.parametrize("din", ["f32", "bf16", "f16"])
+@pytest.mark.parametrize("dout", ["bf16", "f16", "f32"])
+def test_compress_value_dtypes(sb, oracle, M, K, V, din, dout):
+    """Every (dense dtype, value dtype) pair through the fused pack kernel (V
+    <= 128) and the wide-group pack path (V = 256): values are the dense
+    entries converted with round-to-nearest-even, columns and row indices
+    bit-exact against the oracle."""
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16}
+    mask = oracle.random_shflbw_mask(M, K, V, K // 4, oracle.rng(M + V))
+    Wf = oracle.random_dense(M, K, 3)
+    Wd = torch.from_numpy(Wf).cuda().to(tdt[din])
+    a = sb.compress_shflbw(Wd, dev(mask), V, dtype=tdt[dout])
+    Win = Wd.float().cpu().numpy()  # what the converter read
+    p = oracle.compress(Win, mask, V)
+    ri, gn, cols, vals = a.to_host()
+    assert np.array_equal(ri, p.row_indices) and np.array_equal(gn, p.group_ncols)
+    assert np.array_equal(cols, p.cols)
+    want = torch.from_numpy(np.ascontiguousarray(p.values)).to(tdt[dout]).float().numpy()
+    assert np.array_equal(vals, want)
