@@ -5,7 +5,7 @@
 //
 // The reference groups rows by exact mask-row equality with a std::map keyed
 // by the whole row (src/formats.cpp:40-46), cuts each class into V-row chunks
-// of ascending rows and orders the chunks by first row.  Here (M <= 28672):
+// of ascending rows and orders the chunks by first row.  Here (M <= 32768):
 //
 //   K1 k_pack_rows   one warp per row: the mask row becomes 64-bit words with
 //                    column 0 as the MSB of word 0 (so unsigned word order is
@@ -770,7 +770,7 @@ __global__ void k_class_check(const uint64_t* __restrict__ words, int M, int W, 
 }
 
 constexpr int kPlanThreads = 1024;
-constexpr int kPlanMax = 28672;                      // rows: four 16-bit arrays of M in shared memory
+constexpr int kPlanMax = 32768;                      // rows: 16-bit row ids, <= 32 chunks of 1024
 constexpr int kPlanSmall = 4096;                     // above: chunked ranks (k_chunk_rank) instead of the CTA sort
 
 // exclusive scan of one int per thread over a 1024-thread block; *total =
@@ -963,8 +963,9 @@ __device__ __forceinline__ uint16_t* block_sort16(const uint16_t* key, uint16_t*
 // representative; rank of each row among its class's rows in the chunk, and
 // the class's row count in the chunk: cnt[chunk][rep] (zero elsewhere).
 __global__ void __launch_bounds__(kPlanThreads, 1)
-    k_chunk_rank(const uint32_t* __restrict__ rep_by_row, int M, uint16_t* __restrict__ local_rank,
-                 uint16_t* __restrict__ cnt) {
+    k_chunk_rank(const uint32_t* __restrict__ rep_by_row, const uint32_t* __restrict__ csize, int M, int V,
+                 uint16_t* __restrict__ local_rank, uint16_t* __restrict__ cnt, uint16_t* __restrict__ seg_local,
+                 int* __restrict__ chunk_seg, uint32_t* __restrict__ flags) {
     __shared__ uint16_t key[kPlanThreads], a[kPlanThreads], b[kPlanThreads];
     __shared__ uint16_t wcnt[32 * 256];
     __shared__ int tmp[33];
@@ -973,9 +974,25 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
     const int n = min(kPlanThreads, M - r0);
     uint16_t* crow = cnt + static_cast<int64_t>(blockIdx.x) * M;
     for (int i = tid; i < M; i += kPlanThreads) crow[i] = 0;
-    if (tid < n) key[tid] = static_cast<uint16_t>(rep_by_row[r0 + tid]);
+    int cs = 0;
+    bool isrep = false;
+    if (tid < n) {
+        const uint32_t rp = rep_by_row[r0 + tid];
+        key[tid] = static_cast<uint16_t>(rp);
+        isrep = rp == static_cast<uint32_t>(r0 + tid);
+        if (isrep) {
+            cs = static_cast<int>(csize[r0 + tid]);
+            if (cs % V != 0) atomicOr(&flags[2], 1u);  // a failing class
+        }
+    }
     a[tid] = static_cast<uint16_t>(tid);
-    __syncthreads();
+    {   // class segments start at the exclusive scan, in row order, of the
+        // representatives' class sizes: this chunk's part
+        int total;
+        const int ex = block_scan_1024(cs, tmp, &total);
+        if (isrep) seg_local[r0 + tid] = static_cast<uint16_t>(ex);
+        if (tid == 0) chunk_seg[blockIdx.x] = total;
+    }
     const uint16_t* srt = block_sort16(key, a, b, n, 32 - __clz(M - 1), wcnt, tmp);
     const int i = tid;
     int k = -1, head = -1;
@@ -1028,6 +1045,164 @@ __global__ void k_chunk_prefix(const uint32_t* __restrict__ rep_by_row, int M, i
     }
 }
 
+// exclusive scan of v[0..n) (n <= 32) into out[0..n) by warp 0 (smem)
+__device__ __forceinline__ void warp0_scan_small(const int* __restrict__ v, int n, int* out) {
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        const int x = lane < n ? v[lane] : 0;
+        int incl = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        out[lane] = incl - x;
+    }
+    __syncthreads();
+}
+
+// K3c (chunked planner): every row's rank in its class (earlier chunks +
+// this chunk) and its position in the (representative, row) order -- the
+// class's segment start + rank; leader flags (rank % V == 0) numbered within
+// the chunk in row order.  Also clears this chunk's share of the outputs, so
+// a non-conformant mask leaves every slot defined.
+__global__ void __launch_bounds__(kPlanThreads, 1)
+    k_chunk_place(const uint32_t* __restrict__ rep_by_row, const uint16_t* __restrict__ local_rank,
+                  const uint16_t* __restrict__ cnt, const uint16_t* __restrict__ seg_local,
+                  const int* __restrict__ chunk_seg, int M, int V, int nchunks, uint16_t* __restrict__ srt,
+                  uint16_t* __restrict__ rank_pos, uint16_t* __restrict__ gid_local, int* __restrict__ chunk_lead,
+                  int32_t* __restrict__ row_indices, int32_t* __restrict__ group_leader,
+                  int32_t* __restrict__ group_ncols) {
+    __shared__ int seg_off[32];
+    __shared__ int tmp[33];
+    const int tid = threadIdx.x;
+    const int r0 = blockIdx.x * kPlanThreads;
+    const int r = r0 + tid;
+    const int G = M / V;
+    warp0_scan_small(chunk_seg, nchunks, seg_off);
+    bool lead = false;
+    if (r < M) {
+        const int rp = static_cast<int>(rep_by_row[r]);
+        const int rank = cnt[static_cast<int64_t>(r >> 10) * M + rp] + local_rank[r];
+        const int pos = seg_off[rp >> 10] + seg_local[rp] + rank;
+        srt[pos] = static_cast<uint16_t>(r);
+        rank_pos[pos] = static_cast<uint16_t>(rank);
+        lead = rank % V == 0;
+        row_indices[r] = 0;
+    }
+    const int GB = (G + nchunks - 1) / nchunks;
+    for (int g = blockIdx.x * GB + tid; g < min(G, (blockIdx.x + 1) * GB); g += kPlanThreads)
+        group_leader[g] = group_ncols[g] = 0;
+    int total;
+    const int ex = block_scan_1024(lead ? 1 : 0, tmp, &total);
+    if (lead) gid_local[r] = static_cast<uint16_t>(ex);
+    if (tid == 0) chunk_lead[blockIdx.x] = total;
+}
+
+// K3d (chunked planner): sorted positions i of this chunk -> row_indices[g *
+// V + slot]; g = the leader's group number (chunks before it + its number in
+// its chunk); leaders also write group_leader / n_g.
+__global__ void __launch_bounds__(kPlanThreads, 1)
+    k_chunk_assign(const uint16_t* __restrict__ srt, const uint16_t* __restrict__ rank_pos,
+                   const uint16_t* __restrict__ gid_local, const int* __restrict__ chunk_lead,
+                   const int* __restrict__ popc, int M, int V, int nchunks, int32_t* __restrict__ row_indices,
+                   int32_t* __restrict__ group_leader, int32_t* __restrict__ group_ncols) {
+    __shared__ int lead_off[32];
+    warp0_scan_small(chunk_lead, nchunks, lead_off);
+    const int i = blockIdx.x * kPlanThreads + threadIdx.x;
+    if (i >= M) return;
+    const int G = M / V;
+    const int slot = rank_pos[i] % V;
+    const int lead_row = srt[i - slot];
+    const int g = lead_off[lead_row >> 10] + gid_local[lead_row];
+    if (g < G) {
+        row_indices[static_cast<int64_t>(g) * V + slot] = srt[i];
+        if (slot == 0) {
+            group_leader[g] = lead_row;
+            group_ncols[g] = popc[lead_row];
+        }
+    }
+}
+
+// K3e (chunked planner, one CTA): group_ptr = exclusive scan of
+// roundup(n_g, ktile), widest group, status; the lexicographically smallest
+// failing class's smallest row when a chunk flagged one (flags[2]).
+// row_indices == nullptr: validation only.
+__global__ void __launch_bounds__(kPlanThreads, 1)
+    k_plan_finish(const uint32_t* __restrict__ rep_by_row, const uint32_t* __restrict__ csize,
+                  const uint64_t* __restrict__ words, int M, int W, int V, int ktile,
+                  const uint32_t* __restrict__ flags, const int32_t* __restrict__ row_indices,
+                  const int32_t* __restrict__ group_ncols, int32_t* __restrict__ group_ptr,
+                  int32_t* __restrict__ status) {
+    __shared__ int tmp[33];
+    __shared__ int best_s[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool anyfail = flags[2] != 0;
+    int best = -1;
+    if (anyfail) {
+        for (int r = tid; r < M; r += kPlanThreads)
+            if (rep_by_row[r] == static_cast<uint32_t>(r) && csize[r] % static_cast<uint32_t>(V) != 0 &&
+                row_less(words, W, r, best))
+                best = r;
+#pragma unroll 1
+        for (int o = 16; o; o >>= 1) {
+            const int other = __shfl_down_sync(0xffffffffu, best, o);
+            if (lane < o && row_less(words, W, other, best)) best = other;
+        }
+        if (lane == 0) best_s[warp] = best;
+        __syncthreads();
+        if (warp == 0) {
+            best = best_s[lane];
+#pragma unroll 1
+            for (int o = 16; o; o >>= 1) {
+                const int other = __shfl_down_sync(0xffffffffu, best, o);
+                if (lane < o && row_less(words, W, other, best)) best = other;
+            }
+            if (lane == 0) best_s[0] = best;
+        }
+        __syncthreads();
+        best = best_s[0];
+    }
+    const int code = flags[0] ? SHFLBW_BAD_PARAMS
+                              : (flags[1] ? SHFLBW_CUDA_ERROR : (anyfail ? SHFLBW_NONCONFORMANT_MASK : SHFLBW_OK));
+    if (!row_indices) {
+        if (tid == 0) {
+            status[0] = code;
+            status[1] = anyfail ? best : 0;
+            status[2] = status[3] = 0;
+        }
+        return;
+    }
+    const int G = M / V;
+    const int PG = (G + kPlanThreads - 1) / kPlanThreads;
+    const int g0 = min(tid * PG, G), g1 = min(g0 + PG, G);
+    int sum = 0, mx = 0;
+    for (int g = g0; g < g1; ++g) {
+        const int pd = (group_ncols[g] + ktile - 1) / ktile * ktile;
+        sum += pd;
+        mx = max(mx, pd);
+    }
+    int total;
+    int run = block_scan_1024(sum, tmp, &total);
+    for (int g = g0; g < g1; ++g) {
+        group_ptr[g] = run;
+        run += (group_ncols[g] + ktile - 1) / ktile * ktile;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) best_s[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+        int m = 0;
+        for (int w = 0; w < 32; ++w) m = max(m, best_s[w]);
+        group_ptr[G] = total;
+        status[0] = code;
+        status[1] = anyfail ? best : 0;
+        status[2] = total;
+        status[3] = m;
+    }
+}
+
 // K3, one CTA: (1) stable LSD sort of the rows by representative in shared
 // memory (8-bit digits, per-warp digit counts, match_any ranks) -- classes
 // become runs of ascending rows, like the reference's std::map buckets
@@ -1043,8 +1218,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
     k_plan(const uint32_t* __restrict__ rep_by_row, const uint32_t* __restrict__ csize, const int* __restrict__ popc,
            const uint64_t* __restrict__ words, int M, int W, int V, int ktile, const uint32_t* __restrict__ flags,
            int32_t* __restrict__ row_indices, int32_t* __restrict__ group_leader, int32_t* __restrict__ group_ncols,
-           int32_t* __restrict__ group_ptr, int32_t* __restrict__ status, const uint16_t* __restrict__ local_rank,
-           const uint16_t* __restrict__ chunk_pref) {
+           int32_t* __restrict__ group_ptr, int32_t* __restrict__ status) {
     extern __shared__ __align__(16) unsigned char sm_plan[];
     const int Mp = (M + 7) & ~7;
     uint16_t* rep = reinterpret_cast<uint16_t*>(sm_plan);  // rep by row, later rank by sorted position
@@ -1069,7 +1243,7 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
     bool anyfail = false;
     uint16_t* src;
     uint16_t* dst;
-    if (!local_rank) {
+    {
         src = block_sort16(rep, bufa, bufb, M, M > 1 ? 32 - __clz(M - 1) : 0, wcnt, tmp);
         dst = src == bufa ? bufb : bufa;
         // a run (class) starts where the row is its own representative; rank
@@ -1115,49 +1289,6 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
             if (rep[row] == row) cur = i;
             dst[i] = static_cast<uint16_t>(i - cur);
         }
-    } else {
-        // class segments in representative order: exclusive scan over rows of
-        // (row is a representative) * class size (csize staged in bufa);
-        // failing classes found on the way
-        uint16_t* rank_pos = bufb + Mp;  // the 4th array (no digit counters here)
-        load_u16(csize, M, bufa);
-        __syncthreads();
-        for (int r = tid; r < M; r += kPlanThreads)
-            if (rep[r] == r && bufa[r] % V != 0) {
-                anyfail = true;
-                if (row_less(words, W, r, best)) best = r;
-            }
-        block_scan_rows(
-            M, [&](int r) { return rep[r] == r ? static_cast<int>(bufa[r]) : 0; },
-            [&](int r, int x) {
-                if (rep[r] == r) bufb[r] = static_cast<uint16_t>(x);
-            },
-            tmp);
-        // sorted position = segment start + rank (earlier chunks + this chunk)
-#pragma unroll 1
-        for (int r0 = tid; r0 < M; r0 += 8 * kPlanThreads) {
-            int rk[8], rp[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int r = r0 + u * kPlanThreads;
-                rk[u] = rp[u] = 0;
-                if (r < M) {
-                    rp[u] = rep[r];
-                    rk[u] = chunk_pref[static_cast<int64_t>(r >> 10) * M + rp[u]] + local_rank[r];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int r = r0 + u * kPlanThreads;
-                if (r < M) {
-                    const int pos = bufb[rp[u]] + rk[u];
-                    bufa[pos] = static_cast<uint16_t>(r);
-                    rank_pos[pos] = static_cast<uint16_t>(rk[u]);
-                }
-            }
-        }
-        src = bufa;
-        dst = rank_pos;
     }
     __syncthreads();
     const bool vpow2 = (V & (V - 1)) == 0;
@@ -1200,8 +1331,8 @@ __global__ void __launch_bounds__(kPlanThreads, 1)
     }
     // n_g is also kept in shared memory (free by now: the digit counters, or
     // the segment starts) when it fits, so (6) does not re-read it through L2
-    int* ncs = local_rank ? reinterpret_cast<int*>(bufb) : reinterpret_cast<int*>(wcnt);
-    const bool ncs_ok = G <= (local_rank ? Mp / 2 : 32 * 256 / 2);
+    int* ncs = reinterpret_cast<int*>(wcnt);
+    const bool ncs_ok = G <= 32 * 256 / 2;
     if (nlead != G) {  // non-conformant: every output slot defined
         for (int i = tid; i < M; i += kPlanThreads) row_indices[i] = 0;
         for (int g = tid; g < G; g += kPlanThreads) {
@@ -1549,9 +1680,10 @@ int hash_plan_alloc(HashPlan& p, int M, int K, int V, cudaStream_t s) {
     SBW_CUDA(p.csize.alloc(sizeof(uint32_t) * M, s));
     SBW_CUDA(p.flags.alloc(sizeof(uint32_t) * 4, s));
     SBW_CUDA(p.leader.alloc(sizeof(int32_t) * (M / V + 1), s));
-    if (M > kPlanSmall) {  // local ranks [M] + per-chunk class counts [chunks][M]
+    if (M > kPlanSmall) {  // five [M] u16 arrays + per-chunk class counts [chunks][M] + chunk sums
         const size_t nchunks = (M + kPlanThreads - 1) / kPlanThreads;
-        SBW_CUDA(p.chunks.alloc(sizeof(uint16_t) * (((M + 127) & ~127) + nchunks * M), s));
+        const size_t Mp = (static_cast<size_t>(M) + 127) & ~size_t(127);
+        SBW_CUDA(p.chunks.alloc(sizeof(uint16_t) * (5 * Mp + nchunks * M + 128) + 64 * sizeof(int), s));
     }
     p.tab.key = p.table.as<uint64_t>();
     p.tab.minrow = reinterpret_cast<uint32_t*>(p.tab.key + P);
@@ -1573,24 +1705,47 @@ int hash_plan_run(HashPlan& p, const uint8_t* mask, int M, int K, int V, uint64_
     k_class_check<<<grid_for(M, 8), 256, 0, s>>>(p.words.as<uint64_t>(), M, p.W, p.tab, p.rep.as<uint32_t>(),
                                                  p.csize.as<uint32_t>(), p.flags.as<uint32_t>());
     SBW_LAUNCHED("k_class_check");
-    uint16_t* lrank = nullptr;
-    uint16_t* cpref = nullptr;
     if (M > kPlanSmall) {
+        // chunked planner: 1024-row chunks ranked in parallel, one small CTA
+        // for the group offsets and the status
         const int nchunks = (M + kPlanThreads - 1) / kPlanThreads;
-        lrank = p.chunks.as<uint16_t>();
-        cpref = lrank + ((M + 127) & ~127);
-        k_chunk_rank<<<nchunks, kPlanThreads, 0, s>>>(p.rep.as<uint32_t>(), M, lrank, cpref);
+        const size_t Mp = (static_cast<size_t>(M) + 127) & ~size_t(127);
+        uint16_t* lrank = p.chunks.as<uint16_t>();
+        uint16_t* seg_local = lrank + Mp;
+        uint16_t* srt = seg_local + Mp;
+        uint16_t* rank_pos = srt + Mp;
+        uint16_t* gid_local = rank_pos + Mp;
+        uint16_t* cnt = gid_local + Mp;
+        int* chunk_seg = reinterpret_cast<int*>(
+            (reinterpret_cast<uintptr_t>(cnt + static_cast<size_t>(nchunks) * M) + 15) & ~static_cast<uintptr_t>(15));
+        int* chunk_lead = chunk_seg + 32;
+        k_chunk_rank<<<nchunks, kPlanThreads, 0, s>>>(p.rep.as<uint32_t>(), p.csize.as<uint32_t>(), M, V, lrank, cnt,
+                                                      seg_local, chunk_seg, p.flags.as<uint32_t>());
         SBW_LAUNCHED("k_chunk_rank");
-        k_chunk_prefix<<<grid_for(M, 256), 256, 0, s>>>(p.rep.as<uint32_t>(), M, nchunks, cpref);
-        SBW_LAUNCHED("k_chunk_prefix");
+        if (row_indices) {
+            k_chunk_prefix<<<grid_for(M, 256), 256, 0, s>>>(p.rep.as<uint32_t>(), M, nchunks, cnt);
+            SBW_LAUNCHED("k_chunk_prefix");
+            k_chunk_place<<<nchunks, kPlanThreads, 0, s>>>(p.rep.as<uint32_t>(), lrank, cnt, seg_local, chunk_seg, M, V,
+                                                           nchunks, srt, rank_pos, gid_local, chunk_lead, row_indices,
+                                                           p.leader.as<int32_t>(), group_ncols);
+            SBW_LAUNCHED("k_chunk_place");
+            k_chunk_assign<<<nchunks, kPlanThreads, 0, s>>>(srt, rank_pos, gid_local, chunk_lead, p.popc.as<int>(), M,
+                                                            V, nchunks, row_indices, p.leader.as<int32_t>(),
+                                                            group_ncols);
+            SBW_LAUNCHED("k_chunk_assign");
+        }
+        k_plan_finish<<<1, kPlanThreads, 0, s>>>(p.rep.as<uint32_t>(), p.csize.as<uint32_t>(), p.words.as<uint64_t>(),
+                                                 M, p.W, V, SHFLBW_K_TILE, p.flags.as<uint32_t>(), row_indices,
+                                                 group_ncols, group_ptr, status);
+        SBW_LAUNCHED("k_plan_finish");
+        return SHFLBW_OK;
     }
-    const size_t smem = static_cast<size_t>((M + 7) & ~7) * (M > kPlanSmall ? 8 : 6) + (M > kPlanSmall ? 0 : 32 * 256 * 2);
+    const size_t smem = static_cast<size_t>((M + 7) & ~7) * 6 + 32 * 256 * 2;
     if (smem > 48 * 1024)  // per call: the attribute is per device
         SBW_CUDA(cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_plan<<<1, kPlanThreads, smem, s>>>(p.rep.as<uint32_t>(), p.csize.as<uint32_t>(), p.popc.as<int>(),
                                          p.words.as<uint64_t>(), M, p.W, V, SHFLBW_K_TILE, p.flags.as<uint32_t>(),
-                                         row_indices, p.leader.as<int32_t>(), group_ncols, group_ptr, status, lrank,
-                                         cpref);
+                                         row_indices, p.leader.as<int32_t>(), group_ncols, group_ptr, status);
     SBW_LAUNCHED("k_plan");
     return SHFLBW_OK;
 }

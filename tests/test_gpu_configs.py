@@ -7,7 +7,7 @@ shflbw_cu_last_plan), against the oracle.
     test_gpu_parity.py's full-size digest cases (16384 x 4096 V=64, 8192 x
     2048 V=32, 8192 x 1024 V=128, pinned to the compiled reference) plus a
     non-conformant M = 8192 mask, planner-vs-sort-pipeline equality and an M
-    = 32768 case here;
+    = 40960 case here;
   * the large-FFN SpMM (16384 x 4096, N = 8192, 75 %) run at full size with
     the auto plan (persistent kernel), column slices checked against
     oracle.spmm (spmm_execute, src/spmm.cpp:76-146) -- output columns are
@@ -261,6 +261,7 @@ def _packing(a):
 @pytest.mark.parametrize("M,K,V,cpg", [(2048, 2048, 64, 512),    # one-CTA planner (CTA sort)
                                        (8192, 1024, 32, 256),    # chunked ranks
                                        (16384, 512, 64, 128),
+                                       (32768, 128, 64, 32),     # 32 chunks
                                        (6144, 100, 3, 40),       # V not a power of two, K % 16 != 0
                                        (4096, 64, 1, 20),        # V = 1: G = M
                                        (8192, 64, 1, 20)])
@@ -285,10 +286,10 @@ def test_compress_planner_equals_sort_pipeline(sb, oracle, M, K, V, cpg):
     assert np.array_equal(vals.view(np.uint32), oracle.round16(p.values).view(np.uint32))
 
 
-def test_compress_beyond_planner_m32768(sb, oracle):
-    """M = 32768 > the planner's shared-memory bound: the sort-based
-    pipeline, bit-exact against the oracle."""
-    M, K, V = 32768, 128, 64
+def test_compress_beyond_planner_m40960(sb, oracle):
+    """M = 40960 > the planner's bound (16-bit row ids, 32 chunks): the
+    sort-based pipeline, bit-exact against the oracle."""
+    M, K, V = 40960, 128, 64
     mask = oracle.random_shflbw_mask(M, K, V, 40, oracle.rng(11))
     W = oracle.round16(oracle.random_dense(M, K, 6))
     a = sb.compress_shflbw(dev(W), dev(mask), V)
