@@ -1126,12 +1126,12 @@ def test_compress_async_equals_sync(sb, oracle, M, K, V, alpha):
     assert np.array_equal(sb.spmm_execute(a, Bd).cpu().numpy(), sb.spmm_execute(a_sync, Bd).cpu().numpy())
 
 
-def test_compress_async_reports_errors(sb, oracle):
+@pytest.mark.parametrize("M,K,V", [(512, 96, 8), (8192, 128, 32)])  # one-CTA planner, chunked planner
+def test_compress_async_reports_errors(sb, oracle, M, K, V):
     """Non-conformant masks and mask bytes > 1 are reported through the
     device status and raised by finalize (the reference's classes and
     fail_row)."""
-    M, K, V = 512, 96, 8
-    mask = oracle.random_shflbw_mask(M, K, V, 24, oracle.rng(5))
+    mask = oracle.random_shflbw_mask(M, K, V, K // 4, oracle.rng(5))
     mask[7, 3] ^= 1
     want = oracle.validate(mask, V)
     a, status = sb.compress_shflbw_async(torch.zeros(M, K, device="cuda"), dev(mask), V)
