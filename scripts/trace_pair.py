@@ -31,6 +31,8 @@ trA = torch.zeros(1 << 20, dtype=torch.int64, device=dev)
 trB = torch.zeros(1 << 20, dtype=torch.int64, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 names = ["entry", "setup", "dep_wait", "first_full", "last_mma", "accum", "epi_done", "exit"]
+extra = {24: "partial_ok", 25: "recv_ok", 26: "sum_done", 27: "tile_bar", 28: "stores_issued",
+         16: "issue[0]", 8: "full[0]", 9: "full[1]", 10: "full[2]", 11: "full[3]"}
 # the chain is captured in a CUDA graph so the launches run back to back (an
 # eager Python loop issues one launch per ~10 us: every launch ran isolated)
 s = torch.cuda.Stream()
@@ -56,8 +58,10 @@ a = a[a[:, 0] > 0]
 b = b[b[:, 0] > 0]
 t0 = a[:, 0].min()
 print(f"{args.workload} {args.opts}: predecessor {len(a)} CTAs, successor {len(b)} CTAs (us after the predecessor's first entry)")
-for nm, e in zip(names, range(8)):
+for nm, e in list(zip(names, range(8))) + [(v, k) for k, v in sorted(extra.items())]:
     ca, cb = (a[:, e] - t0) / 1e3, (b[:, e] - t0) / 1e3
     ca, cb = ca[a[:, e] > 0], cb[b[:, e] > 0]
+    if not len(ca) or not len(cb):
+        continue
     print(f"  {nm:10s} pred min {ca.min():6.2f} p50 {np.median(ca):6.2f} max {ca.max():6.2f} | "
           f"succ min {cb.min():6.2f} p50 {np.median(cb):6.2f} max {cb.max():6.2f}")
