@@ -199,9 +199,29 @@ def test_baseline_spmm_configs_auto_plan(sb, oracle, M, N, K, V, alpha):
     Bd = dev(B, torch.bfloat16)
     got = sb.spmm_execute(a, Bd).cpu().numpy()
     plan = tc_plan(sb)
-    assert oracle.rel_frobenius(got, oracle.spmm(p, B)) <= TOL, plan
+    ref = oracle.spmm(p, B)
+    assert oracle.rel_frobenius(got, ref) <= TOL, plan
     got16 = sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16).float().cpu().numpy()
     assert np.array_equal(got16, oracle.round16(got)), plan
+    # the error against a float64 recomputation separates the CPU
+    # fp32 error from the tensor core's; the bf16-out mode is within one bf16
+    # ulp of the oracle per element
+    c64 = (W.astype(np.float64) * mask) @ B.astype(np.float64)
+    e_gpu, e_ref = oracle.rel_frobenius(got, c64), oracle.rel_frobenius(ref, c64)
+    print(f"{plan}: rel err vs f64 -- GPU fp32 {e_gpu:.2e}, CPU oracle fp32 {e_ref:.2e}")
+    assert e_gpu <= TOL and e_ref <= TOL
+    # (elements whose magnitude is far below the typical one are results of
+    # cancellation: there the fp32 accumulation-order error of either side
+    # exceeds a bf16 ulp of the tiny result, so they are excluded from the
+    # per-element check -- the fp32 relative-Frobenius bound above covers them)
+    r16 = oracle.round16(ref).astype(np.float64)
+    mag = np.maximum(np.abs(r16), np.abs(got16.astype(np.float64)))
+    ulp = np.where(mag > 0, 2.0 ** (np.floor(np.log2(np.where(mag > 0, mag, 1.0))) - 7), 0.0)
+    ok = np.abs(got16 - r16) <= ulp
+    big = np.abs(ref) >= 2.0 ** -6 * np.sqrt(np.mean(ref.astype(np.float64) ** 2))
+    print(f"  bf16 out within 1 ulp of the oracle: {ok.mean() * 100:.3f} % of all elements, "
+          f"{ok[big].mean() * 100:.3f} % of those >= rms/64")
+    assert np.all(ok[big]), plan
 
 
 # ---------------------------------------------------------------- ResNet-50 convs
