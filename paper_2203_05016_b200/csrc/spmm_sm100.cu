@@ -200,7 +200,10 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
                     r.cs = 4;
                 } else if (fit4 && V >= 64) {
                     r.mode = 2;
-                } else if (fit2) {
+                } else if (fit2 && V < 64) {
+                    // a K split by 2 only for 32-row groups: with 64 rows the
+                    // multicast V split (32 rows per CTA) is faster (GNMT 50 %:
+                    // 4.45 vs 4.57-5.24 us cold, 4.19 vs 4.73 warm)
                     r.mode = 1;
                     r.cs = 2;
                 }
