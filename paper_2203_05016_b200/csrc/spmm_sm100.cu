@@ -429,11 +429,12 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         // gather warps per CTA ("gather_warps", 0 = auto): an SM's gather rate
         // grows with the warps issuing (scripts/fillbench2.cu)
         const int64_t gwo = option("gather_warps");
-        // auto: 8 for units of >= 5 K blocks without a K split (measured
-        // 2-7 % faster: large FFN, FFN2 N=4096, ResNet 3x3 @28/@14) and for
+        // auto: 8 for units of >= 5 K blocks of >= 64 rows without a K split
+        // (measured 2-7 % faster: large FFN, FFN2 N=4096, ResNet 3x3 @28/@14;
+        // with 32 rows, FFN2 N=4096 V=32, 4 warps: 9.76 -> 9.50 us) and for
         // SpMM K splits of <= 32 V rows per CTA (north star 3.63 -> 3.60 us,
         // V = 32 3.74 -> 3.67; with 64 rows, GNMT 50 %, 4.57 -> 4.63: 4)
-        const bool gw8 = (!prm.ksplit && kb_grp >= 5) || (prm.ksplit && vs <= 32 && b.kind == 0);
+        const bool gw8 = (!prm.ksplit && kb_grp >= 5 && vs >= 64) || (prm.ksplit && vs <= 32 && b.kind == 0);
         prm.gw = gwo > 0 ? static_cast<int>(gwo) : (gw8 ? 8 : 4);
         if (prm.gw != 4 && prm.gw != 8) return fail(SHFLBW_BAD_PARAMS, "gather_warps must be 4 or 8");
     }
