@@ -413,6 +413,12 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         stages = 2;
     } else if (stages <= 0) {
         stages = vs >= 128 ? 3 : 4;
+        // 128-row units that fit one CTA per SM (no co-resident pair to keep):
+        // a 6-deep ring -- twice the three 32 KB stages in flight (FFN2
+        // N=4096 V=128: 7.77 -> 6.60 us).  Shorter kernels keep the
+        // two-per-SM footprint that lets the PDL successor co-reside
+        // (north star V=128, K split: 4 stages 4.12 -> 4.95 us).
+        if (vs >= 128 && cs == 1 && !prm.ksplit && units <= num_sms() && kb_grp >= 8) stages = 6;
     }
     if (!prm.persistent && prm.ksplit && option("stages") <= 0) {
         // keep two CTAs per SM next to the DSMEM receive buffer

@@ -38,6 +38,9 @@ cases = {
     "conv7": lambda: sweep.conv_row("conv7", 512, 7, 512, 3, 1, 32, 64, 0.25, 300, dev),
     "c1x1_56": lambda: sweep.conv_row("c1x1_56", 256, 56, 64, 1, 0, 32, 64, 0.25, 300, dev),
     "c1x1_14": lambda: sweep.conv_row("c1x1_14", 1024, 14, 256, 1, 0, 32, 64, 0.25, 300, dev),
+    "attn4096": lambda: sweep.spmm_row("attn4096", 512, 4096, 512, 64, 0.25, 1000, dev),
+    "ffn1_90": lambda: sweep.spmm_row("ffn1_90", 2048, 4096, 512, 64, 0.1, 1000, dev),
+    "ffn2_v128": lambda: sweep.spmm_row("ffn2_v128", 512, 4096, 2048, 128, 0.25, 1000, dev),
 }
 out = {}
 for k in only:
