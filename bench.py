@@ -890,17 +890,22 @@ def main():
         for st in streams:
             s_cap.wait_stream(st)
     reps_e2e = max(1, e2e_steps // per)
+    # three windows, the median reported: the PCIe link is shared with the
+    # host (the same 512 KB H2D read 34 GB/s or 19.6 GB/s on different runs)
+    windows = []
     with torch.cuda.stream(s_cap):
         g_e2e.replay()
         torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s_cap)
-        for _ in range(reps_e2e):
-            g_e2e.replay()
-        e1.record(s_cap)
-        torch.cuda.synchronize()
-    ems = max_over_ranks(torch, dist, e0.elapsed_time(e1)) / (reps_e2e * per)
+        for _ in range(3):
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s_cap)
+            for _ in range(reps_e2e):
+                g_e2e.replay()
+            e1.record(s_cap)
+            torch.cuda.synchronize()
+            windows.append(max_over_ranks(torch, dist, e0.elapsed_time(e1)) / (reps_e2e * per))
+    ems = sorted(windows)[1]
     e2e = {"value": total_flops / (ems * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ems,
            "h2d_bytes_per_step": nb_b, "d2h_bytes_per_step": nb_c, "steps": reps_e2e * per,
            "path": ("C ABI shflbw_cu_spmm (ctypes) with cudaMemcpyAsync (cuda-python) of pinned host B/C: "
@@ -908,7 +913,8 @@ def main():
                     f"({per} steps per graph)"),
            "eager": {"value": total_flops / (eager_ms * 1e-3) / 1e12, "ms_per_step": eager_ms, "steps": e2e_steps,
                      "path": "the same calls issued from Python every step"},
-           "host_buffers_numa_node": numa.node}
+           "host_buffers_numa_node": numa.node,
+           "windows_ms_per_step": windows}
     del Bh, Ch, Bd, Cdv
 
     # ---- roofline of the dominant kernel (the SpMM, one launch per step) ---
