@@ -500,6 +500,7 @@ class RotatingSets:
         self.n = n
         self.mats, self.Bs, self.Cs = [], [], []
         self.compress_ms = None
+        self.compress_graph_ms = None
         for s in range(n):
             W = uniform16(torch, (M, K), 100 + s, dev)
             if s == 0 and not profile:
@@ -514,6 +515,32 @@ class RotatingSets:
                     ts.append((time.perf_counter() - t) * 1e3)
                     del tmp
                 self.compress_ms = sorted(ts[1:])[2]
+                # the asynchronous converter as a CUDA-graph replay (the
+                # in-model use: no host synchronisation), device time per call
+                try:
+                    a_m, st = sb.compress_shflbw_async(W, mask, V, dtype=dtype)
+                    cs = torch.cuda.Stream()
+                    cs.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(cs):
+                        sb.compress_shflbw_async(W, mask, V, dtype=dtype, out=a_m, status=st)
+                    torch.cuda.synchronize()
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=cs):
+                        sb.compress_shflbw_async(W, mask, V, dtype=dtype, out=a_m, status=st)
+                    with torch.cuda.stream(cs):
+                        for _ in range(3):
+                            g.replay()
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(cs)
+                        for _ in range(20):
+                            g.replay()
+                        e1.record(cs)
+                    torch.cuda.synchronize()
+                    sb.finalize(a_m, st)
+                    self.compress_graph_ms = e0.elapsed_time(e1) / 20
+                    del g, a_m, st
+                except Exception as e:  # noqa: BLE001
+                    self.compress_graph_ms = f"unavailable: {type(e).__name__}"
             self.mats.append(sb.compress_shflbw(W, mask, V, dtype=dtype))
             self.Bs.append(uniform16(torch, (K, N), 200 + s, dev, dtype))
             self.Cs.append(torch.empty((out_rows or M, N), dtype=dtype, device=dev))
@@ -948,7 +975,7 @@ def main():
 
     # ---- the sharded large-FFN layer (north_star's 1/2/4/8-GPU shape) ------
     shard = None
-    set_bytes, compress_ms = rot.set_bytes, rot.compress_ms
+    set_bytes, compress_ms, compress_graph_ms = rot.set_bytes, rot.compress_ms, rot.compress_graph_ms
     if not args.no_sharded and args.workload != "lf":
         del rot, mats, Bs, Cs
         torch.cuda.empty_cache()
@@ -972,7 +999,7 @@ def main():
             "speedup_vs_cublas": (value / world / cub["tflops"]) if cub else None,
             "speedup_vs_cublaslt_best": (value / world / lt["tflops"]) if lt and "tflops" in lt else None,
             "cublas": cub, "cublaslt_best": lt, "no_pdl": no_pdl, "fp32_out": f32, "fp16": f16,
-            "tensor_pipe_util_pct": util, "compress_ms": compress_ms, "roofline": roof, "cpu_baseline": cpu,
+            "tensor_pipe_util_pct": util, "compress_ms": compress_ms, "compress_graph_ms": compress_graph_ms, "roofline": roof, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
             "sharded_lf": shard,
