@@ -1489,17 +1489,32 @@ __global__ void __launch_bounds__(256, 8) k_pack_group(const void* __restrict__ 
     const bool live = jj < nvalid;
     const int col = live ? cols_s[jj] : 0;
     for (int v0 = 0; v0 < V; v0 += 32) {
-        float x[8];
+        if constexpr (DT == DIN) {  // same type: the values move as raw bits (no convert pair)
+            T x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int v = v0 + 4 * u + vq;
-            x[u] = 0.0f;
-            if (live && v < V) x[u] = Elem<DIN>::to_f(src[static_cast<int64_t>(rows_s[v]) * K + col]);
-        }
+            for (int u = 0; u < 8; ++u) {
+                const int v = v0 + 4 * u + vq;
+                x[u] = Elem<DT>::from_f(0.0f);
+                if (live && v < V) x[u] = src[static_cast<int64_t>(rows_s[v]) * K + col];
+            }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int v = v0 + 4 * u + vq;
-            if (v < V) stage[jj * SV + v] = Elem<DT>::from_f(x[u]);
+            for (int u = 0; u < 8; ++u) {
+                const int v = v0 + 4 * u + vq;
+                if (v < V) stage[jj * SV + v] = x[u];
+            }
+        } else {
+            float x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int v = v0 + 4 * u + vq;
+                x[u] = 0.0f;
+                if (live && v < V) x[u] = Elem<DIN>::to_f(src[static_cast<int64_t>(rows_s[v]) * K + col]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int v = v0 + 4 * u + vq;
+                if (v < V) stage[jj * SV + v] = Elem<DT>::from_f(x[u]);
+            }
         }
     }
     __syncthreads();
