@@ -135,15 +135,25 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep"))
     ap.add_argument("--only", default="")
+    ap.add_argument("--grid", default="", help="'transformer': BASELINE configs[1] in full -- (M, K) in "
+                    "{512x512, 2048x512, 512x2048} x N in {128, 512, 1024, 4096} x 50/75/90 % x V in {32, 64, 128}")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     rows = []
-    for cfg in SPMM:
+    spmm_cfgs, conv_cfgs = SPMM, CONV
+    if args.grid == "transformer":
+        spmm_cfgs, conv_cfgs = [], []
+        for nm, M, K in (("attn proj", 512, 512), ("FFN1", 2048, 512), ("FFN2", 512, 2048)):
+            for N in (128, 512, 1024, 4096):
+                for alpha in (0.5, 0.25, 0.1):
+                    for V in (32, 64, 128):
+                        spmm_cfgs.append((f"{nm} {M}x{K} N={N} {round((1 - alpha) * 100)}% V={V}", M, N, K, V, alpha))
+    for cfg in spmm_cfgs:
         if args.only and args.only not in cfg[0]:
             continue
         rows.append(spmm_row(*cfg, args.steps if cfg[1] * cfg[2] < 1 << 26 else 20, dev))
         print(json.dumps(rows[-1]), flush=True)
-    for cfg in CONV:
+    for cfg in conv_cfgs:
         if args.only and args.only not in cfg[0]:
             continue
         rows.append(conv_row(*cfg, args.steps, dev))
