@@ -418,14 +418,25 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         stages = 2;
     } else if (stages <= 0) {
         stages = vs >= 128 ? 3 : 4;
-        // 128-row units that fit one CTA per SM (no co-resident pair to keep):
-        // a 6-deep ring -- twice the three 32 KB stages in flight (FFN2
-        // N=4096 V=128: 7.77 -> 6.60 us).  Shorter kernels keep the
-        // two-per-SM footprint that lets the PDL successor co-reside
-        // (north star V=128, K split: 4 stages 4.12 -> 4.95 us).
-        if (vs >= 128 && cs == 1 && !prm.ksplit && units <= num_sms() && kb_grp >= 8) stages = 6;
     }
-    if (!prm.persistent && prm.ksplit && option("stages") <= 0) {
+    // Unclustered grids of at most one CTA per SM: no co-resident pair to
+    // keep room for, so the ring goes as deep as the units are (<= 6 stages,
+    // one CTA's shared memory): FFN2 N=4096 V=128 7.77 -> 6.60 us, FFN1
+    // N=1024 50 % V=128 5.46 -> 4.98, FFN2 N=1024 75 % V=32 5.37 -> 4.95.
+    // Cluster splits keep the two-per-SM footprint: measured both ways over
+    // the transformer grid (`--grid transformer`), deeper rings there won on
+    // some shapes and lost 10-14 % on others (GNMT 50 % 4.51 -> 5.13 us).
+    const int kb_cta = (kb_grp + ksf - 1) / ksf;
+    const bool deep_ring = !prm.persistent && option("stages") <= 0 && units * cs <= num_sms() && cs == 1 &&
+                           !prm.ksplit;
+    if (deep_ring) {
+        const int64_t recv = prm.ksplit ? static_cast<int64_t>(vs / ksf) * (ksf - 1) * kBlockN * 4 : 0;
+        const int64_t fixed = recv + 2048 + kMetaBlocks * kBlockK * 4 + 4 * vs + 256;
+        const int64_t stage = kABytes + static_cast<int64_t>(kBlockK) * vs * 2;
+        const int fit1 = static_cast<int>((232448 - fixed) / stage);
+        const int deep = std::min(std::min(6, fit1), kb_cta);
+        if (deep > stages) stages = deep;
+    } else if (!prm.persistent && prm.ksplit && option("stages") <= 0) {
         // keep two CTAs per SM next to the DSMEM receive buffer
         const int64_t ksf_rows = vs / ksf * (ksf - 1);
         const int64_t fixed = ksf_rows * kBlockN * 4 + 1024 + kMetaBlocks * kBlockK * 4 + 4 * vs + 256;
