@@ -193,20 +193,29 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         Split r{static_cast<int>(option("split")), mode_opt, false, false};
         if (r.mode == 0) {
             r.mode = 3;
-            if (r.cs <= 0 && b.kind == 0 && kb_grp >= 8) {
+            if (r.cs <= 0 && b.kind == 0 && kb_grp >= 4 && kb_grp < 8 && units * 4 <= num_sms() && V <= 64) {
+                // shallow groups on a small grid: 2 x 2 (attention projection
+                // N=128 50 %: V=32 2.75 -> 2.42 us, V=64 2.70 -> 2.49)
+                r.mode = 2;
+            } else if (r.cs <= 0 && b.kind == 0 && kb_grp >= 8) {
                 const bool fit4 = units * 4 <= num_sms(), fit2 = units * 2 <= num_sms();
                 const bool fit2x2 = units * 2 <= 2LL * num_sms();  // two CTAs per SM
                 if (fit4 && kb_grp >= 24) {
                     r.mode = 1;
                     r.cs = 4;
-                } else if (fit4 && V >= 64) {
+                } else if (fit4 && V >= 64 && (V < 128 || kb_grp >= 16)) {
+                    // (128-row groups of < 16 K blocks: the V split by 4, 32
+                    // rows per CTA, is faster: FFN2 N=1024 75 % 5.04 -> 4.53
+                    // us, north star V=128 4.08 -> 4.01; deeper ones keep the
+                    // 2 x 2: FFN2 N=128 50 % 5.05 vs 5.77)
                     r.mode = 2;
-                } else if ((fit2 && (V < 64 || kb_grp >= 16)) || (!fit2 && fit2x2 && kb_grp >= 16 && V <= 64)) {
+                } else if (V <= 64 && ((fit2 && (V < 64 || kb_grp >= 16)) || (!fit2 && fit2x2 && kb_grp >= 16))) {
                     // a K split by 2 for 32-row groups and for deep groups
                     // (>= 16 K blocks, also at two CTAs per SM up to 64 rows:
                     // FFN2 N=1024 50 % V=32 8.07 -> 6.90 us, V=64 7.03 ->
                     // 6.69; at V = 128 the receive buffer costs the second
-                    // CTA: FFN2 N=4096 50 % 9.06 -> 18.3); with 64 rows and
+                    // CTA: FFN2 N=4096 50 % 9.06 -> 18.3, N=128 5.05 -> 7.16;
+                    // 128-row groups take the V split); with 64 rows and
                     // shallower groups the multicast V split is faster
                     // (GNMT 50 %: 4.45 vs 4.57-5.24 us)
                     r.mode = 1;

@@ -953,14 +953,27 @@ def test_spmm_groups_peers_fused_allgather(sb, oracle, M, N, K, V, alpha, persis
     sb.set_option("split_mode", mode)
     try:
         want = sb.spmm_execute(a, Bd, out_dtype=torch.bfloat16)
+        full_plan = sb.last_plan()
         outs = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda") for _ in range(world)]
         G = a.group_count()
+        same = True
         for rank in range(world):
             g0, g1 = G * rank // world, G * (rank + 1) // world
             sb.spmm_groups_peers(a, g0, g1, Bd, outs[rank:] + outs[:rank])  # own buffer first
+            # the auto plan of a shard's smaller grid may pick another cluster
+            # split than the full grid (a K split sums in another order)
+            same &= sb.last_plan().split(" groups=")[0] == full_plan.split(" groups=")[0]
         torch.cuda.synchronize()
         for o in outs:
-            assert torch.equal(o, want)
+            if same:
+                assert torch.equal(o, want)
+            else:  # within one bf16 ulp of the single-GPU result (cancellation
+                # results, far below the typical magnitude, within one ulp of rms/64)
+                w = want.float()
+                mag = torch.maximum(w.abs(), w.pow(2).mean().sqrt() / 64)
+                ulp = 2.0 ** (torch.floor(torch.log2(mag)) - 7)
+                assert not torch.isnan(o.float()).any()
+                assert bool(((o.float() - w).abs() <= ulp).all())
     finally:
         for k in ("persistent", "split", "split_mode"):
             sb.set_option(k, 0)
