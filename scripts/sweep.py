@@ -141,6 +141,15 @@ def main():
     dev = torch.device("cuda", 0)
     rows = []
     spmm_cfgs, conv_cfgs = SPMM, CONV
+    if args.grid == "resnet":  # every stride-1 ResNet-50 bottleneck conv, batch 32, 75 %
+        spmm_cfgs = []
+        conv_cfgs = []
+        for stage, (Cin, mid, Cout, H) in enumerate(((256, 64, 256, 56), (512, 128, 512, 28),
+                                                      (1024, 256, 1024, 14), (2048, 512, 2048, 7))):
+            conv_cfgs += [(f"ResNet 1x1 {Cin}->{mid} @{H}", Cin, H, mid, 1, 0, 32, 64, 0.25),
+                          (f"ResNet 3x3 {mid}->{mid} @{H}", mid, H, mid, 3, 1, 32, 64, 0.25),
+                          (f"ResNet 1x1 {mid}->{Cout} @{H}", mid, H, Cout, 1, 0, 32, 64, 0.25)]
+        conv_cfgs.insert(0, ("ResNet 1x1 64->64 @56", 64, 56, 64, 1, 0, 32, 64, 0.25))
     if args.grid == "transformer":
         spmm_cfgs, conv_cfgs = [], []
         for nm, M, K in (("attn proj", 512, 512), ("FFN1", 2048, 512), ("FFN2", 512, 2048)):
