@@ -44,6 +44,11 @@ cases = {
 }
 out = {}
 for k in only:
+    if k.startswith("c_"):  # ad-hoc 1x1 conv, batch 32, 75 %: c_Cin_H_Cout
+        C_, H_, F_ = (int(x) for x in k[2:].split("_"))
+        r = sweep.conv_row(k, C_, H_, F_, 1, 0, 32, 64, 0.25, 300, dev)
+        out[k] = (round(r["us"], 2), round(r["dense_us"], 2))
+        continue
     if k.startswith("s_"):  # ad-hoc SpMM: s_M_N_K_V_alpha
         M_, N_, K_, V_, a_ = k[2:].split("_")
         r = sweep.spmm_row(k, int(M_), int(N_), int(K_), int(V_), float(a_), 1000, dev)
