@@ -399,9 +399,18 @@ int spmm_tc(const shflbw_cu_matrix* a, int g_begin, int g_end, const Operand& b,
         // ResNet 3x3 @28, 392 units, 12.4 -> 11.8 us; below that the one-CTA-
         // per-unit kernel wins: FFN2 N=4096 256 units 7.4 vs 8.3 us)
         int64_t opt = option("persistent");
-        if (opt == 0) opt = (units * cs > 2LL * num_sms()) ? 2 : -1;
+        // auto, many shallow SpMM units (<= 4 K blocks, <= 64 rows,
+        // unclustered, >= 4 units per SM): 3 CTAs per SM (the 4-gather-warp
+        // instantiation for 64 registers per thread) -- more epilogues in
+        // flight for these epilogue-bound grids: ResNet 1x1 64->256 @56 18.4
+        // -> 17.5 us, 128->512 @28 10.8 -> 10.0, FFN1 N=4096 75 % 8.72 ->
+        // 8.33, 90 % 8.07 -> 7.52.  With fewer units (about one per slot:
+        // 1x1 512->128 @28, +6 %) or the conv producers (3x3 @56, +4 %) the
+        // two-per-SM kernel stays ahead.
+        const bool three = cs == 1 && kb_grp <= 4 && vs <= 64 && b.kind == 0 && units >= 4LL * num_sms();
+        if (opt == 0) opt = (units * cs > 2LL * num_sms()) ? (three ? 3 : 2) : -1;
         prm.persistent = !prm.ksplit && opt > 0 && groups <= 4096 && tile_n == kBlockN ? 1 : 0;
-        prm.per_sm = static_cast<int>(std::min<int64_t>(2, std::max<int64_t>(1, opt)));  // launch bounds: 2
+        prm.per_sm = static_cast<int>(std::min<int64_t>(3, std::max<int64_t>(1, opt)));  // launch bounds: 3 (GW = 4) / 2
     }
     int stages = static_cast<int>(option("stages"));
     if (prm.persistent) {

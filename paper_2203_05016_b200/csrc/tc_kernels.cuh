@@ -998,8 +998,8 @@ __device__ __forceinline__ void persist_store(const TcParams& p, uint32_t t_acc,
     }
 }
 
-template <int DT, int VS, int CS, int KIND, int GW>
-__global__ void __launch_bounds__(192 + 32 * GW, 2)
+template <int DT, int VS, int CS, int KIND, int GW, int MINB = 2>
+__global__ void __launch_bounds__(192 + 32 * GW, MINB)
     k_spmm_persist(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmW,
                    const __grid_constant__ CUtensorMap tmBt, TcParams p,
                    int units, int n_tiles) {
@@ -1369,7 +1369,7 @@ int launch_tc(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap&
 }
 
 
-template <int DT, int VS, int CS, int KIND, int GW>
+template <int DT, int VS, int CS, int KIND, int GW, int MINB = 2>
 int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles, int groups,
                    cudaStream_t s) {
     constexpr int kStage = kABytes + WeightLayout<VS>::kBytes;
@@ -1380,7 +1380,7 @@ int launch_persist(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtenso
                                       : 0) + 1024 +
                         2 * kMetaBlocks * kBlockK * 4 + (VS < 4 ? 4 : VS) * 4 + ((groups + 2) & ~1) * 4 +
                         (2 * prm.stages + 5) * 8 + 16;
-    auto kern = k_spmm_persist<DT, VS, CS, KIND, GW>;
+    auto kern = k_spmm_persist<DT, VS, CS, KIND, GW, MINB>;
     static SmemCaps configured;
     if (const int dev = current_device(); configured.needs(dev, smem)) {
         SBW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1426,6 +1426,11 @@ template <int DT, int VS, int CS, int KIND>
 int launch_persist_gw(const CUtensorMap& tmB, const CUtensorMap& tmW, const CUtensorMap& tmBt, const TcParams& prm, int n_tiles, int groups,
                       cudaStream_t s) {
     if (prm.gw >= 8) return launch_persist<DT, VS, CS, KIND, 8>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
+    // three CTAs per SM (shallow units, epilogue-bound): the instantiation
+    // compiled for that register budget (64 per thread; the two-per-SM one
+    // keeps 72, which the other shapes need)
+    if constexpr (CS == 1)
+        if (prm.per_sm >= 3) return launch_persist<DT, VS, CS, KIND, 4, 3>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
     return launch_persist<DT, VS, CS, KIND, 4>(tmB, tmW, tmBt, prm, n_tiles, groups, s);
 }
 
