@@ -1224,3 +1224,24 @@ def test_blockwise_tile_loads_bitwise(sb, oracle, M, N, K, keep, persistent):
     t = 0 if persistent != -1 else 1
     assert np.array_equal(outs[t][0], outs[-1][0]) and np.array_equal(outs[t][1], outs[-1][1])
     assert oracle.rel_frobenius(outs[t][0][:, :128], oracle.spmm(p, np.ascontiguousarray(B[:, :128]))) <= TOL
+
+
+def test_persistent_three_per_sm_bitwise(sb, oracle):
+    """Many shallow units (FFN1 2048x512, N = 4096): the auto plan runs the
+    persistent kernel 3 CTAs per SM (its 64-register instantiation); the
+    same units at 2 per SM and on the one-CTA-per-unit kernel give the same
+    bits."""
+    M, K, N, V = 2048, 512, 4096, 64
+    mask, W, B = synthetic(oracle, M, K, N, V, 0.25)
+    a, p = compress_both(sb, oracle, W, mask, V)
+    Bd = dev(B, torch.bfloat16)
+    got3 = sb.spmm_execute(a, Bd).cpu().numpy()
+    assert "per_sm=3" in sb.last_plan(), sb.last_plan()
+    outs = []
+    for opt in (2, -1):
+        sb.set_option("persistent", opt)
+        outs.append(sb.spmm_execute(a, Bd).cpu().numpy())
+    sb.set_option("persistent", 0)
+    for o in outs:
+        assert np.array_equal(o, got3)
+    assert oracle.rel_frobenius(got3[:, :256], oracle.spmm(p, np.ascontiguousarray(B[:, :256]))) <= TOL
